@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark: decoded encoder frames/s of the B200 RNN-T greedy decoder.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2|c3|c4|c5|c1] [--exec graph|persistent]
+
+A "step" is one decode of one batch through the captured program (K1 encoder
+projection + the device-resident decode loops).  Default workload (N=1) is
+BASELINE.json configs[1] (C2): Parakeet-RNNT-1.1B-shaped decoder -- encoder
+dim 1024, 2-layer LSTM 640, joint 640, V=1025 (1024 + blank), B=32, T=250,
+frame-looping, max_symbols=5, fp32, random-init weights (Rng(1)) and synthetic
+encoder outputs (Rng(2)).  Under torchrun each rank decodes its own B=32 batch
+(weak scaling, no collective on the data path: utterances are independent);
+--config c5 splits B=256, T=500 across ranks (strong scaling).
+
+Timing: W untimed warm-up decodes, then K decodes each bracketed by CUDA
+events on the decoder stream, with L2 flushed (256 MiB write) before every
+timed decode; barrier + synchronize around the timed region; max over ranks.
+`e2e` repeats the measurement through the C ABI with host buffers: pinned
+host -> device copy of x and out_len, graph launch, device -> host read of
+the emissions, all inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (algo, B, T, ms, durations, layers, hidden, joint, vocab, feature, scaling)
+    "c1": ("fs", 4, 200, 5, (), 1, 320, 320, 128, 256, "weak"),
+    "c2": ("fs", 32, 250, 5, (), 2, 640, 640, 1024, 1024, "weak"),
+    "c3": ("ll", 32, 250, 10, (), 2, 640, 640, 1024, 1024, "weak"),
+    "c4": ("tdt", 32, 250, 10, (0, 1, 2, 3, 4), 2, 640, 640, 1024, 1024, "weak"),
+    "c5": ("fs", 256, 500, 5, (), 2, 640, 640, 1024, 1024, "strong"),
+}
+ALGO_ID = {"fs": 0, "ll": 1, "tdt": 2}
+ALGO_NAME = {"fs": "frame-looping", "ll": "label-looping", "tdt": "TDT label-looping"}
+METRIC = "decoded encoder frames/sec (Parakeet-1.1B dec, B=32); GPU idle %; µs/step"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--exec", default="graph", choices=["graph", "persistent"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--blank-bias", type=float, default=0.0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="target duration of the bounded CPU reference sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def shard(cfg, rank, world):
+    algo, B, T, ms, durs, L, H, J, V, F, scaling = cfg
+    if scaling == "strong":
+        b0, b1 = B * rank // world, B * (rank + 1) // world
+    else:
+        b0, b1 = B * rank, B * (rank + 1)
+    return b0, b1
+
+
+def make_inputs(cfg, b0, b1):
+    from paper_2406_03791_b200 import synth
+    algo, B, T, ms, durs, L, H, J, V, F, scaling = cfg
+    n = (b1 - b0) * T * F
+    x = synth.uniform(2, n, -1.0, 1.0, start=b0 * T * F).reshape(b1 - b0, T, F)
+    lens = np.full(b1 - b0, T, np.int32)
+    return x, lens
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self.proc = None
+        self.th = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        if self.th:
+            self.th.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for i, n in enumerate(names):
+                if s[4 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def cpu_reference_sample(cfg, seconds_target, threads=None):
+    """The reference's own decoders (oracle/_ref: rnnt-sim compiled from its
+    sources + the LstmModel extension) on a bounded sample of the workload."""
+    from oracle import oracle as O
+    algo, B, T, ms, durs, L, H, J, V, F, scaling = cfg
+    d = O.Dims(V, H, H, J, F, durs, O.CELL_LSTM, L)
+    p = O.init_params(1, d)
+    m = O.RefModel(d, p)
+    nproc = os.cpu_count() or 1
+    threads = threads or min(nproc, B)
+    ref_algo = {"fs": "sync_free", "ll": "label_loop", "tdt": "tdt"}[algo]
+    Bs = threads  # one utterance per thread
+    # calibrate on 2 frames, then size the sample to ~seconds_target
+    x, lens = make_inputs(cfg, 0, Bs)
+    Ts = 2
+    _, secs = m.decode(ref_algo, np.ascontiguousarray(x[:, :Ts]), np.full(Bs, Ts, np.int32), ms,
+                       threads)
+    Ts = int(max(2, min(T, Ts * seconds_target / max(secs, 1e-3))))
+    _, secs = m.decode(ref_algo, np.ascontiguousarray(x[:, :Ts]), np.full(Bs, Ts, np.int32), ms,
+                       threads)
+    frames = Bs * Ts
+    return {"value": frames / secs, "unit": "frames/s", "cores": threads, "kind": "reference",
+            "sample": f"{Bs} utterances x {Ts} frames of {ALGO_NAME[algo]} (ms={ms}), "
+                      f"reference rnnt-sim decoders + LstmModel, {threads} threads of {nproc}",
+            "seconds": secs}
+
+
+def run_reference_arm(args, cfg, rank, world):
+    if rank != 0:
+        return
+    algo, B, T, ms, durs, L, H, J, V, F, scaling = cfg
+    secs_per_step = max(2.0, min(20.0, 150.0 / max(args.steps + args.warmup, 1)))
+    vals = []
+    base = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference_sample(cfg, secs_per_step)
+        if i >= args.warmup:
+            vals.append(r["value"])
+        base = r
+    v = float(np.mean(vals)) if vals else base["value"]
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "frames/s",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1000.0 * B * T / v, "higher_is_better": True,
+           "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": config_json(args, cfg),
+           "cpu_baseline": {k: base[k] for k in ("kind", "cores", "sample")} | {"value": v,
+                                                                                "unit": "frames/s"},
+           "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def config_json(args, cfg):
+    algo, B, T, ms, durs, L, H, J, V, F, scaling = cfg
+    return {"workload": f"{args.config}: Parakeet-1.1B-shaped {ALGO_NAME[algo]} decode "
+                        f"(enc {F}, {L}-layer LSTM {H}, joint {J}, V={V + 1}"
+                        f"{', durations ' + str(list(durs)) if durs else ''})",
+            "batch": B, "frames": T, "max_symbols": ms, "algo": algo, "exec": args.exec,
+            "sharding": f"{scaling}: utterances split across {args.gpus} GPU(s), no collective",
+            "weights": "random init Rng(1) U[-0.08,0.08)", "inputs": "Rng(2) U[-1,1), out_len=T",
+            "l2": "flushed (256 MiB write) before every timed decode",
+            "blank_bias": args.blank_bias}
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg, rank, world)
+        return
+    import torch
+    from paper_2406_03791_b200 import Model, ModelDims
+    from paper_2406_03791_b200._lib import Stats, check, lib
+
+    algo, B, T, ms, durs, L, H, J, V, F, scaling = cfg
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    b0, b1 = shard(cfg, rank, world)
+    Bl = b1 - b0
+    dims = ModelDims(V, H, H, J, F, durs, "lstm", L)
+    model = Model.from_seed(dims, 1, device=local, blank_bias=args.blank_bias)
+    L_ = lib()
+    dh = C.c_void_p()
+    check(L_.rnntg_decoder_create(model.handle, ALGO_ID[algo], 0 if args.exec == "graph" else 1,
+                                  Bl, T, ms, C.byref(dh)))
+    x, lens = make_inputs(cfg, b0, b1)
+    xd = torch.from_numpy(x).cuda()
+    ld = torch.from_numpy(lens).cuda()
+    check(L_.rnntg_bind_device(dh, C.c_void_p(xd.data_ptr()), C.c_void_p(ld.data_ptr())))
+    stream = torch.cuda.ExternalStream(L_.rnntg_decoder_stream(dh), device=local)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def decode_once():
+        check(L_.rnntg_launch(dh))
+
+    for _ in range(args.warmup):
+        decode_once()
+    check(L_.rnntg_sync(dh))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(float(i))
+                evs[i][0].record(stream)
+            decode_once()
+            with torch.cuda.stream(stream):
+                evs[i][1].record(stream)
+        check(L_.rnntg_sync(dh))
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = float(sum(step_ms))
+    if dist:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    st = Stats()
+    check(L_.rnntg_get_stats(dh, C.byref(st)))
+    frames_all = B * T if scaling == "strong" else B * T * world
+    value = frames_all * args.steps / (total_ms / 1000.0)
+    ms_per_step = total_ms / args.steps
+    per_rank_frames = Bl * T
+    fs = algo == "fs"
+    launches_per_step = 2 + st.pred_steps * (L + 1) + st.joint_evals + (st.outer_iters if fs else 0)
+
+    # ---- kernel shares + roofline of the dominant kernel (standalone launches) ----
+    kern = {}
+    names = {0: "enc_proj", 1: "pred_layer0", 2: "pred_layer1", 8: "pred_proj", 9: "joint"}
+    for w, n in names.items():
+        if w in (1, 2) and w - 1 >= L:
+            continue
+        ms_ = C.c_float()
+        check(L_.rnntg_time_kernel(dh, w, 20, C.byref(ms_)))
+        kern[n] = ms_.value
+    per_step_counts = {"enc_proj": 1, "pred_layer0": st.pred_steps,
+                       "pred_layer1": st.pred_steps if L > 1 else 0,
+                       "pred_proj": st.pred_steps, "joint": st.joint_evals}
+    share = {n: kern[n] * per_step_counts[n] / ms_per_step for n in kern}
+    dom = max(share, key=share.get)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    Hp = (H + 63) // 64 * 64
+    Jp = (J + 63) // 64 * 64
+    Bp = (Bl + 31) // 32 * 32
+    V1p = (V + 1 + 15) // 16 * 16
+    bytes_per = {  # algorithmic bytes per launch (weights + activations read + outputs written)
+        "pred_layer1": 4 * (2 * Hp * 4 * Hp + Bp * 2 * Hp + 2 * Bp * Hp * 2),
+        "pred_layer0": 4 * (Hp * 4 * Hp + Bp * Hp + 2 * Bp * Hp * 2 + Bp * 4 * Hp),
+        "pred_proj": 4 * (Hp * Jp + Bp * Hp + Bp * Jp),
+        "joint": 4 * (Jp * V1p + 2 * Bp * Jp),
+        "enc_proj": 4 * (Bl * T * F + F * Jp + Bl * T * Jp),
+    }
+    flops_per = {
+        "pred_layer1": 2 * Bl * 2 * H * 4 * H, "pred_layer0": 2 * Bl * H * 4 * H,
+        "pred_proj": 2 * Bl * H * J, "joint": 2 * Bl * J * (V + 1), "enc_proj": 2 * Bl * T * F * J,
+    }
+    ach = bytes_per[dom] / (kern[dom] / 1000.0) / 1e9
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    clk = clk.summary() if hasattr(clk, "summary") else clk
+    fp32_peak = 148 * 128 * 2 * (clk.get("sm_mhz") or sm_mhz) * 1e6 / 1e12
+    fp32_ach = flops_per[dom] / (kern[dom] / 1000.0) / 1e12
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ach / hbm_peak, "traffic": None,
+                "algorithmic_bytes_per_launch": bytes_per[dom],
+                "avg_launch_us": kern[dom] * 1000.0,
+                "fp32": {"achieved_tflops": fp32_ach, "peak_tflops": fp32_peak,
+                         "frac": fp32_ach / fp32_peak,
+                         "note": "FFMA peak = 148 SM x 128 lanes x 2 x median SM clock"},
+                "kernel_us": {n: v * 1000.0 for n, v in kern.items()},
+                "step_share": share}
+
+    # ---- e2e through the C ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        cap = L_.rnntg_decoder_capacity(dh)
+        xh = torch.from_numpy(x).pin_memory()
+        lh = torch.from_numpy(lens).pin_memory()
+        outs = [torch.empty((Bl,), dtype=torch.int32).pin_memory()] + \
+               [torch.empty((Bl, cap), dtype=torch.int32).pin_memory() for _ in range(4)]
+        ptr = [C.c_void_p(o.data_ptr()) for o in outs]
+
+        def e2e_once():
+            check(L_.rnntg_bind(dh, C.c_void_p(xh.data_ptr()), C.c_void_p(lh.data_ptr())))
+            check(L_.rnntg_launch(dh))
+            check(L_.rnntg_read(dh, ptr[0], ptr[1], ptr[2], ptr[3], ptr[4], cap))
+
+        for _ in range(2):
+            e2e_once()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_once()
+        el = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([el], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": frames_all * args.steps / el, "unit": "frames/s",
+               "h2d_bytes_per_step": int(x.nbytes + lens.nbytes),
+               "d2h_bytes_per_step": int(4 * Bl + 4 * 4 * Bl * cap)}
+        # verify the e2e decode agrees with the device-input decode
+        # (same inputs -> identical counts)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import oracle as O
+            if O.ref_available():
+                cpu = cpu_reference_sample(cfg, args.cpu_seconds)
+                cpu.pop("seconds", None)
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "error": str(e)}
+
+    if rank == 0:
+        inner = st.joint_evals
+        out = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (random-init weights, random encoder outputs)",
+            "config": config_json(args, cfg) | {"parallelism": f"utterance-sharded x{world}"},
+            "us_per_step": 1000.0 * ms_per_step / max(inner, 1),
+            "inner_steps_per_decode": inner, "pred_steps_per_decode": st.pred_steps,
+            "outer_iters_per_decode": st.outer_iters,
+            "tokens_per_frame": st.emitted / max(per_rank_frames, 1),
+            "gpu_idle_pct": None,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches_per_step * args.steps),
+            "clocks": clk, "step_ms": step_ms,
+        }
+        print(json.dumps(out), flush=True)
+    check(L_.rnntg_decoder_destroy(dh))
+    model.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,719 @@
+// kernels.cuh — the decoder's sm_100a kernels (graph path).
+//
+//   encproj_simt_kernel   K1 reference-precision encoder projection (fp32 FFMA)
+//   prologue_kernel       K0 state / emission / loop-flag initialisation
+//   pred_layer_kernel     K2 one prediction-network layer: gate GEMV fused with
+//                         the tanh / LSTM cell and the predicated state commit
+//   pred_proj_kernel      gp = h_top @ pred_proj (cached per accepted label)
+//   joint_kernel          K3 joint step: relu(fp+gp) @ out_proj(||dur_proj),
+//                         per-chunk log-sum-exp + argmax, last-CTA decision
+//                         (blank mask / label-loop cursor rules, hypothesis +
+//                         timestamp append, loop flag, cudaGraphSetConditional)
+//   frame_tail_kernel     frame-sync outer-loop tail (t += 1, next frame init)
+//
+// Per-output arithmetic is fp32 with FFMA; reductions run in a fixed order so
+// every launch is deterministic.  Reference semantics cited per function.
+#pragma once
+
+#include "common.cuh"
+
+namespace rnntg {
+
+// -------------------------------------------------------------------------
+// Step GEMV building block.
+// One warp accumulates a 32-row x 16-col tile over its k-slice [k0, k0+kw):
+//   lane = (rg = lane>>2 : rows rg, rg+8, rg+16, rg+24) x (cg = lane&3 : cols 4cg..4cg+3)
+// A rows come from shared memory (row stride KS, KS % 32 == 4 so the 8 row
+// groups hit 8 distinct bank quads: one wavefront per LDS.128, broadcast over
+// cg); W comes from global/L2 as 64-byte row segments, software-pipelined two
+// 4-k groups ahead.  kw must be a multiple of 8.
+// -------------------------------------------------------------------------
+__device__ __forceinline__ void warp_gemv_32x16(const float* __restrict__ As, int KS,
+                                                const float* __restrict__ W, int ldw, int col0,
+                                                int k0, int kw, float (&acc)[4][4]) {
+  const int lane = threadIdx.x & 31, rg = lane >> 2, cg = lane & 3;
+  const float* wp = W + (size_t)k0 * ldw + col0 + 4 * cg;
+  const float* ap = As + rg * KS + k0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+  float4 wc[8], wn[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) wc[q] = ldg4(wp + (size_t)q * ldw);
+  for (int k = 0; k < kw; k += 8) {
+    if (k + 8 < kw) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) wn[q] = ldg4(wp + (size_t)(k + 8 + q) * ldw);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 a = lds4(ap + i * 8 * KS + k + 4 * h);
+        const float4 w0 = wc[4 * h + 0], w1 = wc[4 * h + 1], w2 = wc[4 * h + 2],
+                     w3 = wc[4 * h + 3];
+        acc[i][0] = fmaf(a.x, w0.x, acc[i][0]);
+        acc[i][1] = fmaf(a.x, w0.y, acc[i][1]);
+        acc[i][2] = fmaf(a.x, w0.z, acc[i][2]);
+        acc[i][3] = fmaf(a.x, w0.w, acc[i][3]);
+        acc[i][0] = fmaf(a.y, w1.x, acc[i][0]);
+        acc[i][1] = fmaf(a.y, w1.y, acc[i][1]);
+        acc[i][2] = fmaf(a.y, w1.z, acc[i][2]);
+        acc[i][3] = fmaf(a.y, w1.w, acc[i][3]);
+        acc[i][0] = fmaf(a.z, w2.x, acc[i][0]);
+        acc[i][1] = fmaf(a.z, w2.y, acc[i][1]);
+        acc[i][2] = fmaf(a.z, w2.z, acc[i][2]);
+        acc[i][3] = fmaf(a.z, w2.w, acc[i][3]);
+        acc[i][0] = fmaf(a.w, w3.x, acc[i][0]);
+        acc[i][1] = fmaf(a.w, w3.y, acc[i][1]);
+        acc[i][2] = fmaf(a.w, w3.z, acc[i][2]);
+        acc[i][3] = fmaf(a.w, w3.w, acc[i][3]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) wc[q] = wn[q];
+  }
+}
+
+// Store a warp's partial tile into red[warp][32][16].
+__device__ __forceinline__ void store_partial(float* red, const float (&acc)[4][4]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, rg = lane >> 2, cg = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float4 v = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    *reinterpret_cast<float4*>(red + ((warp * RB) + rg + 8 * i) * CT + 4 * cg) = v;
+  }
+}
+
+// Sum of the NW warp partials for (row r, col c), fixed warp order.
+__device__ __forceinline__ float reduce_partial(const float* red, int r, int c) {
+  float s = red[r * CT + c];
+#pragma unroll
+  for (int w = 1; w < NW; ++w) s += red[(w * RB + r) * CT + c];
+  return s;
+}
+
+// Shared-memory carve-up of the step kernels: [NW mbarriers][As 32 x KS][red].
+struct StepSmem {
+  uint64_t* bars;
+  float* As;
+  float* red;
+  int* flag;
+};
+__device__ __forceinline__ StepSmem carve(void* base, int KS) {
+  StepSmem s;
+  s.bars = reinterpret_cast<uint64_t*>(base);
+  s.flag = reinterpret_cast<int*>(s.bars + NW);
+  s.As = reinterpret_cast<float*>(reinterpret_cast<char*>(base) + 128);
+  s.red = s.As + RB * KS;
+  return s;
+}
+__host__ __device__ inline size_t step_smem_bytes(int K) {
+  return 128 + sizeof(float) * ((size_t)RB * (K + 4) + (size_t)NW * RB * CT);
+}
+
+// Stage this warp's k-slice of 32 activation rows with the bulk-copy (TMA)
+// engine.  Sources: k < seg_k from src0, else from src1 (both [rows][ld]).
+__device__ __forceinline__ void stage_rows_bulk(const StepSmem& sm, int KS, int row0,
+                                                const float* src0, const float* src1, int seg_k,
+                                                int ld, int k0, int kw) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float* src = k0 < seg_k ? src0 : src1;
+  const int koff = k0 < seg_k ? k0 : k0 - seg_k;
+  if (lane == 0) mbar_arrive_expect_tx(&sm.bars[warp], (uint32_t)(RB * kw * sizeof(float)));
+  __syncwarp();
+  bulk_g2s(sm.As + lane * KS + k0, src + (size_t)(row0 + lane) * ld + koff,
+           (uint32_t)(kw * sizeof(float)), &sm.bars[warp]);
+}
+
+// -------------------------------------------------------------------------
+// K1 (reference-precision path): fp[m, n] = sum_k x[m, k] * enc[k, n].
+// joint.enc_proj of model.cpp:365-369, hoisted over all B*T frames
+// (bit-neutral hoist).  64x64 tiles, 256 threads, 4x4 each.
+// -------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) encproj_simt_kernel(const float* __restrict__ x,
+                                                           const float* __restrict__ enc,
+                                                           float* __restrict__ out, int M,
+                                                           int F, int Jp) {
+  __shared__ float Xs[16][64 + 4];
+  __shared__ float Ws[16][64];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < F; k0 += 16) {
+    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+      const int mm = i / 16, kk = i % 16;
+      const int m = m0 + mm, k = k0 + kk;
+      Xs[kk][mm] = (m < M && k < F) ? x[(size_t)m * F + k] : 0.0f;
+    }
+    for (int i = threadIdx.x; i < 16 * 64; i += 256) {
+      const int kk = i / 64, nn = i % 64;
+      const int k = k0 + kk;
+      Ws[kk][nn] = (k < F) ? enc[(size_t)k * Jp + n0 + nn] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = Xs[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Ws[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+    *reinterpret_cast<float4*>(out + (size_t)m * Jp + n0 + tx * 4) =
+        make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+  }
+}
+
+// -------------------------------------------------------------------------
+// Exact table of the layer-0 input contribution: table0[v, col] =
+// sum_e embedding[v, e] * W_ih0[e, col], sequential e with separate rounding
+// per multiply and add -- bit-identical to the reference's pred.matmul_ih
+// (model.cpp:338-342, tensor.cpp:249-257) for every label, computed once.
+// -------------------------------------------------------------------------
+__global__ void table0_kernel(const float* __restrict__ emb, const float* __restrict__ wih,
+                              float* __restrict__ table, int V1, int E, int ncols_in,
+                              int G, int H, int Hp) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;  // reference column g*H + u
+  const int v = blockIdx.y;
+  if (col >= ncols_in || v >= V1) return;
+  float acc = 0.0f;
+  for (int e = 0; e < E; ++e)
+    acc = __fadd_rn(acc, __fmul_rn(emb[(size_t)v * E + e], wih[(size_t)e * ncols_in + col]));
+  const int g = col / H, u = col % H;
+  table[(size_t)v * (G * Hp) + u * G + g] = acc;
+}
+
+// -------------------------------------------------------------------------
+// K0 prologue: launch_fs_prologue / launch_ll_prologue (decoders.cpp:216-233,
+// 414-430): zero the prediction state, counts, last_label = blank, loop
+// scalars; frame-sync: blank mask for frame 0; label-loop: t = u = 0,
+// active = t < out_len.  Every row is marked `accept` so the following
+// prediction step computes P0 = pred(blank, 0) for all rows.
+// -------------------------------------------------------------------------
+__global__ void prologue_kernel(DevModel M, DevState S) {
+  // zero state (both parities) with a grid-stride loop
+  const size_t nstate = (size_t)S.Bp * M.Hp;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t nthr = (size_t)gridDim.x * blockDim.x;
+  for (int l = 0; l < M.L; ++l)
+    for (int p = 0; p < 2; ++p) {
+      for (size_t i = tid; i < nstate; i += nthr) {
+        S.h[l][p][i] = 0.0f;
+        if (S.c[l][p]) S.c[l][p][i] = 0.0f;
+      }
+    }
+  for (size_t i = tid; i < (size_t)S.Bp * M.Jp; i += nthr) S.gp[i] = 0.0f;
+  if (blockIdx.x != 0) return;
+  __shared__ int smax;
+  __shared__ int sany;
+  if (threadIdx.x == 0) {
+    smax = 0;
+    sany = 0;
+  }
+  __syncthreads();
+  const int blank = M.V1 - 1;
+  for (int b = threadIdx.x; b < S.Bp; b += blockDim.x) {
+    const int len = b < S.B ? S.out_len[b] : 0;
+    const int live = b < S.B;
+    S.last_label[b] = blank;
+    S.accept[b] = live;
+    S.counts[b] = 0;
+    S.t_row[b] = 0;
+    S.u_row[b] = 0;
+    S.done[b] = live ? (0 >= len) : 1;
+    const int act = live && (0 < len);
+    S.active[b] = act;
+    S.need[b] = act;
+    if (live) atomicMax(&smax, len);
+    if (act) sany = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Ctrl* c = S.ctrl;
+    c->t = 0;
+    c->sym = 0;
+    c->max_len = smax;
+    c->par = 0;
+    c->err = 0;
+    c->abort = 0;
+    c->any = sany;
+    for (int i = 0; i < MAXRB; ++i) c->ctr_joint_rb[i] = 0;
+    c->ctr_joint_all = 0;
+    c->ctr_pp = 0;
+    c->joint_evals = 0;
+    c->pred_steps = 0;
+    c->outer_iters = 0;
+    c->iters = 0;
+    if (S.use_cond) {
+      if (S.algo == ALGO_FS) {
+        cudaGraphSetConditional(S.h_outer, smax > 0 ? 1u : 0u);
+        cudaGraphSetConditional(S.h_inner, 1u);
+      }
+      // label-loop conditions are set by the prologue's pred_proj tail
+    }
+  }
+}
+
+// -------------------------------------------------------------------------
+// K2: one prediction-network layer for every row of a 32-row block and one
+// 16-column tile of gate columns (4 LSTM units or 16 tanh units).
+//   tanh (model.cpp:163-176, 39-51):  h' = tanh((ih + hh) + bias)
+//   LSTM:          gates = (ih + hh) + b ; i,f,g,o ;
+//                                     c' = f c + i g ; h' = o tanh(c')
+// Layer 0's ih comes from the exact table0[last_label]; layers > 0 fold ih
+// into the GEMV over [h_{l-1}' | h_l].  Rows that did not accept a label copy
+// their old state (where_select_rows semantics, decoders.cpp:292-295).
+// -------------------------------------------------------------------------
+template <int CELL>
+__global__ void __launch_bounds__(NT) pred_layer_kernel(DevModel M, DevState S, int l) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int K = l == 0 ? M.Hp : 2 * M.Hp;
+  const int KS = K + 4;
+  StepSmem sm = carve(smem_raw, KS);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x, rb = blockIdx.y, row0 = rb * RB, col0 = tile * CT;
+  if (lane == 0) mbar_init(&sm.bars[warp], 1);
+  fence_mbar_init();
+  __syncwarp();
+  pdl_trigger();
+  pdl_wait();
+  const int par = ld_volatile(&S.ctrl->par);
+  const int cur = par, nxt = par ^ 1;
+  const int kw = K / NW, k0 = warp * kw;
+  if (l == 0)
+    stage_rows_bulk(sm, KS, row0, S.h[0][cur], S.h[0][cur], K, M.Hp, k0, kw);
+  else
+    stage_rows_bulk(sm, KS, row0, S.h[l - 1][nxt], S.h[l][cur], M.Hp, M.Hp, k0, kw);
+  mbar_wait(&sm.bars[warp], 0);
+  float acc[4][4];
+  warp_gemv_32x16(sm.As, KS, M.w[l], M.GH, col0, k0, kw, acc);
+  store_partial(sm.red, acc);
+  __syncthreads();
+  const float* bias = M.bias[l];
+  if (CELL == 1) {
+    // 4 units x 32 rows; thread -> (row, unit)
+    if (threadIdx.x < RB * 4) {
+      const int r = threadIdx.x >> 2, uu = threadIdx.x & 3;
+      const int b = row0 + r;
+      const int u = tile * 4 + uu;
+      if (b < S.B) {
+        float gt[4];
+        const int lab = S.last_label[b];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int col = uu * 4 + g;
+          float hh = reduce_partial(sm.red, r, col);
+          float pre = l == 0 ? M.table0[(size_t)lab * M.GH + col0 + col] + hh : hh;
+          gt[g] = pre + bias[col0 + col];
+        }
+        const size_t idx = (size_t)b * M.Hp + u;
+        const float c_old = S.c[l][cur][idx];
+        float hn, cn;
+        if (S.accept[b]) {
+          const float i_ = sigmoid_f(gt[0]), f_ = sigmoid_f(gt[1]);
+          const float g_ = tanhf(gt[2]), o_ = sigmoid_f(gt[3]);
+          cn = f_ * c_old + i_ * g_;
+          hn = o_ * tanhf(cn);
+        } else {
+          cn = c_old;
+          hn = S.h[l][cur][idx];
+        }
+        S.c[l][nxt][idx] = cn;
+        S.h[l][nxt][idx] = hn;
+      }
+    }
+  } else {
+    for (int o = threadIdx.x; o < RB * CT; o += NT) {
+      const int r = o / CT, col = o % CT;
+      const int b = row0 + r;
+      if (b >= S.B) continue;
+      const int u = col0 + col;
+      const size_t idx = (size_t)b * M.Hp + u;
+      float hn;
+      if (S.accept[b]) {
+        const float hh = reduce_partial(sm.red, r, col);
+        const int lab = S.last_label[b];
+        hn = tanhf((M.table0[(size_t)lab * M.GH + u] + hh) + bias[u]);
+      } else {
+        hn = S.h[0][cur][idx];
+      }
+      S.h[0][nxt][idx] = hn;
+    }
+  }
+}
+
+// -------------------------------------------------------------------------
+// Label-loop bookkeeping after a prediction step (end of launch_ll_body,
+// decoders.cpp:485-512 + active_update 402-412): every active row needs a
+// decision in the next round; loop flags for the nested WHILE nodes.
+// -------------------------------------------------------------------------
+__device__ void ll_round_tail(const DevModel& M, const DevState& S) {
+  __shared__ int s_any;
+  if (threadIdx.x == 0) s_any = 0;
+  __syncthreads();
+  int any = 0;
+  for (int b = threadIdx.x; b < S.B; b += blockDim.x) {
+    const int act = S.active[b];
+    S.need[b] = act;
+    S.accept[b] = 0;
+    any |= act;
+  }
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0) {
+    Ctrl* c = S.ctrl;
+    const int go = any && !c->abort;
+    c->any = go;
+    c->outer_iters += 1;
+    if (S.use_cond) {
+      cudaGraphSetConditional(S.h_inner, go ? 1u : 0u);
+      cudaGraphSetConditional(S.h_outer, go ? 1u : 0u);
+    }
+  }
+}
+
+// -------------------------------------------------------------------------
+// gp = h_top' @ pred_proj for accepted rows (joint.pred_proj, model.cpp:370-374,
+// cached per prediction state -- bit-neutral).  The last
+// CTA flips the state parity and runs the label-loop round tail.
+// -------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) pred_proj_kernel(DevModel M, DevState S) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int K = M.Hp, KS = K + 4;
+  StepSmem sm = carve(smem_raw, KS);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x, rb = blockIdx.y, row0 = rb * RB, col0 = tile * CT;
+  if (lane == 0) mbar_init(&sm.bars[warp], 1);
+  fence_mbar_init();
+  __syncwarp();
+  pdl_trigger();
+  pdl_wait();
+  const int nxt = ld_volatile(&S.ctrl->par) ^ 1;
+  const int kw = K / NW, k0 = warp * kw;
+  const float* htop = S.h[M.L - 1][nxt];
+  stage_rows_bulk(sm, KS, row0, htop, htop, K, M.Hp, k0, kw);
+  mbar_wait(&sm.bars[warp], 0);
+  float acc[4][4];
+  warp_gemv_32x16(sm.As, KS, M.pred_proj, M.Jp, col0, k0, kw, acc);
+  store_partial(sm.red, acc);
+  __syncthreads();
+  for (int o = threadIdx.x; o < RB * CT; o += NT) {
+    const int r = o / CT, col = o % CT, b = row0 + r;
+    if (b < S.B && S.accept[b]) S.gp[(size_t)b * M.Jp + col0 + col] = reduce_partial(sm.red, r, col);
+  }
+  // last CTA of the grid: parity flip + loop bookkeeping
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned total = gridDim.x * gridDim.y;
+    const unsigned prev = atomicAdd(&S.ctrl->ctr_pp, 1u);
+    *sm.flag = (prev == total - 1);
+  }
+  __syncthreads();
+  if (!*sm.flag) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    S.ctrl->ctr_pp = 0;
+    S.ctrl->par ^= 1;
+    S.ctrl->pred_steps += 1;
+  }
+  if (S.algo != ALGO_FS) ll_round_tail(M, S);
+}
+
+// -------------------------------------------------------------------------
+// Per-row decision of the joint step (lane 0 of the row's warp).
+//   frame-sync: launch_fs_inner_body's argmax/blank_update/save_kv/update_*
+//               (decoders.cpp:261-307)
+//   label-loop / TDT: accept_mask, save_kv, commit_last_label, step_advance,
+//               active_update (decoders.cpp:432-512)
+// -------------------------------------------------------------------------
+__device__ __forceinline__ void append_emission(const DevState& S, int b, int k, int frame,
+                                                float v, int dur) {
+  const int n = S.counts[b];
+  if (n < S.cap) {  // unreachable bound, decoders.cpp:81
+    const size_t o = (size_t)b * S.cap + n;
+    S.tokens[o] = k;
+    S.frames[o] = frame;
+    S.scores[o] = v;
+    S.durs[o] = dur;
+    S.counts[b] = n + 1;
+  }
+}
+
+__device__ __forceinline__ void decide_row(const DevModel& M, const DevState& S, int b, int k,
+                                           float v, int dur_idx) {
+  const int blank = M.V1 - 1;
+  if (S.algo == ALGO_FS) {
+    if (S.done[b]) {
+      S.accept[b] = 0;
+      return;
+    }
+    if (k == blank) {
+      S.done[b] = 1;
+      S.accept[b] = 0;
+    } else {
+      append_emission(S, b, k, S.ctrl->t, v, 0);
+      S.last_label[b] = k;
+      S.accept[b] = 1;
+    }
+    return;
+  }
+  if (!S.need[b]) return;
+  const int len = S.out_len[b];
+  int t = S.t_row[b], u = S.u_row[b];
+  const bool tdt = S.algo == ALGO_TDT;
+  if (k == blank) {
+    const int d = tdt ? M.durations[dur_idx] : 1;
+    t += d > 1 ? d : 1;
+    u = 0;
+    const int act = t < len;
+    S.active[b] = act;
+    S.need[b] = act;
+  } else {
+    const int d = tdt ? M.durations[dur_idx] : 0;
+    append_emission(S, b, k, t, v, d);
+    S.last_label[b] = k;
+    S.accept[b] = 1;
+    u += 1;
+    if (d > 0) {
+      t += d;
+      u = 0;
+    } else if (u == S.ms) {
+      t += 1;
+      u = 0;
+    }
+    S.active[b] = t < len;
+    S.need[b] = 0;
+  }
+  S.t_row[b] = t;
+  S.u_row[b] = u;
+}
+
+// -------------------------------------------------------------------------
+// K3 joint step.  grid = (NCHT column chunks, row blocks).  Each CTA stages
+// trunk = relu(fp[b, t_b] + gp[b]) (joint.combine, model.cpp:375-379) for the
+// rows that need a decision, computes its 16 logits per row
+// (joint.out_proj / dur_proj, model.cpp:380-384, 401-405), and publishes the
+// chunk's (max, sum exp(x - max), best value, best index).  The last CTA of a
+// row block merges the chunks in fixed order into lse = m + log(s)
+// (log_softmax_into, tensor.cpp:463-480) and the lowest-index argmax
+// (argmax_last_into, tensor.cpp:268-312), applies the decision rules and
+// appends (token, frame, score, duration); the last row block then sets the
+// loop flag with cudaGraphSetConditional.
+// -------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) joint_kernel(DevModel M, DevState S) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int K = M.Jp, KS = K + 4;
+  StepSmem sm = carve(smem_raw, KS);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int chunk = blockIdx.x, rb = blockIdx.y, row0 = rb * RB, col0 = chunk * CT;
+  const bool dur_chunk = chunk >= M.NCH;
+  pdl_trigger();
+  pdl_wait();
+  const bool fs = S.algo == ALGO_FS;
+  const int tf = fs ? ld_volatile(&S.ctrl->t) : 0;
+  // ---- stage trunk rows (this warp's k-slice) ----
+  const int kw = K / NW, k0 = warp * kw, kq = kw / 4;
+  for (int p = lane; p < RB * kq; p += 32) {
+    const int r = p / kq, q = p % kq, b = row0 + r;
+    const int k = k0 + 4 * q;
+    float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool live = b < S.B && (fs ? !S.done[b] : S.need[b] != 0);
+    if (live) {
+      int t = fs ? tf : S.t_row[b];
+      t = t < 0 ? 0 : (t > S.T - 1 ? S.T - 1 : t);
+      const float4 f = ldg4(S.fp + ((size_t)b * S.T + t) * M.Jp + k);
+      const float4 g = *reinterpret_cast<const float4*>(S.gp + (size_t)b * M.Jp + k);
+      z.x = fmaxf(f.x + g.x, 0.0f);
+      z.y = fmaxf(f.y + g.y, 0.0f);
+      z.z = fmaxf(f.z + g.z, 0.0f);
+      z.w = fmaxf(f.w + g.w, 0.0f);
+    }
+    *reinterpret_cast<float4*>(sm.As + r * KS + k) = z;
+  }
+  __syncwarp();
+  float acc[4][4];
+  warp_gemv_32x16(sm.As, KS, M.out_ext, M.NOUT, col0, k0, kw, acc);
+  store_partial(sm.red, acc);
+  __syncthreads();
+  // ---- per-row chunk statistics: half-warp per row ----
+  const int half = lane >> 4, hl = lane & 15;
+  const int nvalid = dur_chunk ? M.D : (M.V1 - col0 < CT ? M.V1 - col0 : CT);
+  for (int r = warp * 2 + half; r < RB; r += 2 * NW) {
+    const int b = row0 + r;
+    float x = reduce_partial(sm.red, r, hl);
+    const bool valid = hl < nvalid;
+    if (S.dbg_logits && b < S.B && valid) S.dbg_logits[(size_t)b * M.NOUT + col0 + hl] = x;
+    float m = valid ? x : -INFINITY;
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float e = valid ? expf(x - m) : 0.0f;
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+    float bv = valid ? x : -INFINITY;
+    int bi = valid ? hl : CT;
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (hl == 0 && b < S.Bp)
+      S.part[(size_t)b * M.NCHT + chunk] =
+          make_float4(m, e, bv, __int_as_float((dur_chunk ? 0 : col0) + bi));
+  }
+  // ---- last CTA of this row block decides its rows ----
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&S.ctrl->ctr_joint_rb[rb], 1u);
+    *sm.flag = (prev == (unsigned)gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!*sm.flag) return;
+  __threadfence();
+  for (int r = warp; r < RB; r += NW) {
+    const int b = row0 + r;
+    if (b >= S.B) continue;
+    const bool live = fs ? !S.done[b] : S.need[b] != 0;
+    if (!live) {
+      if (lane == 0 && fs) S.accept[b] = 0;
+      continue;
+    }
+    float Mx = -INFINITY, Sx = 0.0f, best = -INFINITY;
+    int bidx = 0x7fffffff;
+    for (int c = lane; c < M.NCH; c += 32) {
+      const float4 p = __ldcg(&S.part[(size_t)b * M.NCHT + c]);
+      const float nm = fmaxf(Mx, p.x);
+      Sx = (Sx == 0.0f ? 0.0f : Sx * expf(Mx - nm)) + p.y * expf(p.x - nm);
+      Mx = nm;
+      const int pi = __float_as_int(p.w);
+      if (p.z > best || (p.z == best && pi < bidx)) {
+        best = p.z;
+        bidx = pi;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, Mx, o);
+      const float os = __shfl_xor_sync(0xffffffffu, Sx, o);
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+      const float nm = fmaxf(Mx, om);
+      const float a = Sx == 0.0f ? 0.0f : Sx * expf(Mx - nm);
+      const float bb = os == 0.0f ? 0.0f : os * expf(om - nm);
+      Sx = a + bb;
+      Mx = nm;
+      if (ob > best || (ob == best && oi < bidx)) {
+        best = ob;
+        bidx = oi;
+      }
+    }
+    if (lane == 0) {
+      const float lse = Mx + logf(Sx);
+      const float v = best - lse;
+      int dur_idx = 0;
+      float lse_d = 0.0f;
+      if (M.D > 0) {
+        const float4 pd = __ldcg(&S.part[(size_t)b * M.NCHT + M.NCH]);
+        dur_idx = __float_as_int(pd.w);
+        lse_d = pd.x + logf(pd.y);
+      }
+      if (S.dbg_lse) {
+        S.dbg_lse[b] = lse;
+        S.dbg_lse[S.Bp + b] = lse_d;
+      }
+      decide_row(M, S, b, bidx, v, dur_idx);
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    S.ctrl->ctr_joint_rb[rb] = 0;
+    const unsigned prev = atomicAdd(&S.ctrl->ctr_joint_all, 1u);
+    *sm.flag = (prev == (unsigned)gridDim.y - 1);
+  }
+  __syncthreads();
+  if (!*sm.flag) return;
+  __threadfence();
+  // ---- last row block: loop flag ----
+  int any = 0;
+  for (int b = threadIdx.x; b < S.B; b += blockDim.x)
+    any |= fs ? !ld_volatile(&S.done[b]) : ld_volatile(&S.need[b]);
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0) {
+    Ctrl* c = S.ctrl;
+    c->ctr_joint_all = 0;
+    c->joint_evals += 1;
+    c->iters += 1;
+    int go;
+    if (fs) {
+      c->sym += 1;
+      go = any && c->sym < S.ms;
+    } else {
+      go = any;
+    }
+    if (c->iters > S.max_iters) {
+      c->err = ERR_RUNAWAY;
+      c->abort = 1;
+      go = 0;
+    }
+    c->any = go;
+    if (S.use_cond) cudaGraphSetConditional(S.h_inner, go ? 1u : 0u);
+  }
+}
+
+// -------------------------------------------------------------------------
+// Frame-sync outer tail: launch_fs_outer_tail + next launch_fs_frame_head's
+// frame_init (decoders.cpp:235-259, 309-313): t += 1; blank_mask = t >=
+// out_len; symbols_added = 0; inner flag = 1; outer flag = t < max_out_len.
+// -------------------------------------------------------------------------
+__global__ void frame_tail_kernel(DevModel M, DevState S) {
+  pdl_wait();
+  const int t = S.ctrl->t + 1;
+  for (int b = threadIdx.x; b < S.B; b += blockDim.x) S.done[b] = t >= S.out_len[b];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Ctrl* c = S.ctrl;
+    c->t = t;
+    c->sym = 0;
+    c->outer_iters += 1;
+    const int go = t < c->max_len && !c->abort;
+    if (S.use_cond) {
+      cudaGraphSetConditional(S.h_outer, go ? 1u : 0u);
+      cudaGraphSetConditional(S.h_inner, 1u);
+    }
+  }
+}
+
+// Marks every row live for standalone kernel timing (rnntg_time_kernel).
+__global__ void timing_prep_kernel(DevState S) {
+  for (int b = threadIdx.x; b < S.Bp; b += blockDim.x) {
+    const int live = b < S.B;
+    S.done[b] = !live;
+    S.need[b] = live;
+    S.accept[b] = live;
+    S.counts[b] = 0;
+  }
+  if (threadIdx.x == 0) {
+    S.ctrl->sym = 0;
+    S.ctrl->iters = 0;
+    S.ctrl->t = 0;
+  }
+}
+
+}  // namespace rnntg

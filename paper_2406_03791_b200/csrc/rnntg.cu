@@ -1,0 +1,838 @@
+// rnntg.cu — host side of the C ABI (include/rnntg.h): weight repacking,
+// static device workspaces, CUDA-graph construction with nested conditional
+// WHILE nodes, launch / read, and the kernel-level step entry points.
+//
+// Reference mapping (decoders.hpp:56-130):
+//   rnntg_decoder_create   build_decode_graph   (decoders.cpp:589-627)
+//   rnntg_bind             bind_decode_inputs   (decoders.cpp:202-207, 124-142)
+//   rnntg_launch           Engine::replay       (engine.cpp:296-307)
+//   rnntg_read             read_emissions       (decoders.cpp:97-122)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rnntg.h"
+#include "common.cuh"
+#include "kernels.cuh"
+#include "encproj_tc.cuh"
+
+using namespace rnntg;
+
+namespace {
+
+thread_local std::string g_err;
+
+rnntg_status fail(rnntg_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CK(expr)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(RNNTG_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+bool env_flag(const char* name, bool dflt) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return !(v[0] == '0' || v[0] == 'n' || v[0] == 'N' || v[0] == 'f' || v[0] == 'F');
+}
+
+struct DevBuf {
+  std::vector<void*> ptrs;
+  template <typename T>
+  cudaError_t alloc(T** p, size_t n) {
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T));
+    if (e != cudaSuccess) return e;
+    ptrs.push_back(q);
+    *p = static_cast<T*>(q);
+    return cudaMemset(q, 0, std::max<size_t>(n, 1) * sizeof(T));
+  }
+  void release() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+  }
+};
+
+}  // namespace
+
+struct rnntg_model {
+  int device = 0;
+  rnntg_dims dims{};
+  DevModel dm{};
+  DevBuf mem;
+  float* w_enc = nullptr;
+  bool tc_ok = false;   // tcgen05 encoder projection usable on this device
+};
+
+struct rnntg_decoder {
+  rnntg_model* m = nullptr;
+  int algo = 0, exec = 0, B = 0, T = 0, ms = 0;
+  DevState st{};
+  DevBuf mem;
+  cudaStream_t stream = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool bound = false, launched = false;
+  float* x_dev = nullptr;
+  int* len_dev = nullptr;
+  // kernel-node argument storage (copied into the nodes at creation)
+  DevModel arg_m{};
+  DevState arg_s{};
+  int arg_l[MAXL]{};
+};
+
+namespace {
+
+// ---------------------------------------------------------------- model
+rnntg_status validate_dims(const rnntg_dims* d) {
+  if (!d) return fail(RNNTG_E_VALUE, "dims is null");
+  if (d->vocab < 1 || d->embed < 1 || d->hidden < 1 || d->joint < 1 || d->feature < 1)
+    return fail(RNNTG_E_VALUE, "all transducer dimensions must be >= 1");
+  if (d->cell != RNNTG_CELL_TANH && d->cell != RNNTG_CELL_LSTM)
+    return fail(RNNTG_E_VALUE, "unknown cell");
+  if (d->layers < 1 || d->layers > RNNTG_MAX_LAYERS)
+    return fail(RNNTG_E_VALUE, "layers must lie in [1, 4]");
+  if (d->cell == RNNTG_CELL_TANH && d->layers != 1)
+    return fail(RNNTG_E_VALUE, "the tanh prediction network has exactly one layer");
+  if (d->num_durations < 0 || d->num_durations > RNNTG_MAX_DURATIONS)
+    return fail(RNNTG_E_VALUE, "too many duration classes");
+  if (d->num_durations > 0) {  // model.cpp:69-78
+    if (d->durations[0] != 0 && d->durations[0] != 1)
+      return fail(RNNTG_E_VALUE, "first duration must be 0 or 1");
+    for (int i = 1; i < d->num_durations; ++i)
+      if (d->durations[i] <= d->durations[i - 1])
+        return fail(RNNTG_E_VALUE, "durations must be strictly ascending");
+  }
+  return RNNTG_OK;
+}
+
+int num_weights(const rnntg_dims* d) { return 1 + 3 * d->layers + 3 + (d->num_durations > 0); }
+
+template <typename T>
+cudaError_t upload(DevBuf& mem, T** dst, const std::vector<T>& src) {
+  cudaError_t e = mem.alloc(dst, src.size());
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+// ---------------------------------------------------------------- state
+rnntg_status alloc_state(rnntg_model* m, DevBuf& mem, DevState& s, int algo, int B, int T,
+                         int ms, bool debug) {
+  const DevModel& M = m->dm;
+  s = DevState{};
+  s.B = B;
+  s.Bp = round_up(B, RB);
+  s.nrb = s.Bp / RB;
+  s.T = T;
+  s.ms = ms;
+  s.cap = std::max(1, T * ms);
+  s.algo = algo;
+  s.max_iters = 1000000;  // engine.hpp:249 default while-iteration cap
+  const size_t Bp = s.Bp;
+  CK(mem.alloc(&s.fp, (size_t)B * T * M.Jp));
+  for (int l = 0; l < M.L; ++l)
+    for (int p = 0; p < 2; ++p) {
+      CK(mem.alloc(&s.h[l][p], Bp * M.Hp));
+      if (M.cell == RNNTG_CELL_LSTM) CK(mem.alloc(&s.c[l][p], Bp * M.Hp));
+    }
+  CK(mem.alloc(&s.gp, Bp * M.Jp));
+  int* ints = nullptr;
+  CK(mem.alloc(&ints, Bp * 8));
+  s.last_label = ints;
+  s.accept = ints + Bp;
+  s.done = ints + 2 * Bp;
+  s.need = ints + 3 * Bp;
+  s.active = ints + 4 * Bp;
+  s.t_row = ints + 5 * Bp;
+  s.u_row = ints + 6 * Bp;
+  s.counts = ints + 7 * Bp;
+  CK(mem.alloc(&s.tokens, (size_t)B * s.cap));
+  CK(mem.alloc(&s.frames, (size_t)B * s.cap));
+  CK(mem.alloc(&s.scores, (size_t)B * s.cap));
+  CK(mem.alloc(&s.durs, (size_t)B * s.cap));
+  CK(mem.alloc(&s.part, Bp * M.NCHT));
+  CK(mem.alloc(&s.ctrl, 1));
+  if (debug) {
+    CK(mem.alloc(&s.dbg_logits, Bp * M.NOUT));
+    CK(mem.alloc(&s.dbg_lse, 2 * Bp));
+  }
+  return RNNTG_OK;
+}
+
+size_t joint_smem(const DevModel& M) { return step_smem_bytes(M.Jp); }
+size_t layer_smem(const DevModel& M, int l) { return step_smem_bytes(l == 0 ? M.Hp : 2 * M.Hp); }
+size_t pp_smem(const DevModel& M) { return step_smem_bytes(M.Hp); }
+
+cudaError_t set_smem_attrs(const DevModel& M) {
+  const int big = (int)std::max({joint_smem(M), layer_smem(M, 1), layer_smem(M, 0), pp_smem(M)});
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(pred_layer_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                big)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(pred_layer_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                big)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(pred_proj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                big)) != cudaSuccess)
+    return e;
+  return cudaFuncSetAttribute(joint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+}
+
+// ---------------------------------------------------------------- graph
+struct Builder {
+  cudaGraph_t g;
+  cudaGraphNode_t last = nullptr;
+  bool last_kernel = false;
+  bool pdl = true;
+
+  cudaError_t kernel(const void* fn, dim3 grid, dim3 block, size_t smem, void** args) {
+    cudaGraphNodeParams p{};
+    p.type = cudaGraphNodeTypeKernel;
+    p.kernel.func = const_cast<void*>(fn);
+    p.kernel.gridDim = grid;
+    p.kernel.blockDim = block;
+    p.kernel.sharedMemBytes = (unsigned)smem;
+    p.kernel.kernelParams = args;
+    cudaGraphEdgeData e{};
+    if (pdl && last_kernel) {
+      e.from_port = cudaGraphKernelNodePortProgrammatic;
+      e.type = cudaGraphDependencyTypeProgrammatic;
+    }
+    cudaGraphNode_t n;
+    cudaError_t err = cudaGraphAddNode_v2(&n, g, last ? &last : nullptr, last ? &e : nullptr,
+                                          last ? 1 : 0, &p);
+    if (err != cudaSuccess) return err;
+    last = n;
+    last_kernel = true;
+    return cudaSuccess;
+  }
+
+  cudaError_t while_node(cudaGraphConditionalHandle h, cudaGraph_t* body) {
+    cudaGraphNodeParams p{};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    cudaGraphNode_t n;
+    cudaError_t err = cudaGraphAddNode(&n, g, last ? &last : nullptr, last ? 1 : 0, &p);
+    if (err != cudaSuccess) return err;
+    *body = p.conditional.phGraph_out[0];
+    last = n;
+    last_kernel = false;
+    return cudaSuccess;
+  }
+};
+
+void* kargs2(DevModel* m, DevState* s, void** out) {
+  out[0] = m;
+  out[1] = s;
+  return out;
+}
+
+// Adds the prediction step: L layer kernels + pred_proj.
+cudaError_t add_pred_step(Builder& b, rnntg_decoder* d) {
+  const DevModel& M = d->m->dm;
+  const int nrb = d->st.nrb;
+  cudaError_t e;
+  for (int l = 0; l < M.L; ++l) {
+    void* args[3] = {&d->arg_m, &d->arg_s, &d->arg_l[l]};
+    const void* fn = M.cell == RNNTG_CELL_LSTM ? (const void*)pred_layer_kernel<1>
+                                               : (const void*)pred_layer_kernel<0>;
+    if ((e = b.kernel(fn, dim3(M.GH / CT, nrb), dim3(NT), layer_smem(M, l), args)) != cudaSuccess)
+      return e;
+  }
+  void* args[2] = {&d->arg_m, &d->arg_s};
+  return b.kernel((const void*)pred_proj_kernel, dim3(M.Jp / CT, nrb), dim3(NT), pp_smem(M), args);
+}
+
+cudaError_t add_joint(Builder& b, rnntg_decoder* d) {
+  const DevModel& M = d->m->dm;
+  void* args[2] = {&d->arg_m, &d->arg_s};
+  return b.kernel((const void*)joint_kernel, dim3(M.NCHT, d->st.nrb), dim3(NT), joint_smem(M),
+                  args);
+}
+
+cudaError_t add_encproj(Builder& b, rnntg_decoder* d);
+
+cudaError_t build_graph(rnntg_decoder* d) {
+  const bool pdl = env_flag("RNNTG_PDL", true);
+  cudaError_t e;
+  if ((e = cudaGraphCreate(&d->graph, 0)) != cudaSuccess) return e;
+  if ((e = cudaGraphConditionalHandleCreate(&d->st.h_outer, d->graph, 0, 0)) != cudaSuccess)
+    return e;
+  if ((e = cudaGraphConditionalHandleCreate(&d->st.h_inner, d->graph, 0, 0)) != cudaSuccess)
+    return e;
+  d->st.use_cond = 1;
+  d->arg_m = d->m->dm;
+  d->arg_s = d->st;
+  for (int l = 0; l < MAXL; ++l) d->arg_l[l] = l;
+
+  Builder root{d->graph};
+  root.pdl = pdl;
+  if ((e = add_encproj(root, d)) != cudaSuccess) return e;
+  {
+    void* args[2] = {&d->arg_m, &d->arg_s};
+    if ((e = root.kernel((const void*)prologue_kernel, dim3(148), dim3(256), 0, args)) !=
+        cudaSuccess)
+      return e;
+  }
+  if ((e = add_pred_step(root, d)) != cudaSuccess) return e;  // P0 = pred(blank, 0)
+  cudaGraph_t outer_body;
+  if ((e = root.while_node(d->st.h_outer, &outer_body)) != cudaSuccess) return e;
+  Builder ob{outer_body};
+  ob.pdl = pdl;
+  cudaGraph_t inner_body;
+  if ((e = ob.while_node(d->st.h_inner, &inner_body)) != cudaSuccess) return e;
+  Builder ib{inner_body};
+  ib.pdl = pdl;
+  if (d->algo == RNNTG_ALGO_FRAME_SYNC) {
+    // WHILE t < max_len { WHILE any(!blank) && sym < ms { joint; pred } ; tail }
+    if ((e = add_joint(ib, d)) != cudaSuccess) return e;
+    if ((e = add_pred_step(ib, d)) != cudaSuccess) return e;
+    void* args[2] = {&d->arg_m, &d->arg_s};
+    if ((e = ob.kernel((const void*)frame_tail_kernel, dim3(1), dim3(256), 0, args)) !=
+        cudaSuccess)
+      return e;
+  } else {
+    // WHILE any(active) { WHILE any(need) { joint } ; pred (accepted rows) }
+    if ((e = add_joint(ib, d)) != cudaSuccess) return e;
+    if ((e = add_pred_step(ob, d)) != cudaSuccess) return e;
+  }
+  return cudaGraphInstantiate(&d->gexec, d->graph, 0);
+}
+
+}  // namespace
+
+// =====================================================================
+extern "C" {
+
+const char* rnntg_last_error(void) { return g_err.c_str(); }
+int rnntg_abi_version(void) { return RNNTG_ABI_VERSION; }
+
+int rnntg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+rnntg_status rnntg_model_create(int device, const rnntg_dims* dims, const float* const* weights,
+                                int nweights, rnntg_model** out) {
+  if (!out) return fail(RNNTG_E_VALUE, "out is null");
+  *out = nullptr;
+  rnntg_status st = validate_dims(dims);
+  if (st) return st;
+  if (!weights || nweights != num_weights(dims))
+    return fail(RNNTG_E_VALUE, "expected " + std::to_string(num_weights(dims)) + " weight tensors");
+  for (int i = 0; i < nweights; ++i)
+    if (!weights[i]) return fail(RNNTG_E_VALUE, "null weight pointer");
+  if (rnntg_device_count() == 0) return fail(RNNTG_E_CUDA, "no CUDA device");
+  CK(cudaSetDevice(device));
+  auto* m = new rnntg_model;
+  m->device = device;
+  m->dims = *dims;
+  DevModel& M = m->dm;
+  const rnntg_dims& d = *dims;
+  M.V1 = d.vocab + 1;
+  M.E = d.embed;
+  M.H = d.hidden;
+  M.Hp = round_up(d.hidden, 64);
+  M.L = d.layers;
+  M.cell = d.cell;
+  M.G = d.cell == RNNTG_CELL_LSTM ? 4 : 1;
+  M.GH = M.G * M.Hp;
+  M.J = d.joint;
+  M.Jp = round_up(d.joint, 64);
+  M.F = d.feature;
+  M.Fp = round_up(d.feature, 64);
+  M.D = d.num_durations;
+  for (int i = 0; i < M.D; ++i) M.durations[i] = d.durations[i];
+  M.V1p = round_up(M.V1, CT);
+  M.NOUT = M.V1p + (M.D ? CT : 0);
+  M.NCH = M.V1p / CT;
+  M.NCHT = M.NCH + (M.D ? 1 : 0);
+  const int H = M.H, Hp = M.Hp, G = M.G, GH = M.GH, J = M.J, Jp = M.Jp, V1 = M.V1;
+  auto fail_free = [&](rnntg_status s, const std::string& msg) {
+    m->mem.release();
+    delete m;
+    return fail(s, msg);
+  };
+#define CKM(expr)                                                                   \
+  do {                                                                              \
+    cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return fail_free(RNNTG_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+  // gate-column interleave: reference column g*H + u -> u*G + g
+  auto gcol = [&](int refcol) { return (refcol % H) * G + refcol / H; };
+  const int gcols = G * H;
+  for (int l = 0; l < M.L; ++l) {
+    const float* w_ih = weights[1 + 3 * l];
+    const float* w_hh = weights[2 + 3 * l];
+    const float* bias = weights[3 + 3 * l];
+    const int rows = l == 0 ? Hp : 2 * Hp;
+    std::vector<float> W((size_t)rows * GH, 0.0f);
+    const int hh_row0 = l == 0 ? 0 : Hp;
+    for (int k = 0; k < H; ++k)
+      for (int c = 0; c < gcols; ++c) W[(size_t)(hh_row0 + k) * GH + gcol(c)] = w_hh[(size_t)k * gcols + c];
+    if (l > 0)
+      for (int k = 0; k < H; ++k)
+        for (int c = 0; c < gcols; ++c) W[(size_t)k * GH + gcol(c)] = w_ih[(size_t)k * gcols + c];
+    float* dw = nullptr;
+    CKM(upload(m->mem, &dw, W));
+    M.w[l] = dw;
+    std::vector<float> bv(GH, 0.0f);
+    for (int c = 0; c < gcols; ++c) bv[gcol(c)] = bias[c];
+    float* db = nullptr;
+    CKM(upload(m->mem, &db, bv));
+    M.bias[l] = db;
+  }
+  {  // table0 = embedding @ W_ih0 (exact sequential k, on device)
+    std::vector<float> emb(weights[0], weights[0] + (size_t)V1 * M.E);
+    std::vector<float> wih(weights[1], weights[1] + (size_t)M.E * gcols);
+    float *demb = nullptr, *dwih = nullptr, *dtab = nullptr;
+    CKM(upload(m->mem, &demb, emb));
+    CKM(upload(m->mem, &dwih, wih));
+    CKM(m->mem.alloc(&dtab, (size_t)V1 * GH));
+    table0_kernel<<<dim3((gcols + 127) / 128, V1), 128>>>(demb, dwih, dtab, V1, M.E, gcols, G, H,
+                                                          Hp);
+    CKM(cudaGetLastError());
+    CKM(cudaDeviceSynchronize());
+    M.table0 = dtab;
+  }
+  const int base = 1 + 3 * M.L;
+  {
+    std::vector<float> pp((size_t)Hp * Jp, 0.0f);
+    for (int k = 0; k < H; ++k)
+      for (int j = 0; j < J; ++j) pp[(size_t)k * Jp + j] = weights[base + 1][(size_t)k * J + j];
+    float* dp = nullptr;
+    CKM(upload(m->mem, &dp, pp));
+    M.pred_proj = dp;
+  }
+  {
+    std::vector<float> oe((size_t)Jp * M.NOUT, 0.0f);
+    for (int k = 0; k < J; ++k) {
+      for (int v = 0; v < V1; ++v) oe[(size_t)k * M.NOUT + v] = weights[base + 2][(size_t)k * V1 + v];
+      for (int c = 0; c < M.D; ++c)
+        oe[(size_t)k * M.NOUT + M.V1p + c] = weights[base + 3][(size_t)k * M.D + c];
+    }
+    float* dp = nullptr;
+    CKM(upload(m->mem, &dp, oe));
+    M.out_ext = dp;
+  }
+  {
+    std::vector<float> en((size_t)M.Fp * Jp, 0.0f);
+    for (int k = 0; k < M.F; ++k)
+      for (int j = 0; j < J; ++j) en[(size_t)k * Jp + j] = weights[base][(size_t)k * J + j];
+    float* dp = nullptr;
+    CKM(upload(m->mem, &dp, en));
+    M.enc = dp;
+    // tcgen05 operands: enc^T K-major [Jp][Fp], split into tf32 hi / lo
+    std::vector<float> hi((size_t)Jp * M.Fp, 0.0f), lo((size_t)Jp * M.Fp, 0.0f);
+    for (int k = 0; k < M.F; ++k)
+      for (int j = 0; j < J; ++j) {
+        const float v = weights[base][(size_t)k * J + j];
+        float h;
+        uint32_t u;
+        std::memcpy(&u, &v, 4);
+        u &= 0xffffe000u;
+        std::memcpy(&h, &u, 4);
+        hi[(size_t)j * M.Fp + k] = h;
+        lo[(size_t)j * M.Fp + k] = v - h;
+      }
+    float *dh = nullptr, *dl = nullptr;
+    CKM(upload(m->mem, &dh, hi));
+    CKM(upload(m->mem, &dl, lo));
+    M.enc_hi = dh;
+    M.enc_lo = dl;
+  }
+  CKM(set_smem_attrs(M));
+  m->tc_ok = encproj_tc_supported(M);
+#undef CKM
+  *out = m;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_model_destroy(rnntg_model* m) {
+  if (!m) return RNNTG_OK;
+  cudaSetDevice(m->device);
+  m->mem.release();
+  delete m;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_decoder_create(rnntg_model* m, int algo, int exec, int batch, int max_frames,
+                                  int max_symbols, rnntg_decoder** out) {
+  if (!out) return fail(RNNTG_E_VALUE, "out is null");
+  *out = nullptr;
+  if (!m) return fail(RNNTG_E_STATE, "model is null");
+  if (batch < 1 || max_frames < 1) return fail(RNNTG_E_VALUE, "batch and frames must be >= 1");
+  if (max_symbols < 1) return fail(RNNTG_E_VALUE, "max_symbols must be >= 1");
+  if (batch > RB * MAXRB) return fail(RNNTG_E_VALUE, "batch must be <= 1024 per decoder");
+  if (algo < 0 || algo > 2) return fail(RNNTG_E_VALUE, "unknown algo");
+  if (algo == RNNTG_ALGO_TDT_LABEL_LOOP && m->dm.D == 0)
+    return fail(RNNTG_E_STATE, "duration-head decoding needs a model with a duration head");
+  if (exec != RNNTG_EXEC_GRAPH && exec != RNNTG_EXEC_PERSISTENT)
+    return fail(RNNTG_E_VALUE, "unknown exec mode");
+  CK(cudaSetDevice(m->device));
+  auto* d = new rnntg_decoder;
+  d->m = m;
+  d->algo = algo;
+  d->exec = exec;
+  d->B = batch;
+  d->T = max_frames;
+  d->ms = max_symbols;
+  rnntg_status st = alloc_state(m, d->mem, d->st, algo, batch, max_frames, max_symbols, false);
+  cudaError_t e = cudaSuccess;
+  if (!st) {
+    if ((e = d->mem.alloc(&d->x_dev, (size_t)batch * max_frames * m->dm.F)) == cudaSuccess &&
+        (e = d->mem.alloc(&d->len_dev, (size_t)batch)) == cudaSuccess &&
+        (e = cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking)) == cudaSuccess &&
+        (e = cudaEventCreate(&d->ev0)) == cudaSuccess &&
+        (e = cudaEventCreate(&d->ev1)) == cudaSuccess) {
+      d->st.x = d->x_dev;
+      d->st.out_len = d->len_dev;
+      if (exec == RNNTG_EXEC_GRAPH) e = build_graph(d);
+      else st = fail(RNNTG_E_STATE, "persistent executor not available in this build");
+    }
+  }
+  if (!st && e != cudaSuccess) st = fail(RNNTG_E_CUDA, std::string("decoder setup: ") + cudaGetErrorString(e));
+  if (st) {
+    rnntg_decoder_destroy(d);
+    return st;
+  }
+  *out = d;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_decoder_destroy(rnntg_decoder* d) {
+  if (!d) return RNNTG_OK;
+  cudaSetDevice(d->m->device);
+  if (d->stream) cudaStreamSynchronize(d->stream);
+  if (d->gexec) cudaGraphExecDestroy(d->gexec);
+  if (d->graph) cudaGraphDestroy(d->graph);
+  if (d->ev0) cudaEventDestroy(d->ev0);
+  if (d->ev1) cudaEventDestroy(d->ev1);
+  if (d->stream) cudaStreamDestroy(d->stream);
+  d->mem.release();
+  delete d;
+  return RNNTG_OK;
+}
+
+int rnntg_decoder_capacity(const rnntg_decoder* d) { return d ? d->st.cap : 0; }
+void* rnntg_decoder_stream(rnntg_decoder* d) { return d ? (void*)d->stream : nullptr; }
+
+static rnntg_status check_lengths(const rnntg_decoder* d, const int32_t* out_len) {
+  for (int b = 0; b < d->B; ++b)
+    if (out_len[b] < 0 || out_len[b] > d->T)  // decoders.cpp:136-140
+      return fail(RNNTG_E_DIMENSION, "out_len entries must lie in [0, frames]");
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_bind(rnntg_decoder* d, const float* x, const int32_t* out_len) {
+  if (!d) return fail(RNNTG_E_STATE, "decoder is null");
+  if (!x || !out_len) return fail(RNNTG_E_DIMENSION, "null input");
+  rnntg_status st = check_lengths(d, out_len);
+  if (st) return st;
+  CK(cudaSetDevice(d->m->device));
+  CK(cudaMemcpyAsync(d->x_dev, x, sizeof(float) * (size_t)d->B * d->T * d->m->dm.F,
+                     cudaMemcpyHostToDevice, d->stream));
+  CK(cudaMemcpyAsync(d->len_dev, out_len, sizeof(int32_t) * d->B, cudaMemcpyHostToDevice,
+                     d->stream));
+  d->bound = true;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_bind_device(rnntg_decoder* d, const float* x_dev, const int32_t* len_dev) {
+  if (!d) return fail(RNNTG_E_STATE, "decoder is null");
+  if (!x_dev || !len_dev) return fail(RNNTG_E_DIMENSION, "null input");
+  CK(cudaSetDevice(d->m->device));
+  std::vector<int32_t> lens(d->B);
+  CK(cudaMemcpyAsync(lens.data(), len_dev, sizeof(int32_t) * d->B, cudaMemcpyDeviceToHost,
+                     d->stream));
+  CK(cudaStreamSynchronize(d->stream));
+  rnntg_status st = check_lengths(d, lens.data());
+  if (st) return st;
+  CK(cudaMemcpyAsync(d->x_dev, x_dev, sizeof(float) * (size_t)d->B * d->T * d->m->dm.F,
+                     cudaMemcpyDeviceToDevice, d->stream));
+  CK(cudaMemcpyAsync(d->len_dev, len_dev, sizeof(int32_t) * d->B, cudaMemcpyDeviceToDevice,
+                     d->stream));
+  d->bound = true;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_launch(rnntg_decoder* d) {
+  if (!d) return fail(RNNTG_E_STATE, "decoder is null");
+  if (!d->bound) return fail(RNNTG_E_STATE, "captured decoder is not initialized (no inputs bound)");
+  CK(cudaSetDevice(d->m->device));
+  CK(cudaEventRecord(d->ev0, d->stream));
+  CK(cudaGraphLaunch(d->gexec, d->stream));
+  CK(cudaEventRecord(d->ev1, d->stream));
+  d->launched = true;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_sync(rnntg_decoder* d) {
+  if (!d) return fail(RNNTG_E_STATE, "decoder is null");
+  CK(cudaSetDevice(d->m->device));
+  CK(cudaStreamSynchronize(d->stream));
+  if (d->launched) {
+    int err = 0;
+    CK(cudaMemcpy(&err, &d->st.ctrl->err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err == ERR_RUNAWAY) return fail(RNNTG_E_RUNAWAY, "while node exceeded the iteration cap");
+  }
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_read(rnntg_decoder* d, int32_t* counts, int32_t* tokens, int32_t* frames,
+                        float* scores, int32_t* durations, int cap) {
+  if (!d) return fail(RNNTG_E_STATE, "decoder is null");
+  rnntg_status st = rnntg_sync(d);
+  if (st) return st;
+  const int B = d->B, dc = d->st.cap;
+  if (cap < 1) return fail(RNNTG_E_VALUE, "cap must be >= 1");
+  std::vector<int32_t> cnt(B);
+  CK(cudaMemcpy(cnt.data(), d->st.counts, sizeof(int32_t) * B, cudaMemcpyDeviceToHost));
+  if (counts) std::memcpy(counts, cnt.data(), sizeof(int32_t) * B);
+  const int w = std::min(cap, dc);
+  auto copy2d = [&](void* dst, const void* src, size_t es) -> cudaError_t {
+    if (!dst) return cudaSuccess;
+    return cudaMemcpy2D(dst, es * cap, src, es * dc, es * w, B, cudaMemcpyDeviceToHost);
+  };
+  CK(copy2d(tokens, d->st.tokens, 4));
+  CK(copy2d(frames, d->st.frames, 4));
+  CK(copy2d(scores, d->st.scores, 4));
+  CK(copy2d(durations, d->st.durs, 4));
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_get_stats(rnntg_decoder* d, rnntg_stats* s) {
+  if (!d || !s) return fail(RNNTG_E_STATE, "null argument");
+  rnntg_status st = rnntg_sync(d);
+  if (st) return st;
+  Ctrl c;
+  CK(cudaMemcpy(&c, d->st.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+  std::vector<int32_t> cnt(d->B);
+  CK(cudaMemcpy(cnt.data(), d->st.counts, sizeof(int32_t) * d->B, cudaMemcpyDeviceToHost));
+  s->joint_evals = c.joint_evals;
+  s->pred_steps = c.pred_steps;
+  s->outer_iters = c.outer_iters;
+  s->emitted = 0;
+  for (int v : cnt) s->emitted += v;
+  s->gpu_ms = 0.0f;
+  if (d->launched) CK(cudaEventElapsedTime(&s->gpu_ms, d->ev0, d->ev1));
+  return RNNTG_OK;
+}
+
+// ---------------------------------------------------------------- step API
+rnntg_status rnntg_step_joint(rnntg_model* m, int batch, const float* f, const float* g,
+                              float* logp, float* dur_logp) {
+  if (!m) return fail(RNNTG_E_STATE, "model is null");
+  if (batch < 1 || batch > RB * MAXRB) return fail(RNNTG_E_VALUE, "bad batch");
+  if (!f || !g || !logp) return fail(RNNTG_E_DIMENSION, "null buffer");
+  CK(cudaSetDevice(m->device));
+  const DevModel& M = m->dm;
+  DevBuf mem;
+  DevState s;
+  rnntg_status st = alloc_state(m, mem, s, RNNTG_ALGO_FRAME_SYNC, batch, 1, 1, true);
+  if (st) {
+    mem.release();
+    return st;
+  }
+  float* xd = nullptr;
+  int* lens = nullptr;
+  auto run = [&]() -> rnntg_status {
+    CK(mem.alloc(&xd, (size_t)batch * M.F));
+    CK(mem.alloc(&lens, (size_t)batch));
+    CK(cudaMemcpy(xd, f, sizeof(float) * batch * M.F, cudaMemcpyHostToDevice));
+    s.x = xd;
+    s.out_len = lens;
+    s.use_cond = 0;
+    // encoder projection of the B single-frame rows
+    CK(launch_encproj(M, m->tc_ok, xd, s.fp, batch, 0));
+    // h_top' rows = g (state parity 0 -> next buffer is 1)
+    CK(cudaMemcpy2D(s.h[M.L - 1][1], sizeof(float) * M.Hp, g, sizeof(float) * M.H,
+                    sizeof(float) * M.H, batch, cudaMemcpyHostToDevice));
+    std::vector<int> ones(batch, 1), zeros(batch, 0);
+    CK(cudaMemcpy(s.accept, ones.data(), sizeof(int) * batch, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(s.done, zeros.data(), sizeof(int) * batch, cudaMemcpyHostToDevice));
+    CK(cudaMemset(s.ctrl, 0, sizeof(Ctrl)));
+    pred_proj_kernel<<<dim3(M.Jp / CT, s.nrb), NT, pp_smem(M)>>>(M, s);
+    CK(cudaGetLastError());
+    joint_kernel<<<dim3(M.NCHT, s.nrb), NT, joint_smem(M)>>>(M, s);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    std::vector<float> lg((size_t)s.Bp * M.NOUT), lse(2 * s.Bp);
+    CK(cudaMemcpy(lg.data(), s.dbg_logits, sizeof(float) * lg.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(lse.data(), s.dbg_lse, sizeof(float) * lse.size(), cudaMemcpyDeviceToHost));
+    for (int b = 0; b < batch; ++b) {
+      for (int v = 0; v < M.V1; ++v) logp[(size_t)b * M.V1 + v] = lg[(size_t)b * M.NOUT + v] - lse[b];
+      if (dur_logp && M.D)
+        for (int c = 0; c < M.D; ++c)
+          dur_logp[(size_t)b * M.D + c] = lg[(size_t)b * M.NOUT + M.V1p + c] - lse[s.Bp + b];
+    }
+    return RNNTG_OK;
+  };
+  st = run();
+  mem.release();
+  return st;
+}
+
+rnntg_status rnntg_step_prediction(rnntg_model* m, int batch, const int32_t* labels,
+                                   const float* state, float* state_out) {
+  if (!m) return fail(RNNTG_E_STATE, "model is null");
+  if (batch < 1 || batch > RB * MAXRB) return fail(RNNTG_E_VALUE, "bad batch");
+  if (!labels || !state || !state_out) return fail(RNNTG_E_DIMENSION, "null buffer");
+  const DevModel& M = m->dm;
+  for (int b = 0; b < batch; ++b)
+    if (labels[b] < 0 || labels[b] >= M.V1)  // embedding_lookup_into, tensor.cpp:499-502
+      return fail(RNNTG_E_INDEX, "embedding id " + std::to_string(labels[b]) + " out of range");
+  CK(cudaSetDevice(m->device));
+  DevBuf mem;
+  DevState s;
+  rnntg_status st = alloc_state(m, mem, s, RNNTG_ALGO_FRAME_SYNC, batch, 1, 1, false);
+  if (st) {
+    mem.release();
+    return st;
+  }
+  const bool lstm = M.cell == RNNTG_CELL_LSTM;
+  const int W = lstm ? 2 * M.L * M.H : M.H;
+  auto run = [&]() -> rnntg_status {
+    for (int l = 0; l < M.L; ++l) {
+      const int ho = lstm ? 2 * l * M.H : 0;
+      CK(cudaMemcpy2D(s.h[l][0], sizeof(float) * M.Hp, state + ho, sizeof(float) * W,
+                      sizeof(float) * M.H, batch, cudaMemcpyHostToDevice));
+      if (lstm)
+        CK(cudaMemcpy2D(s.c[l][0], sizeof(float) * M.Hp, state + ho + M.H, sizeof(float) * W,
+                        sizeof(float) * M.H, batch, cudaMemcpyHostToDevice));
+    }
+    std::vector<int> ones(batch, 1);
+    CK(cudaMemcpy(s.accept, ones.data(), sizeof(int) * batch, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(s.last_label, labels, sizeof(int) * batch, cudaMemcpyHostToDevice));
+    CK(cudaMemset(s.ctrl, 0, sizeof(Ctrl)));
+    s.use_cond = 0;
+    for (int l = 0; l < M.L; ++l) {
+      if (lstm)
+        pred_layer_kernel<1><<<dim3(M.GH / CT, s.nrb), NT, layer_smem(M, l)>>>(M, s, l);
+      else
+        pred_layer_kernel<0><<<dim3(M.GH / CT, s.nrb), NT, layer_smem(M, l)>>>(M, s, l);
+      CK(cudaGetLastError());
+    }
+    CK(cudaDeviceSynchronize());
+    for (int l = 0; l < M.L; ++l) {
+      const int ho = lstm ? 2 * l * M.H : 0;
+      CK(cudaMemcpy2D(state_out + ho, sizeof(float) * W, s.h[l][1], sizeof(float) * M.Hp,
+                      sizeof(float) * M.H, batch, cudaMemcpyDeviceToHost));
+      if (lstm)
+        CK(cudaMemcpy2D(state_out + ho + M.H, sizeof(float) * W, s.c[l][1], sizeof(float) * M.Hp,
+                        sizeof(float) * M.H, batch, cudaMemcpyDeviceToHost));
+    }
+    return RNNTG_OK;
+  };
+  st = run();
+  mem.release();
+  return st;
+}
+
+rnntg_status rnntg_time_kernel(rnntg_decoder* d, int which, int reps, float* avg_ms) {
+  if (!d || !avg_ms || reps < 1) return fail(RNNTG_E_VALUE, "bad arguments");
+  CK(cudaSetDevice(d->m->device));
+  const DevModel& M = d->m->dm;
+  DevState s = d->st;
+  s.use_cond = 0;
+  s.max_iters = (long long)1 << 60;
+  cudaStream_t st = d->stream;
+  auto launch_one = [&]() -> cudaError_t {
+    if (which == 0) return launch_encproj(M, d->m->tc_ok, d->x_dev, s.fp, d->B * d->T, st);
+    if (which >= 1 && which <= M.L) {
+      const int l = which - 1;
+      if (M.cell == RNNTG_CELL_LSTM)
+        pred_layer_kernel<1><<<dim3(M.GH / CT, s.nrb), NT, layer_smem(M, l), st>>>(M, s, l);
+      else
+        pred_layer_kernel<0><<<dim3(M.GH / CT, s.nrb), NT, layer_smem(M, l), st>>>(M, s, l);
+      return cudaGetLastError();
+    }
+    if (which == 8) {
+      pred_proj_kernel<<<dim3(M.Jp / CT, s.nrb), NT, pp_smem(M), st>>>(M, s);
+      return cudaGetLastError();
+    }
+    if (which == 9) {
+      timing_prep_kernel<<<1, 256, 0, st>>>(s);
+      joint_kernel<<<dim3(M.NCHT, s.nrb), NT, joint_smem(M), st>>>(M, s);
+      return cudaGetLastError();
+    }
+    return cudaErrorInvalidValue;
+  };
+  timing_prep_kernel<<<1, 256, 0, st>>>(s);
+  CK(cudaGetLastError());
+  CK(launch_one());  // warm
+  CK(cudaStreamSynchronize(st));
+  float total = 0.0f;
+  for (int r = 0; r < reps; ++r) {
+    if (which == 9) {
+      timing_prep_kernel<<<1, 256, 0, st>>>(s);
+      CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(d->ev0, st));
+    if (which == 9) {
+      joint_kernel<<<dim3(M.NCHT, s.nrb), NT, joint_smem(M), st>>>(M, s);
+      CK(cudaGetLastError());
+    } else {
+      CK(launch_one());
+    }
+    CK(cudaEventRecord(d->ev1, st));
+    CK(cudaEventSynchronize(d->ev1));
+    float ms = 0.0f;
+    CK(cudaEventElapsedTime(&ms, d->ev0, d->ev1));
+    total += ms;
+  }
+  *avg_ms = total / reps;
+  d->launched = false;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_enc_proj(rnntg_model* m, int rows, const float* x, float* fp) {
+  if (!m) return fail(RNNTG_E_STATE, "model is null");
+  if (rows < 1 || !x || !fp) return fail(RNNTG_E_DIMENSION, "bad arguments");
+  CK(cudaSetDevice(m->device));
+  const DevModel& M = m->dm;
+  DevBuf mem;
+  float *xd = nullptr, *od = nullptr;
+  auto run = [&]() -> rnntg_status {
+    CK(mem.alloc(&xd, (size_t)rows * M.F));
+    CK(mem.alloc(&od, (size_t)rows * M.Jp));
+    CK(cudaMemcpy(xd, x, sizeof(float) * rows * M.F, cudaMemcpyHostToDevice));
+    CK(launch_encproj(M, m->tc_ok, xd, od, rows, 0));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy2D(fp, sizeof(float) * M.J, od, sizeof(float) * M.Jp, sizeof(float) * M.J, rows,
+                    cudaMemcpyDeviceToHost));
+    return RNNTG_OK;
+  };
+  rnntg_status st = run();
+  mem.release();
+  return st;
+}
+
+}  // extern "C"
+
+namespace {
+cudaError_t add_encproj(Builder& b, rnntg_decoder* d) {
+  const DevModel& M = d->m->dm;
+  const int rows = d->B * d->T;
+  return encproj_add_node(b.g, &b.last, &b.last_kernel, M, d->m->tc_ok, d->x_dev, d->st.fp, rows);
+}
+}  // namespace

@@ -1,0 +1,199 @@
+"""GPU parity: the CUDA decoder (through the C ABI) against the CPU oracle.
+
+Mirrors the reference's own decoder tests (tests/test_decoders.cpp,
+tests/acceptance.cpp criteria 1-2) with the comparator of tests/parity.py.
+"""
+import gzip
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.parity import EPS_MARGIN, RTOL, ParityReport, compare_batch, rel_err
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2406_03791_b200")
+from paper_2406_03791_b200 import DecodeAlgo, Model, ModelDims  # noqa: E402
+from paper_2406_03791_b200 import decoders as D  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "reference_golden.json.gz")
+
+
+def _need_gpu():
+    if P._lib.lib().rnntg_device_count() < 1:
+        pytest.fail("no CUDA device visible: GPU tests must run on the B200")
+
+
+def to_model_dims(d: O.Dims) -> ModelDims:
+    return ModelDims(d.vocab, d.embed, d.hidden, d.joint, d.feature, tuple(d.durations),
+                     "lstm" if d.cell == O.CELL_LSTM else "tanh", d.layers)
+
+
+@pytest.fixture(scope="module")
+def golden():
+    with gzip.open(GOLD, "rt") as fh:
+        return json.load(fh)
+
+
+def run_case(seed, tdt, algo, report):
+    c = O.random_case(seed, tdt)
+    m = Model(to_model_dims(c.dims), c.params)
+    ref = O.decode_batch(c.dims, c.params, c.x, c.out_len, c.max_symbols, tdt, record=True)
+    cap = D.build_decode_graph(m, algo, c.x.shape[0], c.x.shape[1], c.max_symbols)
+    got = D.replay_decode(cap, c.x, c.out_len)
+    report.merge(compare_batch(got, ref, c.dims.vocab, tdt, f"seed{seed}/{algo.name}"))
+    # replaying the same graph on the same inputs is bit-identical
+    again = D.replay_decode(cap, c.x, c.out_len)
+    assert all(a == b for a, b in zip(got, again))
+    cap.close()
+    m.close()
+    return got
+
+
+def test_device_present():
+    _need_gpu()
+
+
+@pytest.mark.parametrize("algo", [DecodeAlgo.FrameSync, DecodeAlgo.LabelLoop])
+def test_random_cases_rnnt(algo):
+    """acceptance.cpp criterion 1: seeds 1..200."""
+    _need_gpu()
+    rep = ParityReport()
+    for seed in range(1, 201):
+        run_case(seed, False, algo, rep)
+    print(f"\n{algo.name}: {rep.utterances} utts, {rep.exact} exact, {rep.permitted} permitted "
+          f"near-tie divergences (eps {EPS_MARGIN}), max score rel {rep.max_score_rel:.2e}")
+    assert rep.ok, rep.failures[:5]
+    assert rep.permitted <= max(2, rep.utterances // 100)
+
+
+def test_random_cases_tdt():
+    """acceptance.cpp criterion 2: seeds 1000..1199."""
+    _need_gpu()
+    rep = ParityReport()
+    for seed in range(1000, 1200):
+        run_case(seed, True, DecodeAlgo.TdtLabelLoop, rep)
+    print(f"\nTDT: {rep.utterances} utts, {rep.exact} exact, {rep.permitted} permitted")
+    assert rep.ok, rep.failures[:5]
+
+
+def test_pinned_duration_heads(golden):
+    """test_decoders.cpp:351-402: TDT with a pinned duration head == label looping."""
+    _need_gpu()
+    for rec in golden["pinned_durations"]:
+        d = O.Dims(14, 6, 8, 6, 6, tuple(rec["durations"]))
+        p = O.init_params(rec["params_seed"], d)
+        p[7][:, :] = -1.0
+        p[7][:, 0] = 1.0
+        x = O.fill_uniform(rec["x_seed"], -1.0, 1.0, (rec["B"], rec["T"], 6))
+        lens = np.array(rec["out_len"], np.int32)
+        m = Model(to_model_dims(d), p)
+        tdt = D.tdt_label_looping_decode(m, x, lens, rec["tdt_ms"])
+        ll = D.label_looping_decode(m, x, lens, rec["ll_ms"])
+        assert [h.tokens for h in tdt] == [h.tokens for h in ll]
+        assert [h.frames for h in tdt] == [h.frames for h in ll]
+        ref = O.decode_batch(d, p, x, lens, rec["ll_ms"], False, record=True)
+        rep = compare_batch(ll, ref, d.vocab, False, "pinned")
+        assert rep.ok, rep.failures
+        m.close()
+
+
+@pytest.mark.parametrize("idx", range(6))
+def test_lstm_golden(golden, idx):
+    """LSTM configs (C1 dims, C2 dims) against the reference's LstmModel output."""
+    _need_gpu()
+    rec = golden["lstm"][idx]
+    d = O.Dims(rec["vocab"], rec["hidden"], rec["hidden"], rec["joint"], rec["feature"],
+               tuple(rec["durations"]), O.CELL_LSTM, rec["layers"])
+    p = O.init_params(1, d)
+    x = O.fill_uniform(2, -1.0, 1.0, (rec["B"], rec["T"], rec["feature"]))
+    lens = np.array(rec["out_len"], np.int32)
+    tdt = bool(rec["durations"])
+    algo = {"graph_fs": DecodeAlgo.FrameSync, "graph_ll": DecodeAlgo.LabelLoop,
+            "graph_tdt": DecodeAlgo.TdtLabelLoop}[rec["algo"]]
+    m = Model(to_model_dims(d), p)
+    got = D.replay_decode(D.build_decode_graph(m, algo, rec["B"], rec["T"], rec["ms"]), x, lens)
+    ref = O.decode_batch(d, p, x, lens, rec["ms"], tdt, record=True)
+    # the oracle itself is pinned to the golden reference output
+    for h, g in zip(ref, rec["hyps"]):
+        assert h.tokens == g["tokens"] and h.frames == g["frames"]
+    rep = compare_batch(got, ref, d.vocab, tdt, rec["name"])
+    print(f"\n{rec['name']}: {rep.exact}/{rep.utterances} exact, {rep.permitted} permitted, "
+          f"max score rel {rep.max_score_rel:.2e}")
+    assert rep.ok, rep.failures
+
+
+@pytest.mark.parametrize("cell,layers,tdt", [("tanh", 1, False), ("lstm", 2, True),
+                                              ("lstm", 1, False), ("lstm", 3, True)])
+def test_step_joint_and_prediction(cell, layers, tdt):
+    """test_model.cpp:224-270 analogue: kernel logits / states vs the oracle."""
+    _need_gpu()
+    for (V, H, J, F, E) in [(29, 32, 24, 16, 20), (1024, 640, 640, 1024, 640), (7, 5, 4, 3, 6)]:
+        if cell == "lstm":
+            E = H
+        d = O.Dims(V, E, H, J, F, (0, 1, 2, 3, 4) if tdt else (),
+                   O.CELL_LSTM if cell == "lstm" else O.CELL_TANH, layers)
+        p = O.init_params(3, d)
+        m = Model(to_model_dims(d), p)
+        B = 37
+        st = O.fill_uniform(5, -1.0, 1.0, (B, d.state_width))
+        labels = np.array([(i * 7) % (V + 1) for i in range(B)], np.int32)
+        got = m.prediction(labels, st)
+        ref = O.prediction(d, p, labels, st)
+        assert np.max(np.abs(got - ref)) < 2e-5
+        f = O.fill_uniform(6, -1.0, 1.0, (B, F))
+        off = 0 if cell == "tanh" else 2 * (layers - 1) * H
+        g = np.ascontiguousarray(ref[:, off:off + H])
+        lg, dl = m.joint(f, g)
+        rl, rdl = O.joint(d, p, f, ref)
+        assert rel_err(lg, rl) < RTOL, rel_err(lg, rl)
+        if tdt:
+            assert rel_err(dl, rdl) < RTOL
+        m.close()
+
+
+def test_enc_proj_precision():
+    """K1 against a float64 restatement (3xTF32 budget: well inside 1e-4)."""
+    _need_gpu()
+    d = O.Dims(1024, 640, 640, 640, 1024, (), O.CELL_LSTM, 2)
+    p = O.init_params(1, d)
+    m = Model(to_model_dims(d), p)
+    x = O.fill_uniform(2, -1.0, 1.0, (300, 1024))
+    got = m.enc_proj(x)
+    ref = x.astype(np.float64) @ p[7].astype(np.float64)
+    err = np.max(np.abs(got - ref)) / np.max(np.abs(ref))
+    assert err < 1e-5, err
+    m.close()
+
+
+def test_full_size_properties():
+    """C2 (B=32, T=250, 2x640 LSTM, V=1025): properties at full size --
+    frame-sync == label-looping bitwise, batch independence, determinism,
+    timestamps monotone, counts <= T*ms."""
+    _need_gpu()
+    dims = ModelDims(1024, 640, 640, 640, 1024, (), "lstm", 2)
+    m = Model.from_seed(dims, 1)
+    from paper_2406_03791_b200 import synth
+    B, T = 32, 250
+    x = synth.encoder_outputs(2, B, T, 1024)
+    lens = np.full(B, T, np.int32)
+    lens[5] = 100
+    lens[9] = 0
+    fs = D.greedy_decode_sync_free(m, x, lens, 5)
+    fs2 = D.greedy_decode_sync_free(m, x, lens, 5)
+    assert all(a == b for a, b in zip(fs, fs2))
+    ll = D.label_looping_decode(m, x, lens, 5)
+    assert all(a.tokens == b.tokens and a.frames == b.frames for a, b in zip(fs, ll))
+    for b, h in enumerate(fs):
+        assert len(h.tokens) <= lens[b] * 5
+        assert all(0 <= t < 1025 - 1 for t in h.tokens)
+        assert all(h.frames[i] <= h.frames[i + 1] for i in range(len(h.frames) - 1))
+        assert all(0 <= f < max(lens[b], 1) for f in h.frames)
+    assert len(fs[9].tokens) == 0
+    # batch independence: a sub-batch decodes identically
+    sub = D.greedy_decode_sync_free(m, np.ascontiguousarray(x[3:7]), lens[3:7], 5)
+    assert all(a == b for a, b in zip(sub, fs[3:7]))
+    m.close()
