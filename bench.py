@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--exec", default="graph", choices=["graph", "persistent"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-compare", action="store_true",
+                    help="skip timing the other executor (graph vs persistent)")
     ap.add_argument("--blank-bias", type=float, default=0.0)
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="target duration of the bounded CPU reference sample")
@@ -197,6 +199,112 @@ def run_reference_arm(args, cfg, rank, world):
     print(json.dumps(out), flush=True)
 
 
+def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent):
+    """Dominant kernel's achieved bandwidth / FLOP rate, measured with CUDA
+    events on standalone launches of the decoder's own kernels."""
+    from paper_2406_03791_b200._lib import check
+    algo, B, T, ms, durs, L, H, J, V, F, scaling = cfg
+    kern = {}
+    names = {0: "enc_proj"}
+    if persistent:
+        names[10] = "persistent"
+    else:
+        names.update({1: "pred_layer0", 2: "pred_layer1", 8: "pred_proj", 9: "joint"})
+    for w, n in names.items():
+        if w in (1, 2) and w - 1 >= L:
+            continue
+        ms_ = C.c_float()
+        check(L_.rnntg_time_kernel(dh, w, 3 if w == 10 else 20, C.byref(ms_)))
+        kern[n] = ms_.value
+    Hp = (H + 63) // 64 * 64
+    Jp = (J + 63) // 64 * 64
+    Bp = (Bl + 31) // 32 * 32
+    V1 = V + 1
+    V1p = (V1 + 15) // 16 * 16
+    Dn = len(durs)
+    # algorithmic weight bytes of one prediction step / one joint step (fp32)
+    pred_w = 4 * (H * 4 * H * (2 * L - 1) + 4 * H * L + H * J)
+    joint_w = 4 * J * (V1 + Dn)
+    bytes_per = {  # algorithmic bytes per launch (weights + activations read + outputs written)
+        "pred_layer1": 4 * (2 * Hp * 4 * Hp + Bp * 2 * Hp + 2 * Bp * Hp * 2),
+        "pred_layer0": 4 * (Hp * 4 * Hp + Bp * Hp + 2 * Bp * Hp * 2 + Bp * 4 * Hp),
+        "pred_proj": 4 * (Hp * Jp + Bp * Hp + Bp * Jp),
+        "joint": 4 * (Jp * V1p + 2 * Bp * Jp),
+        "enc_proj": 4 * (Bl * T * F + F * Jp + Bl * T * Jp),
+        "persistent": st.pred_steps * pred_w + st.joint_evals * joint_w,
+    }
+    pred_f = 2 * Bl * (4 * H * H * (2 * L - 1) + H * J)
+    joint_f = 2 * Bl * J * (V1 + Dn)
+    flops_per = {
+        "pred_layer1": 2 * Bl * 2 * H * 4 * H, "pred_layer0": 2 * Bl * H * 4 * H,
+        "pred_proj": 2 * Bl * H * J, "joint": 2 * Bl * J * V1, "enc_proj": 2 * Bl * T * F * J,
+        "persistent": st.pred_steps * pred_f + st.joint_evals * joint_f,
+    }
+    per_step_counts = {"enc_proj": 1, "pred_layer0": st.pred_steps,
+                       "pred_layer1": st.pred_steps if L > 1 else 0,
+                       "pred_proj": st.pred_steps, "joint": st.joint_evals, "persistent": 1}
+    share = {n: kern[n] * per_step_counts[n] / ms_per_step for n in kern}
+    dom = max(share, key=share.get)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    clk = clk.summary() if hasattr(clk, "summary") else clk
+    sm_mhz = clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+    ach = bytes_per[dom] / (kern[dom] / 1000.0) / 1e9
+    fp32_ach = flops_per[dom] / (kern[dom] / 1000.0) / 1e12
+    # per inner step roofline (north star): max(weight bytes / HBM, FLOPs / FP32 peak)
+    steps = max(st.joint_evals, 1)
+    step_bytes = (st.pred_steps * pred_w + st.joint_evals * joint_w) / steps
+    step_flops = (st.pred_steps * pred_f + st.joint_evals * joint_f) / steps
+    t_step = ms_per_step * 1000.0 / steps
+    t_roof = max(step_bytes / (hbm_peak * 1e3), step_flops / (fp32_peak * 1e6))
+    return {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+            "frac": ach / hbm_peak, "traffic": None,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)",
+            "algorithmic_bytes_per_launch": bytes_per[dom],
+            "avg_launch_us": kern[dom] * 1000.0,
+            "fp32": {"achieved_tflops": fp32_ach, "peak_tflops": fp32_peak,
+                     "frac": fp32_ach / fp32_peak,
+                     "note": "FFMA peak = 148 SM x 128 lanes x 2 x median SM clock under load"},
+            "per_step": {"weight_bytes": step_bytes, "flops": step_flops,
+                         "roofline_us": t_roof, "measured_us": t_step, "frac": t_roof / t_step},
+            "kernel_us": {n: v * 1000.0 for n, v in kern.items()},
+            "step_share": share}, clk
+
+
+def measure_alt_exec(args, L_, model, cfg, xd, ld, Bl, T, frames_all):
+    """Time the other executor (graph <-> persistent) on the same inputs."""
+    import torch
+    from paper_2406_03791_b200._lib import Stats, check
+    algo = cfg[0]
+    other = "graph" if args.exec == "persistent" else "persistent"
+    dh = C.c_void_p()
+    rc = L_.rnntg_decoder_create(model.handle, ALGO_ID[algo], 0 if other == "graph" else 1, Bl, T,
+                                 cfg[3], C.byref(dh))
+    if rc != 0:
+        return {"exec": other, "unavailable": L_.rnntg_last_error().decode()}
+    check(L_.rnntg_bind_device(dh, C.c_void_p(xd.data_ptr()), C.c_void_p(ld.data_ptr())))
+    for _ in range(2):
+        check(L_.rnntg_launch(dh))
+    check(L_.rnntg_sync(dh))
+    n = 3
+    tot = 0.0
+    for _ in range(n):
+        check(L_.rnntg_launch(dh))
+        check(L_.rnntg_sync(dh))
+        s = Stats()
+        check(L_.rnntg_get_stats(dh, C.byref(s)))
+        tot += s.gpu_ms
+    check(L_.rnntg_decoder_destroy(dh))
+    ms = tot / n
+    return {"exec": other, "value": frames_all / (ms / 1000.0), "ms_per_step": ms,
+            "us_per_step": 1000.0 * ms / max(s.joint_evals, 1)}
+
+
 def config_json(args, cfg):
     algo, B, T, ms, durs, L, H, J, V, F, scaling = cfg
     return {"workload": f"{args.config}: Parakeet-1.1B-shaped {ALGO_NAME[algo]} decode "
@@ -277,57 +385,12 @@ def main():
     ms_per_step = total_ms / args.steps
     per_rank_frames = Bl * T
     fs = algo == "fs"
-    launches_per_step = 2 + st.pred_steps * (L + 1) + st.joint_evals + (st.outer_iters if fs else 0)
-
-    # ---- kernel shares + roofline of the dominant kernel (standalone launches) ----
-    kern = {}
-    names = {0: "enc_proj", 1: "pred_layer0", 2: "pred_layer1", 8: "pred_proj", 9: "joint"}
-    for w, n in names.items():
-        if w in (1, 2) and w - 1 >= L:
-            continue
-        ms_ = C.c_float()
-        check(L_.rnntg_time_kernel(dh, w, 20, C.byref(ms_)))
-        kern[n] = ms_.value
-    per_step_counts = {"enc_proj": 1, "pred_layer0": st.pred_steps,
-                       "pred_layer1": st.pred_steps if L > 1 else 0,
-                       "pred_proj": st.pred_steps, "joint": st.joint_evals}
-    share = {n: kern[n] * per_step_counts[n] / ms_per_step for n in kern}
-    dom = max(share, key=share.get)
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    Hp = (H + 63) // 64 * 64
-    Jp = (J + 63) // 64 * 64
-    Bp = (Bl + 31) // 32 * 32
-    V1p = (V + 1 + 15) // 16 * 16
-    bytes_per = {  # algorithmic bytes per launch (weights + activations read + outputs written)
-        "pred_layer1": 4 * (2 * Hp * 4 * Hp + Bp * 2 * Hp + 2 * Bp * Hp * 2),
-        "pred_layer0": 4 * (Hp * 4 * Hp + Bp * Hp + 2 * Bp * Hp * 2 + Bp * 4 * Hp),
-        "pred_proj": 4 * (Hp * Jp + Bp * Hp + Bp * Jp),
-        "joint": 4 * (Jp * V1p + 2 * Bp * Jp),
-        "enc_proj": 4 * (Bl * T * F + F * Jp + Bl * T * Jp),
-    }
-    flops_per = {
-        "pred_layer1": 2 * Bl * 2 * H * 4 * H, "pred_layer0": 2 * Bl * H * 4 * H,
-        "pred_proj": 2 * Bl * H * J, "joint": 2 * Bl * J * (V + 1), "enc_proj": 2 * Bl * T * F * J,
-    }
-    ach = bytes_per[dom] / (kern[dom] / 1000.0) / 1e9
-    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
-    clk = clk.summary() if hasattr(clk, "summary") else clk
-    fp32_peak = 148 * 128 * 2 * (clk.get("sm_mhz") or sm_mhz) * 1e6 / 1e12
-    fp32_ach = flops_per[dom] / (kern[dom] / 1000.0) / 1e12
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-                "frac": ach / hbm_peak, "traffic": None,
-                "algorithmic_bytes_per_launch": bytes_per[dom],
-                "avg_launch_us": kern[dom] * 1000.0,
-                "fp32": {"achieved_tflops": fp32_ach, "peak_tflops": fp32_peak,
-                         "frac": fp32_ach / fp32_peak,
-                         "note": "FFMA peak = 148 SM x 128 lanes x 2 x median SM clock"},
-                "kernel_us": {n: v * 1000.0 for n, v in kern.items()},
-                "step_share": share}
+    persistent = args.exec == "persistent"
+    if persistent:
+        launches_per_step = 2
+    else:
+        launches_per_step = 2 + st.pred_steps * (L + 1) + st.joint_evals + (st.outer_iters if fs else 0)
+    roofline, clk = roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent)
 
     # ---- e2e through the C ABI with host buffers ----
     e2e = None
@@ -362,6 +425,10 @@ def main():
         # verify the e2e decode agrees with the device-input decode
         # (same inputs -> identical counts)
 
+    alt = None
+    if not args.no_compare:
+        alt = measure_alt_exec(args, L_, model, cfg, xd, ld, Bl, T, frames_all)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -387,7 +454,7 @@ def main():
             "gpu_idle_pct": None,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches_per_step * args.steps),
-            "clocks": clk, "step_ms": step_ms,
+            "clocks": clk, "step_ms": step_ms, "alt_exec": alt,
         }
         print(json.dumps(out), flush=True)
     check(L_.rnntg_decoder_destroy(dh))

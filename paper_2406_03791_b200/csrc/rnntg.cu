@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "encproj_tc.cuh"
+#include "persistent.cuh"
 
 using namespace rnntg;
 
@@ -71,7 +72,7 @@ struct rnntg_model {
   rnntg_dims dims{};
   DevModel dm{};
   DevBuf mem;
-  float* w_enc = nullptr;
+  std::vector<std::vector<float>> host_w;  // reference-order weights (persistent packing)
   bool tc_ok = false;   // tcgen05 encoder projection usable on this device
 };
 
@@ -91,6 +92,9 @@ struct rnntg_decoder {
   DevModel arg_m{};
   DevState arg_s{};
   int arg_l[MAXL]{};
+  // persistent executor
+  pk::PParams pp{};
+  size_t psmem = 0;
 };
 
 namespace {
@@ -265,6 +269,130 @@ cudaError_t add_joint(Builder& b, rnntg_decoder* d) {
 }
 
 cudaError_t add_encproj(Builder& b, rnntg_decoder* d);
+
+// Persistent executor setup: per-CTA weight packing (resident in shared
+// memory for the whole decode), chunk-major activation buffers, checks that
+// the model fits (LSTM <= 2 layers or tanh, batch <= 256, smem budget).
+rnntg_status setup_persistent(rnntg_decoder* d) {
+  rnntg_model* m = d->m;
+  const DevModel& M = m->dm;
+  const rnntg_dims& dd = m->dims;
+  const bool lstm = M.cell == RNNTG_CELL_LSTM;
+  if (M.L > 2) return fail(RNNTG_E_VALUE, "persistent executor supports at most 2 layers");
+  if (d->B > pk::MAXB) return fail(RNNTG_E_VALUE, "persistent executor supports batch <= 256");
+  const int umax = lstm ? pk::UMAX_LSTM : pk::UMAX_TANH;
+  const int H = M.H, J = M.J, V1 = M.V1, D = M.D, NJ = V1 + D, Hp = M.Hp, Jp = M.Jp;
+  const int Gc = lstm ? 4 : 1;
+  int G = std::max({(H + umax - 1) / umax, (J + pk::C2 - 1) / pk::C2, (NJ + pk::C2 - 1) / pk::C2, 1});
+  int nsm = 0, optin = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
+  if (G > nsm) return fail(RNNTG_E_VALUE, "model too wide for the persistent executor");
+  const int wfloats = Hp * pk::C1 + (M.L == 2 ? 2 * Hp * pk::C1 : 0) + Hp * pk::C2 + Jp * pk::C2;
+  int ns = 0;
+  for (int cand = pk::MAX_NS; cand >= 2; --cand)
+    if (pk::smem_bytes(wfloats, cand, d->B) <= (size_t)optin) {
+      ns = cand;
+      break;
+    }
+  if (!ns) return fail(RNNTG_E_VALUE, "persistent executor: weights exceed shared memory");
+  d->psmem = pk::smem_bytes(wfloats, ns, d->B);
+  CK(cudaFuncSetAttribute(pk::persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)d->psmem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pk::persistent_kernel, pk::NTH,
+                                                   d->psmem));
+  if (per_sm < 1 || G > per_sm * nsm)
+    return fail(RNNTG_E_VALUE, "persistent executor cannot be co-resident");
+  // ---- pack weights per CTA ----
+  const auto& w = m->host_w;
+  const int L = M.L, bse = 1 + 3 * L;
+  const int off_hh0 = 0, off_w1 = Hp * pk::C1, off_pp = off_w1 + (L == 2 ? 2 * Hp * pk::C1 : 0),
+            off_j = off_pp + Hp * pk::C2;
+  std::vector<float> pack((size_t)G * wfloats, 0.0f), bias((size_t)G * 2 * pk::C1, 0.0f);
+  for (int c = 0; c < G; ++c) {
+    float* P = pack.data() + (size_t)c * wfloats;
+    const int u0 = pk::own_lo(H, c, G), u1 = pk::own_lo(H, c + 1, G);
+    for (int lu = 0; lu < u1 - u0; ++lu)
+      for (int g = 0; g < Gc; ++g) {
+        const int col = lu * Gc + g, rc = g * H + u0 + lu;
+        for (int k = 0; k < H; ++k) {
+          P[off_hh0 + k * pk::C1 + col] = w[2][(size_t)k * Gc * H + rc];
+          if (L == 2) {
+            P[off_w1 + k * pk::C1 + col] = w[4][(size_t)k * Gc * H + rc];
+            P[off_w1 + (Hp + k) * pk::C1 + col] = w[5][(size_t)k * Gc * H + rc];
+          }
+        }
+        bias[(size_t)c * 2 * pk::C1 + col] = w[3][rc];
+        if (L == 2) bias[(size_t)c * 2 * pk::C1 + pk::C1 + col] = w[6][rc];
+      }
+    const int p0 = pk::own_lo(J, c, G), p1 = pk::own_lo(J, c + 1, G);
+    for (int k = 0; k < H; ++k)
+      for (int lj = 0; lj < p1 - p0; ++lj) P[off_pp + k * pk::C2 + lj] = w[bse + 1][(size_t)k * J + p0 + lj];
+    const int n0 = pk::own_lo(NJ, c, G), n1 = pk::own_lo(NJ, c + 1, G);
+    for (int k = 0; k < J; ++k)
+      for (int ln = 0; ln < n1 - n0; ++ln) {
+        const int n = n0 + ln;
+        P[off_j + k * pk::C2 + ln] =
+            n < V1 ? w[bse + 2][(size_t)k * V1 + n] : w[bse + 3][(size_t)k * D + (n - V1)];
+      }
+  }
+  pk::PParams& pp = d->pp;
+  pp = pk::PParams{};
+  pp.G = G;
+  pp.B = d->B;
+  pp.nrb = d->st.nrb;
+  pp.T = d->T;
+  pp.ms = d->ms;
+  pp.cap = d->st.cap;
+  pp.algo = d->algo;
+  pp.L = L;
+  pp.cell = M.cell;
+  pp.H = H;
+  pp.Hp = Hp;
+  pp.J = J;
+  pp.Jp = Jp;
+  pp.V1 = V1;
+  pp.D = D;
+  pp.NJ = NJ;
+  pp.ns = ns;
+  pp.max_iters = d->st.max_iters;
+  for (int i = 0; i < D; ++i) pp.durations[i] = dd.durations[i];
+  pp.wfloats = wfloats;
+  pp.off_hh0 = off_hh0;
+  pp.off_w1 = off_w1;
+  pp.off_pp = off_pp;
+  pp.off_j = off_j;
+  pp.GH = M.GH;
+  pp.Gg = M.G;
+  pp.table0 = M.table0;
+  float* dp = nullptr;
+  CK(upload(d->mem, &dp, pack));
+  pp.wpack = dp;
+  CK(upload(d->mem, &dp, bias));
+  pp.bias = dp;
+  const size_t Bp = d->st.Bp;
+  CK(d->mem.alloc(&pp.h0, Bp * Hp));
+  CK(d->mem.alloc(&pp.h1[0], Bp * Hp));
+  CK(d->mem.alloc(&pp.h1[1], Bp * Hp));
+  CK(d->mem.alloc(&pp.trunk, Bp * Jp));
+  CK(d->mem.alloc(&pp.hh0own, (size_t)G * d->B * pk::C1));
+  CK(d->mem.alloc(&pp.cown, (size_t)G * 2 * d->B * pk::UMAX_TANH));
+  CK(d->mem.alloc(&pp.gpown, (size_t)G * d->B * pk::C2));
+  CK(d->mem.alloc(&pp.partv, (size_t)G * d->B));
+  CK(d->mem.alloc(&pp.partd, (size_t)G * d->B));
+  CK(d->mem.alloc(&pp.bar, 2));
+  pp.fp = d->st.fp;
+  pp.out_len = d->len_dev;
+  pp.tokens = d->st.tokens;
+  pp.frames = d->st.frames;
+  pp.scores = d->st.scores;
+  pp.durs = d->st.durs;
+  pp.counts = d->st.counts;
+  pp.ctrl = d->st.ctrl;
+  (void)Gc;
+  return RNNTG_OK;
+}
 
 cudaError_t build_graph(rnntg_decoder* d) {
   const bool pdl = env_flag("RNNTG_PDL", true);
@@ -462,6 +590,23 @@ rnntg_status rnntg_model_create(int device, const rnntg_dims* dims, const float*
   }
   CKM(set_smem_attrs(M));
   m->tc_ok = encproj_tc_supported(M);
+  {
+    m->host_w.resize(nweights);
+    const rnntg_dims& dd = *dims;
+    const int V1_ = dd.vocab + 1, Gc = dd.cell == RNNTG_CELL_LSTM ? 4 * dd.hidden : dd.hidden;
+    for (int l = 0; l < dd.layers; ++l) {
+      const int in = l == 0 ? dd.embed : dd.hidden;
+      m->host_w[1 + 3 * l].assign(weights[1 + 3 * l], weights[1 + 3 * l] + (size_t)in * Gc);
+      m->host_w[2 + 3 * l].assign(weights[2 + 3 * l], weights[2 + 3 * l] + (size_t)dd.hidden * Gc);
+      m->host_w[3 + 3 * l].assign(weights[3 + 3 * l], weights[3 + 3 * l] + Gc);
+    }
+    const int bse = 1 + 3 * dd.layers;
+    m->host_w[bse + 1].assign(weights[bse + 1], weights[bse + 1] + (size_t)dd.hidden * dd.joint);
+    m->host_w[bse + 2].assign(weights[bse + 2], weights[bse + 2] + (size_t)dd.joint * V1_);
+    if (dd.num_durations)
+      m->host_w[bse + 3].assign(weights[bse + 3],
+                                weights[bse + 3] + (size_t)dd.joint * dd.num_durations);
+  }
 #undef CKM
   *out = m;
   return RNNTG_OK;
@@ -507,7 +652,7 @@ rnntg_status rnntg_decoder_create(rnntg_model* m, int algo, int exec, int batch,
       d->st.x = d->x_dev;
       d->st.out_len = d->len_dev;
       if (exec == RNNTG_EXEC_GRAPH) e = build_graph(d);
-      else st = fail(RNNTG_E_STATE, "persistent executor not available in this build");
+      else st = setup_persistent(d);
     }
   }
   if (!st && e != cudaSuccess) st = fail(RNNTG_E_CUDA, std::string("decoder setup: ") + cudaGetErrorString(e));
@@ -580,7 +725,14 @@ rnntg_status rnntg_launch(rnntg_decoder* d) {
   if (!d->bound) return fail(RNNTG_E_STATE, "captured decoder is not initialized (no inputs bound)");
   CK(cudaSetDevice(d->m->device));
   CK(cudaEventRecord(d->ev0, d->stream));
-  CK(cudaGraphLaunch(d->gexec, d->stream));
+  if (d->exec == RNNTG_EXEC_PERSISTENT) {
+    CK(launch_encproj(d->m->dm, d->m->tc_ok, d->x_dev, d->st.fp, d->B * d->T, d->stream));
+    void* args[1] = {&d->pp};
+    CK(cudaLaunchCooperativeKernel((const void*)pk::persistent_kernel, dim3(d->pp.G), dim3(pk::NTH),
+                                   args, d->psmem, d->stream));
+  } else {
+    CK(cudaGraphLaunch(d->gexec, d->stream));
+  }
   CK(cudaEventRecord(d->ev1, d->stream));
   d->launched = true;
   return RNNTG_OK;
@@ -758,6 +910,12 @@ rnntg_status rnntg_time_kernel(rnntg_decoder* d, int which, int reps, float* avg
   cudaStream_t st = d->stream;
   auto launch_one = [&]() -> cudaError_t {
     if (which == 0) return launch_encproj(M, d->m->tc_ok, d->x_dev, s.fp, d->B * d->T, st);
+    if (which == 10) {  // the persistent decode kernel alone (fp already projected)
+      if (d->exec != RNNTG_EXEC_PERSISTENT) return cudaErrorInvalidValue;
+      void* args[1] = {&d->pp};
+      return cudaLaunchCooperativeKernel((const void*)pk::persistent_kernel, dim3(d->pp.G),
+                                         dim3(pk::NTH), args, d->psmem, st);
+    }
     if (which >= 1 && which <= M.L) {
       const int l = which - 1;
       if (M.cell == RNNTG_CELL_LSTM)

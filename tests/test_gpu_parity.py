@@ -38,11 +38,14 @@ def golden():
         return json.load(fh)
 
 
-def run_case(seed, tdt, algo, report):
+EXECS = [D.Exec.Graph, D.Exec.Persistent]
+
+
+def run_case(seed, tdt, algo, report, exec=D.Exec.Graph):
     c = O.random_case(seed, tdt)
     m = Model(to_model_dims(c.dims), c.params)
     ref = O.decode_batch(c.dims, c.params, c.x, c.out_len, c.max_symbols, tdt, record=True)
-    cap = D.build_decode_graph(m, algo, c.x.shape[0], c.x.shape[1], c.max_symbols)
+    cap = D.build_decode_graph(m, algo, c.x.shape[0], c.x.shape[1], c.max_symbols, exec)
     got = D.replay_decode(cap, c.x, c.out_len)
     report.merge(compare_batch(got, ref, c.dims.vocab, tdt, f"seed{seed}/{algo.name}"))
     # replaying the same graph on the same inputs is bit-identical
@@ -57,26 +60,28 @@ def test_device_present():
     _need_gpu()
 
 
+@pytest.mark.parametrize("exec", EXECS, ids=lambda e: e.name)
 @pytest.mark.parametrize("algo", [DecodeAlgo.FrameSync, DecodeAlgo.LabelLoop])
-def test_random_cases_rnnt(algo):
+def test_random_cases_rnnt(algo, exec):
     """acceptance.cpp criterion 1: seeds 1..200."""
     _need_gpu()
     rep = ParityReport()
     for seed in range(1, 201):
-        run_case(seed, False, algo, rep)
-    print(f"\n{algo.name}: {rep.utterances} utts, {rep.exact} exact, {rep.permitted} permitted "
+        run_case(seed, False, algo, rep, exec)
+    print(f"\n{algo.name}/{exec.name}: {rep.utterances} utts, {rep.exact} exact, {rep.permitted} permitted "
           f"near-tie divergences (eps {EPS_MARGIN}), max score rel {rep.max_score_rel:.2e}")
     assert rep.ok, rep.failures[:5]
     assert rep.permitted <= max(2, rep.utterances // 100)
 
 
-def test_random_cases_tdt():
+@pytest.mark.parametrize("exec", EXECS, ids=lambda e: e.name)
+def test_random_cases_tdt(exec):
     """acceptance.cpp criterion 2: seeds 1000..1199."""
     _need_gpu()
     rep = ParityReport()
     for seed in range(1000, 1200):
-        run_case(seed, True, DecodeAlgo.TdtLabelLoop, rep)
-    print(f"\nTDT: {rep.utterances} utts, {rep.exact} exact, {rep.permitted} permitted")
+        run_case(seed, True, DecodeAlgo.TdtLabelLoop, rep, exec)
+    print(f"\nTDT/{exec.name}: {rep.utterances} utts, {rep.exact} exact, {rep.permitted} permitted")
     assert rep.ok, rep.failures[:5]
 
 
@@ -101,8 +106,9 @@ def test_pinned_duration_heads(golden):
         m.close()
 
 
+@pytest.mark.parametrize("exec", EXECS, ids=lambda e: e.name)
 @pytest.mark.parametrize("idx", range(6))
-def test_lstm_golden(golden, idx):
+def test_lstm_golden(golden, idx, exec):
     """LSTM configs (C1 dims, C2 dims) against the reference's LstmModel output."""
     _need_gpu()
     rec = golden["lstm"][idx]
@@ -114,14 +120,17 @@ def test_lstm_golden(golden, idx):
     tdt = bool(rec["durations"])
     algo = {"graph_fs": DecodeAlgo.FrameSync, "graph_ll": DecodeAlgo.LabelLoop,
             "graph_tdt": DecodeAlgo.TdtLabelLoop}[rec["algo"]]
+    if exec == D.Exec.Persistent and rec["layers"] > 2:
+        pytest.skip("persistent executor supports <= 2 layers")
     m = Model(to_model_dims(d), p)
-    got = D.replay_decode(D.build_decode_graph(m, algo, rec["B"], rec["T"], rec["ms"]), x, lens)
+    got = D.replay_decode(D.build_decode_graph(m, algo, rec["B"], rec["T"], rec["ms"], exec), x,
+                          lens)
     ref = O.decode_batch(d, p, x, lens, rec["ms"], tdt, record=True)
     # the oracle itself is pinned to the golden reference output
     for h, g in zip(ref, rec["hyps"]):
         assert h.tokens == g["tokens"] and h.frames == g["frames"]
     rep = compare_batch(got, ref, d.vocab, tdt, rec["name"])
-    print(f"\n{rec['name']}: {rep.exact}/{rep.utterances} exact, {rep.permitted} permitted, "
+    print(f"\n{rec['name']}/{exec.name}: {rep.exact}/{rep.utterances} exact, {rep.permitted} permitted, "
           f"max score rel {rep.max_score_rel:.2e}")
     assert rep.ok, rep.failures
 
@@ -169,7 +178,8 @@ def test_enc_proj_precision():
     m.close()
 
 
-def test_full_size_properties():
+@pytest.mark.parametrize("exec", EXECS, ids=lambda e: e.name)
+def test_full_size_properties(exec):
     """C2 (B=32, T=250, 2x640 LSTM, V=1025): properties at full size --
     frame-sync == label-looping bitwise, batch independence, determinism,
     timestamps monotone, counts <= T*ms."""
@@ -182,10 +192,10 @@ def test_full_size_properties():
     lens = np.full(B, T, np.int32)
     lens[5] = 100
     lens[9] = 0
-    fs = D.greedy_decode_sync_free(m, x, lens, 5)
-    fs2 = D.greedy_decode_sync_free(m, x, lens, 5)
+    fs = D.greedy_decode_sync_free(m, x, lens, 5, exec)
+    fs2 = D.greedy_decode_sync_free(m, x, lens, 5, exec)
     assert all(a == b for a, b in zip(fs, fs2))
-    ll = D.label_looping_decode(m, x, lens, 5)
+    ll = D.label_looping_decode(m, x, lens, 5, exec)
     assert all(a.tokens == b.tokens and a.frames == b.frames for a, b in zip(fs, ll))
     for b, h in enumerate(fs):
         assert len(h.tokens) <= lens[b] * 5
@@ -194,6 +204,26 @@ def test_full_size_properties():
         assert all(0 <= f < max(lens[b], 1) for f in h.frames)
     assert len(fs[9].tokens) == 0
     # batch independence: a sub-batch decodes identically
-    sub = D.greedy_decode_sync_free(m, np.ascontiguousarray(x[3:7]), lens[3:7], 5)
+    sub = D.greedy_decode_sync_free(m, np.ascontiguousarray(x[3:7]), lens[3:7], 5, exec)
     assert all(a == b for a, b in zip(sub, fs[3:7]))
+    m.close()
+
+
+def test_executors_agree_full_size():
+    """Graph and persistent executors on C2 shapes: identical token/frame
+    sequences (different FMA orders; any near-tie would show up here)."""
+    _need_gpu()
+    dims = ModelDims(1024, 640, 640, 640, 1024, (), "lstm", 2)
+    m = Model.from_seed(dims, 1)
+    from paper_2406_03791_b200 import synth
+    B, T = 32, 250
+    x = synth.encoder_outputs(2, B, T, 1024)
+    lens = np.full(B, T, np.int32)
+    g = D.greedy_decode_sync_free(m, x, lens, 5, D.Exec.Graph)
+    p = D.greedy_decode_sync_free(m, x, lens, 5, D.Exec.Persistent)
+    same = sum(a.tokens == b.tokens and a.frames == b.frames for a, b in zip(g, p))
+    print(f"\nexecutors agree on {same}/{B} utterances")
+    assert same == B
+    for a, b in zip(g, p):
+        assert rel_err(a.scores, b.scores) < RTOL
     m.close()
