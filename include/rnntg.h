@@ -158,6 +158,10 @@ rnntg_status rnntg_step_prediction(rnntg_model* m, int batch,
  *        8 = pred_proj, 9 = joint step. */
 rnntg_status rnntg_time_kernel(rnntg_decoder* d, int which, int reps, float* avg_ms);
 
+/* Persistent executor phase profile (CTA 0, ns per phase, accumulated since
+ * the last call; needs RNNTG_PROF=1 at decoder creation). */
+rnntg_status rnntg_debug_profile(rnntg_decoder* d, unsigned long long* out16);
+
 /* Encoder projection only (K1): fp[M,J] = x[M,F] @ enc_proj, host buffers. */
 rnntg_status rnntg_enc_proj(rnntg_model* m, int rows, const float* x, float* fp);
 

@@ -69,6 +69,7 @@ struct PParams {
   float* gpown;         // [G][B][C2]
   float4* partv;        // [G][B]
   float4* partd;        // [G][B]
+  unsigned long long* prof;  // optional [16] phase times (ns) of CTA 0
   int* tokens;
   int* frames;
   float* scores;
@@ -369,6 +370,15 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
   const float* WJ = sm.w + P.off_j;
   Ring rg{0};
   long long joint_evals = 0, pred_steps = 0, outer_iters = 0, iters = 0;
+  unsigned long long t_last = 0;
+  auto mark = [&](int id) {
+    if (P.prof && cta == 0 && tid == 0) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+      if (t_last) P.prof[id] += now - t_last;
+      t_last = now;
+    }
+  };
   int err = 0;
   __syncthreads();
 
@@ -415,8 +425,11 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
 
   // ---- the prediction step for accepted rows (after decisions) ----
   auto pred_step = [&]() {
+    mark(2);
     cell0();
+    mark(3);
     grid_barrier(P.bar, G);
+    mark(4);
     const int par = sm.misc[4];
     if (P.L == 2) {
       // hh0 for the next step: h0' @ W_hh0 (owned gate columns)
@@ -429,6 +442,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
           }
         });
       }
+      mark(5);
       // layer 1: [h0' | h1] @ W_1, fused LSTM cell; h1 ping-pong
       {
         ASrc A{P.h0, P.Hp, P.h1[par], P.Hp};
@@ -455,8 +469,10 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
         });
       }
       __syncthreads();
+      mark(6);
       if (tid == 0) sm.misc[4] = par ^ 1;
       grid_barrier(P.bar, G);
+      mark(7);
       // pred_proj over h1', trunk
       {
         ASrc A{P.h1[par ^ 1], P.Hp, nullptr, 0};
@@ -486,9 +502,12 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
       });
     }
     __syncthreads();
+    mark(8);
     refresh_trunk(true);
     ++pred_steps;
+    mark(9);
     grid_barrier(P.bar, G);
+    mark(10);
   };
 
   // prologue: P0 = pred(blank, 0) for every row (decoders.cpp:414-430)
@@ -549,7 +568,9 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
     }
     ++joint_evals;
     ++iters;
+    mark(0);
     grid_barrier(P.bar, G);
+    mark(1);
 
     // ---- D: decisions (identical in every CTA) ----
     {
@@ -713,7 +734,9 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
         if (!fs) ++outer_iters;
       } else {
         refresh_trunk(false);
+        mark(11);
         grid_barrier(P.bar, G);
+        mark(12);
       }
       for (int b = tid; b < B; b += NTH) sm.flag[b] &= ~2;
       __syncthreads();

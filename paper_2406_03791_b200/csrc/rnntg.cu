@@ -382,6 +382,17 @@ rnntg_status setup_persistent(rnntg_decoder* d) {
   CK(d->mem.alloc(&pp.partv, (size_t)G * d->B));
   CK(d->mem.alloc(&pp.partd, (size_t)G * d->B));
   CK(d->mem.alloc(&pp.bar, 2));
+  if (env_flag("RNNTG_PROF", false)) CK(d->mem.alloc(&pp.prof, 16));
+  if (const char* e = std::getenv("RNNTG_NS")) {
+    const int want = std::atoi(e);
+    if (want >= 2 && want <= pk::MAX_NS && pk::smem_bytes(wfloats, want, d->B) <= (size_t)optin) {
+      ns = want;
+      pp.ns = ns;
+      d->psmem = pk::smem_bytes(wfloats, ns, d->B);
+      CK(cudaFuncSetAttribute(pk::persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)d->psmem));
+    }
+  }
   pp.fp = d->st.fp;
   pp.out_len = d->len_dev;
   pp.tokens = d->st.tokens;
@@ -960,6 +971,16 @@ rnntg_status rnntg_time_kernel(rnntg_decoder* d, int which, int reps, float* avg
   }
   *avg_ms = total / reps;
   d->launched = false;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_debug_profile(rnntg_decoder* d, unsigned long long* out16) {
+  if (!d || !out16) return fail(RNNTG_E_VALUE, "bad arguments");
+  if (d->exec != RNNTG_EXEC_PERSISTENT || !d->pp.prof)
+    return fail(RNNTG_E_STATE, "profiling needs the persistent executor and RNNTG_PROF=1");
+  CK(cudaStreamSynchronize(d->stream));
+  CK(cudaMemcpy(out16, d->pp.prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  CK(cudaMemset(d->pp.prof, 0, 16 * sizeof(unsigned long long)));
   return RNNTG_OK;
 }
 
