@@ -289,13 +289,9 @@ rnntg_status setup_persistent(rnntg_decoder* d) {
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
   if (G > nsm) return fail(RNNTG_E_VALUE, "model too wide for the persistent executor");
   const int wfloats = Hp * pk::C1 + (M.L == 2 ? 2 * Hp * pk::C1 : 0) + Hp * pk::C2 + Jp * pk::C2;
-  int ns = 0;
-  for (int cand = pk::MAX_NS; cand >= 2; --cand)
-    if (pk::smem_bytes(wfloats, cand, d->B) <= (size_t)optin) {
-      ns = cand;
-      break;
-    }
-  if (!ns) return fail(RNNTG_E_VALUE, "persistent executor: weights exceed shared memory");
+  const int ns = 0;
+  if (pk::smem_bytes(wfloats, ns, d->B) > (size_t)optin)
+    return fail(RNNTG_E_VALUE, "persistent executor: weights exceed shared memory");
   d->psmem = pk::smem_bytes(wfloats, ns, d->B);
   CK(cudaFuncSetAttribute(pk::persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)d->psmem));
@@ -383,16 +379,14 @@ rnntg_status setup_persistent(rnntg_decoder* d) {
   CK(d->mem.alloc(&pp.partd, (size_t)G * d->B));
   CK(d->mem.alloc(&pp.bar, 2));
   if (env_flag("RNNTG_PROF", false)) CK(d->mem.alloc(&pp.prof, 16));
-  if (const char* e = std::getenv("RNNTG_NS")) {
-    const int want = std::atoi(e);
-    if (want >= 2 && want <= pk::MAX_NS && pk::smem_bytes(wfloats, want, d->B) <= (size_t)optin) {
-      ns = want;
-      pp.ns = ns;
-      d->psmem = pk::smem_bytes(wfloats, ns, d->B);
-      CK(cudaFuncSetAttribute(pk::persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)d->psmem));
+  // CTAs owning duration-head columns (joint columns >= V1)
+  pp.dc0 = G;
+  pp.dc1 = G;
+  for (int c = 0; c < G; ++c)
+    if (pk::own_lo(NJ, c + 1, G) > V1) {
+      pp.dc0 = c;
+      break;
     }
-  }
   pp.fp = d->st.fp;
   pp.out_len = d->len_dev;
   pp.tokens = d->st.tokens;
