@@ -1,0 +1,768 @@
+// persistent.cuh — K5: the whole decode loop in ONE cooperative persistent
+// kernel (the "persistent-kernel alternative" to the conditional-node graph).
+//
+// Every CTA (one per SM) keeps its slice of the prediction/joint weights
+// resident in shared memory for the entire decode and streams only the
+// per-step activations through a TMA bulk-copy ring:
+//
+//   owned by CTA c        smem (C2: 2x640 LSTM, J=640, V=1025)
+//   LSTM units [u0,u1)    W_hh0[Hp][20]  (layer-0 recurrent gates)
+//                         W_1 [2Hp][20]  (layer-1 [ih;hh] gates)
+//   pred_proj cols        W_pp[Hp][8]
+//   joint cols            W_J [Jp][8]    (out_proj || dur_proj columns)
+//
+// One inner step (frame-sync) or label-loop iteration:
+//   J   trunk @ W_J -> per-CTA (max, sumexp, best, idx)       -> grid barrier
+//   D   every CTA merges all partials for all rows (redundant,
+//       identical): argmax / lse / decision rules; CTA 0 appends
+//       the hypothesis; layer-0 cell for own units using the
+//       exact table0[label] + precomputed h0 @ W_hh0            -> grid barrier
+//   P1  [h0'|h1] @ W_1 -> layer-1 cell for own units; h0' @ W_hh0
+//       for the next step                                       -> grid barrier
+//   Pp  h1' @ W_pp -> gp (accepted rows) and trunk = relu(fp[t]+gp) -> barrier
+// Steps where no row accepted a label skip the prediction phases (the
+// trunk is refreshed in D instead), exactly like the reference commits
+// prediction state only for accepted rows (decoders.cpp:292-295, 474-482).
+//
+// All per-row control state (labels, cursors, masks) is replicated in every
+// CTA's shared memory and updated identically, so only activations, joint
+// partials and emissions touch global memory.
+#pragma once
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace rnntg {
+namespace pk {
+
+constexpr int KC = 64;          // k per activation chunk
+constexpr int CH_FLOATS = KC * RB;  // 2048 floats = 8 KB per (row block, chunk)
+constexpr int C1 = 20;          // gate columns per CTA (5 LSTM units / 20 tanh units)
+constexpr int C2 = 8;           // pred_proj / joint columns per CTA
+constexpr int UMAX_LSTM = 5;
+constexpr int UMAX_TANH = 20;
+constexpr int NCW = 8;          // consumer warps
+constexpr int NTH = (NCW + 1) * 32;  // + 1 producer warp
+constexpr int MAXB = 256;       // rows per decoder in the persistent path
+constexpr int MAX_NS = 4;
+
+struct PParams {
+  int G;            // CTAs
+  int B, nrb, T, ms, cap, algo, L, cell;
+  int H, Hp, J, Jp, V1, D, NJ;   // NJ = V1 + D joint columns
+  int ns;           // ring slots
+  int dc0, dc1;     // CTAs owning duration columns: [dc0, dc1)
+  long long max_iters;
+  int durations[MAXD];
+  const float* wpack;   // [G][wfloats] packed per-CTA weights
+  int wfloats;          // floats per CTA in wpack
+  int off_hh0, off_w1, off_pp, off_j;  // float offsets inside a CTA's pack
+  const float* bias;    // [G][2][C1] per-CTA bias of owned gate columns (layer 0, 1)
+  const float* table0;  // [V1][GH] (graph-path layout, col = u*G + g)
+  int GH, Gg;           // GH = Gg*Hp
+  const float* fp;      // [B*T][Jp]
+  const int* out_len;
+  float* h0;            // [nrb][Hp/64][64][32] swizzled chunks
+  float* h1[2];         // same, ping-pong
+  float* trunk;         // [nrb][Jp/64][64][32]
+  float* hh0own;        // [G][B][C1]
+  float* cown;          // [G][2][B][UMAX]
+  float* gpown;         // [G][B][C2]
+  float4* partv;        // [B][G]
+  float4* partd;        // [B][G]
+  unsigned long long* prof;  // optional [16] phase times (ns) of CTA 0
+  int* tokens;
+  int* frames;
+  float* scores;
+  int* durs;
+  int* counts;
+  Ctrl* ctrl;
+  unsigned* bar;        // grid barrier word
+};
+
+__host__ __device__ inline int own_lo(int n, int c, int G) { return (int)((long long)n * c / G); }
+
+// Shared-memory layout (bytes): [weights][ring ns x 8KB][red 4 x 32 x C1][ctrl][mbarriers]
+struct Smem {
+  float* w;
+  float* ring;
+  float* red;
+  int* label;
+  int* tb;
+  int* ub;
+  int* flag;     // bit0 done(FS)/!active(LL), bit1 accept, bit2 need-decision
+  int* kdec;     // decided label per row (this step)
+  float* vdec;   // score
+  int* ddec;     // duration value
+  int* misc;     // [0]=any accept, [1]=any live, [2]=t, [3]=sym, [4]=par, [5]=finish
+  uint64_t* full;
+  uint64_t* empty;
+  uint64_t* wbar;
+};
+
+__host__ __device__ inline size_t smem_bytes(int wfloats, int ns, int B) {
+  size_t b = (size_t)wfloats * 4 + (size_t)ns * CH_FLOATS * 4 + 4 * RB * C1 * 4;
+  b += (size_t)B * 4 * 7 + 64;
+  b = (b + 15) / 16 * 16;
+  b += 8 * (2 * MAX_NS + 1);
+  return b;
+}
+
+__device__ inline Smem carve_p(unsigned char* base, const PParams& P) {
+  Smem s;
+  s.w = reinterpret_cast<float*>(base);
+  s.ring = s.w + P.wfloats;
+  s.red = s.ring + P.ns * CH_FLOATS;
+  int* ip = reinterpret_cast<int*>(s.red + 4 * RB * C1);
+  s.label = ip;
+  s.tb = ip + P.B;
+  s.ub = ip + 2 * P.B;
+  s.flag = ip + 3 * P.B;
+  s.kdec = ip + 4 * P.B;
+  s.vdec = reinterpret_cast<float*>(ip + 5 * P.B);
+  s.ddec = ip + 6 * P.B;
+  s.misc = ip + 7 * P.B;
+  size_t off = (size_t)(reinterpret_cast<unsigned char*>(s.misc + 16) - base);
+  off = (off + 15) / 16 * 16;
+  s.full = reinterpret_cast<uint64_t*>(base + off);
+  s.empty = s.full + MAX_NS;
+  s.wbar = s.empty + MAX_NS;
+  return s;
+}
+
+// ------------------------------------------------------------ grid barrier
+// Split arrive / wait on one word: the master CTA adds 0x80000000-(G-1),
+// the others 1, so bit 31 flips when the last CTA arrives (the algorithm of
+// cooperative_groups' grid sync: 1.2 us on B200 vs 2.5 us for a
+// count+generation pair, scripts/microbench.cu), with independent work
+// allowed between the two halves.
+__device__ __forceinline__ unsigned bar_arrive(unsigned* bar, int G) {
+  // order generic-proxy global stores before other CTAs' bulk-copy reads
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __syncthreads();
+  unsigned old = 0;
+  if (threadIdx.x == 0) {
+    const unsigned nb = blockIdx.x == 0 ? 0x80000000u - (unsigned)(G - 1) : 1u;
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(bar), "r"(nb) : "memory");
+  }
+  return old;
+}
+
+__device__ __forceinline__ void bar_wait(unsigned* bar, unsigned old) {
+  if (threadIdx.x == 0) {
+    unsigned cur;
+    do {
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+    } while (((old ^ cur) & 0x80000000u) == 0);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, int G) { bar_wait(bar, bar_arrive(bar, G)); }
+
+// ------------------------------------------------------------ activations
+// Element (row b, feature k) of a chunk-major swizzled activation buffer with
+// K features: [rb][K/64][64][32], row index XOR-swizzled by (k & 3) << 3 so a
+// warp's 32 LDS.128 (8 row quads x 4 k) spread over all banks.
+__device__ __forceinline__ size_t act_idx(int b, int k, int K) {
+  const int rb = b >> 5, r = b & 31, ch = k >> 6, kk = k & 63;
+  return ((size_t)(rb * (K >> 6) + ch) * KC + kk) * RB + (r ^ ((kk & 3) << 3));
+}
+
+// A source for a GEMV pass: up to two concatenated buffers.
+struct ASrc {
+  const float* a0;
+  int k0;  // features in a0
+  const float* a1;
+  int k1;  // features in a1
+};
+
+// Chunk sequence counter shared by the producer and the consumers.
+struct Ring {
+  unsigned n;  // chunks issued / consumed so far
+};
+
+// Producer: issue all chunks of a pass (row blocks x chunks) into the ring.
+__device__ __forceinline__ void produce(const Smem& sm, const PParams& P, Ring& rg, const ASrc& A) {
+  const int lane = threadIdx.x & 31;
+  const int nch0 = A.k0 >> 6, nch = nch0 + (A.k1 >> 6);
+  for (int rb = 0; rb < P.nrb; ++rb)
+    for (int ch = 0; ch < nch; ++ch) {
+      const unsigned n = rg.n++;
+      const int slot = n % P.ns;
+      if (lane == 0) {
+        if (n >= (unsigned)P.ns) mbar_wait(&sm.empty[slot], ((n / P.ns) - 1) & 1);
+        const float* src = ch < nch0
+                               ? A.a0 + (size_t)(rb * nch0 + ch) * CH_FLOATS
+                               : A.a1 + (size_t)(rb * (A.k1 >> 6) + (ch - nch0)) * CH_FLOATS;
+        mbar_arrive_expect_tx(&sm.full[slot], CH_FLOATS * 4);
+        bulk_g2s(sm.ring + (size_t)slot * CH_FLOATS, src, CH_FLOATS * 4, &sm.full[slot]);
+      }
+    }
+  __syncwarp();
+}
+
+// Consumer inner loop over one chunk: acc[i][c] += A[k][4rq+i] * W[kbase+k][c]
+// for this lane's two k-steps (k = 8*warp + 4*j + ks).
+template <int C>
+__device__ __forceinline__ void mac_chunk(const float* chunk, const float* W, int kbase,
+                                          float (&acc)[4][C]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rq = lane >> 2, ks = lane & 3;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int k = 8 * warp + 4 * j + ks;
+    const float4 a = lds4(chunk + k * RB + ((4 * rq) ^ (ks << 3)));
+    const float* wr = W + (size_t)(kbase + k) * C;
+#pragma unroll
+    for (int q = 0; q < C / 4; ++q) {
+      const float4 w = lds4(wr + 4 * q);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float av = i == 0 ? a.x : (i == 1 ? a.y : (i == 2 ? a.z : a.w));
+        acc[i][4 * q + 0] = fmaf(av, w.x, acc[i][4 * q + 0]);
+        acc[i][4 * q + 1] = fmaf(av, w.y, acc[i][4 * q + 1]);
+        acc[i][4 * q + 2] = fmaf(av, w.z, acc[i][4 * q + 2]);
+        acc[i][4 * q + 3] = fmaf(av, w.w, acc[i][4 * q + 3]);
+      }
+    }
+  }
+}
+
+// Reduce acc over the 4 ks lanes and the 8 consumer warps into out[32][C]
+// (smem red, fixed order: ((w0+w4)+(w1+w5))+((w2+w6)+(w3+w7))).  Called by
+// the consumer warps only; uses named barrier 1 (256 threads).
+template <int C>
+__device__ __forceinline__ void reduce_tile(const Smem& sm, float (&acc)[4][C]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rq = lane >> 2, ks = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      float v = acc[i][c];
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      acc[i][c] = v;
+    }
+  float* red = sm.red;
+  if (warp < 4 && ks == 0)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < C; ++c) red[(warp * RB + 4 * rq + i) * C + c] = acc[i][c];
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+  if (warp >= 4 && ks == 0)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < C; ++c) red[((warp - 4) * RB + 4 * rq + i) * C + c] += acc[i][c];
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+
+__device__ __forceinline__ float red_sum(const Smem& sm, int r, int c, int C) {
+  const float* red = sm.red;
+  return (red[r * C + c] + red[(RB + r) * C + c]) + (red[(2 * RB + r) * C + c] + red[(3 * RB + r) * C + c]);
+}
+
+// One GEMV pass over an activation source for every row block.  The producer
+// warp streams chunks; consumers accumulate and call epi(rb) after reducing
+// each row block's tile into sm.red (consumers synchronise on barrier 1).
+template <int C, typename Epi>
+__device__ __forceinline__ void gemv_pass(const Smem& sm, const PParams& P, Ring& rg,
+                                          const ASrc& A, const float* W, Epi epi) {
+  const int warp = threadIdx.x >> 5;
+  const int nch = (A.k0 + A.k1) >> 6;
+  if (warp == NCW) {
+    produce(sm, P, rg, A);
+    return;
+  }
+  for (int rb = 0; rb < P.nrb; ++rb) {
+    float acc[4][C];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[i][c] = 0.0f;
+    for (int ch = 0; ch < nch; ++ch) {
+      const unsigned n = rg.n++;
+      const int slot = n % P.ns;
+      mbar_wait(&sm.full[slot], (n / P.ns) & 1);
+      mac_chunk<C>(sm.ring + (size_t)slot * CH_FLOATS, W, ch * KC, acc);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.empty[slot])) : "memory");
+    }
+    reduce_tile<C>(sm, acc);
+    epi(rb);
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+  }
+}
+
+__device__ __forceinline__ void store_act(float* buf, int b, int k, int K, float v) {
+  buf[act_idx(b, k, K)] = v;
+}
+
+// ------------------------------------------------------------ the kernel
+__global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Smem sm = carve_p(smem_raw, P);
+  const int cta = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = P.G, B = P.B;
+  const bool lstm = P.cell == 1;
+  const int umax = lstm ? UMAX_LSTM : UMAX_TANH;
+  const int u0 = own_lo(P.H, cta, G), u1 = own_lo(P.H, cta + 1, G);
+  const int nu = u1 - u0;                          // owned units
+  const int p0 = own_lo(P.J, cta, G), p1 = own_lo(P.J, cta + 1, G);
+  const int n0 = own_lo(P.NJ, cta, G), n1 = own_lo(P.NJ, cta + 1, G);
+  const int blank = P.V1 - 1;
+  const bool fs = P.algo == ALGO_FS, tdt = P.algo == ALGO_TDT;
+  float* hh0own = P.hh0own + (size_t)cta * B * C1;
+  float* cown = P.cown + (size_t)cta * 2 * B * umax;
+  float* gpown = P.gpown + (size_t)cta * B * C2;
+  const float* bias = P.bias + (size_t)cta * 2 * C1;
+
+  // ---- one-time setup: barriers, resident weights, control state ----
+  if (tid == 0) {
+    for (int i = 0; i < P.ns; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], NCW);
+    }
+    mbar_init(sm.wbar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const size_t bytes = (size_t)P.wfloats * 4;
+    mbar_arrive_expect_tx(sm.wbar, (uint32_t)bytes);
+    const float* src = P.wpack + (size_t)cta * P.wfloats;
+    for (size_t o = 0; o < bytes; o += 32768) {
+      const uint32_t nb = (uint32_t)(bytes - o < 32768 ? bytes - o : 32768);
+      bulk_g2s(reinterpret_cast<unsigned char*>(sm.w) + o,
+               reinterpret_cast<const unsigned char*>(src) + o, nb, sm.wbar);
+    }
+  }
+  int maxlen = 0;
+  for (int b = tid; b < B; b += NTH) {
+    sm.label[b] = blank;
+    sm.tb[b] = 0;
+    sm.ub[b] = 0;
+    const int len = P.out_len[b];
+    sm.flag[b] = (fs ? (0 >= len) : !(0 < len)) | 2;  // accept all for P0
+    if (cta == 0) P.counts[b] = 0;
+  }
+  for (int b = 0; b < B; ++b) maxlen = max(maxlen, __ldg(&P.out_len[b]));
+  // zero own state: h0/h1 (both parities) for owned units, c, hh0 (= 0 @ W), gp
+  for (int i = tid; i < B * nu; i += NTH) {
+    const int b = i / nu, u = u0 + i % nu;
+    store_act(P.h0, b, u, P.Hp, 0.0f);
+    store_act(P.h1[0], b, u, P.Hp, 0.0f);
+    store_act(P.h1[1], b, u, P.Hp, 0.0f);
+  }
+  for (int i = tid; i < 2 * B * umax; i += NTH) cown[i] = 0.0f;
+  for (int i = tid; i < B * C1; i += NTH) hh0own[i] = 0.0f;
+  for (int i = tid; i < B * C2; i += NTH) gpown[i] = 0.0f;
+  if (tid == 0) {
+    sm.misc[2] = 0;  // t
+    sm.misc[3] = 0;  // sym
+    sm.misc[4] = 0;  // par
+  }
+  mbar_wait(sm.wbar, 0);
+  const float* Whh0 = sm.w + P.off_hh0;
+  const float* W1 = sm.w + P.off_w1;
+  const float* Wpp = sm.w + P.off_pp;
+  const float* WJ = sm.w + P.off_j;
+  Ring rg{0};
+  long long joint_evals = 0, pred_steps = 0, outer_iters = 0, iters = 0;
+  unsigned long long t_last = 0;
+  auto mark = [&](int id) {
+    if (P.prof && cta == 0 && tid == 0) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+      if (t_last) P.prof[id] += now - t_last;
+      t_last = now;
+    }
+  };
+  int err = 0;
+  __syncthreads();
+
+  // ---- layer-0 cell for owned units (accepted rows) ----
+  // gates = (table0[label] + hh0) + b   (model.cpp:48 order; App. B)
+  auto cell0 = [&]() {
+    const int G4 = P.Gg;
+    for (int i = tid; i < B * nu; i += NTH) {
+      const int b = i / nu, lu = i % nu, u = u0 + lu;
+      if (!(sm.flag[b] & 2)) continue;
+      const int lab = sm.label[b];
+      if (lstm) {
+        float g4[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const float ih = __ldg(&P.table0[(size_t)lab * P.GH + u * G4 + g]);
+          g4[g] = (ih + hh0own[b * C1 + lu * 4 + g]) + bias[lu * 4 + g];
+        }
+        const float c_old = cown[b * umax + lu];
+        const float i_ = sigmoid_f(g4[0]), f_ = sigmoid_f(g4[1]);
+        const float g_ = tanhf(g4[2]), o_ = sigmoid_f(g4[3]);
+        const float cn = f_ * c_old + i_ * g_;
+        cown[b * umax + lu] = cn;
+        store_act(P.h0, b, u, P.Hp, o_ * tanhf(cn));
+      } else {
+        const float ih = __ldg(&P.table0[(size_t)lab * P.GH + u]);
+        store_act(P.h0, b, u, P.Hp, tanhf((ih + hh0own[b * C1 + lu]) + bias[lu]));
+      }
+    }
+  };
+
+  // ---- trunk = relu(fp[b, t_b] + gp) for owned joint-input columns ----
+  auto refresh_trunk = [&](bool gp_fresh) {
+    (void)gp_fresh;
+    const int np = p1 - p0;
+    for (int i = tid; i < B * np; i += NTH) {
+      const int b = i / np, lj = i % np, j = p0 + lj;
+      int t = fs ? sm.misc[2] : sm.tb[b];
+      t = t < 0 ? 0 : (t > P.T - 1 ? P.T - 1 : t);
+      const float f = __ldg(&P.fp[((size_t)b * P.T + t) * P.Jp + j]);
+      store_act(P.trunk, b, j, P.Jp, fmaxf(f + gpown[b * C2 + lj], 0.0f));
+    }
+  };
+
+  // ---- the prediction step for accepted rows (after decisions) ----
+  auto pred_step = [&]() {
+    mark(2);
+    cell0();
+    mark(3);
+    grid_barrier(P.bar, G);
+    mark(4);
+    const int par = sm.misc[4];
+    if (P.L == 2) {
+      // layer 1: [h0' | h1] @ W_1, fused LSTM cell; h1 ping-pong
+      {
+        ASrc A{P.h0, P.Hp, P.h1[par], P.Hp};
+        gemv_pass<C1>(sm, P, rg, A, W1, [&](int rb) {
+          for (int o = tid; o < RB * nu; o += 256) {
+            const int r = o / nu, lu = o % nu, b = rb * RB + r, u = u0 + lu;
+            if (b >= B) continue;
+            float hn;
+            if (sm.flag[b] & 2) {
+              float g4[4];
+#pragma unroll
+              for (int g = 0; g < 4; ++g) g4[g] = red_sum(sm, r, lu * 4 + g, C1) + bias[C1 + lu * 4 + g];
+              const float c_old = cown[(B + b) * umax + lu];
+              const float i_ = sigmoid_f(g4[0]), f_ = sigmoid_f(g4[1]);
+              const float g_ = tanhf(g4[2]), o_ = sigmoid_f(g4[3]);
+              const float cn = f_ * c_old + i_ * g_;
+              cown[(B + b) * umax + lu] = cn;
+              hn = o_ * tanhf(cn);
+            } else {
+              hn = P.h1[par][act_idx(b, u, P.Hp)];
+            }
+            store_act(P.h1[par ^ 1], b, u, P.Hp, hn);
+          }
+        });
+      }
+      __syncthreads();
+      mark(6);
+      if (tid == 0) sm.misc[4] = par ^ 1;
+      // arrive; the next step's h0' @ W_hh0 needs no other CTA -> hides the barrier
+      const unsigned ticket = bar_arrive(P.bar, G);
+      // hh0 for the next step: h0' @ W_hh0 (owned gate columns)
+      {
+        ASrc A{P.h0, P.Hp, nullptr, 0};
+        gemv_pass<C1>(sm, P, rg, A, Whh0, [&](int rb) {
+          for (int o = tid; o < RB * C1; o += 256) {
+            const int r = o / C1, c = o % C1, b = rb * RB + r;
+            if (b < B && (sm.flag[b] & 2)) hh0own[b * C1 + c] = red_sum(sm, r, c, C1);
+          }
+        });
+      }
+      mark(5);
+      bar_wait(P.bar, ticket);
+      mark(7);
+      // pred_proj over h1', trunk
+      {
+        ASrc A{P.h1[par ^ 1], P.Hp, nullptr, 0};
+        gemv_pass<C2>(sm, P, rg, A, Wpp, [&](int rb) {
+          const int np = p1 - p0;
+          for (int o = tid; o < RB * np; o += 256) {
+            const int r = o / np, lj = o % np, b = rb * RB + r;
+            if (b < B && (sm.flag[b] & 2)) gpown[b * C2 + lj] = red_sum(sm, r, lj, C2);
+          }
+        });
+      }
+    } else {
+      // one layer: pred_proj over h0' plus the next step's hh0 (same chunks)
+      ASrc A{P.h0, P.Hp, nullptr, 0};
+      gemv_pass<C1>(sm, P, rg, A, Whh0, [&](int rb) {
+        for (int o = tid; o < RB * C1; o += 256) {
+          const int r = o / C1, c = o % C1, b = rb * RB + r;
+          if (b < B && (sm.flag[b] & 2)) hh0own[b * C1 + c] = red_sum(sm, r, c, C1);
+        }
+      });
+      gemv_pass<C2>(sm, P, rg, A, Wpp, [&](int rb) {
+        const int np = p1 - p0;
+        for (int o = tid; o < RB * np; o += 256) {
+          const int r = o / np, lj = o % np, b = rb * RB + r;
+          if (b < B && (sm.flag[b] & 2)) gpown[b * C2 + lj] = red_sum(sm, r, lj, C2);
+        }
+      });
+    }
+    __syncthreads();
+    mark(8);
+    refresh_trunk(true);
+    ++pred_steps;
+    mark(9);
+    grid_barrier(P.bar, G);
+    mark(10);
+  };
+
+  // prologue: P0 = pred(blank, 0) for every row (decoders.cpp:414-430)
+  pred_step();
+  for (int b = tid; b < B; b += NTH) sm.flag[b] &= ~2;
+  __syncthreads();
+  bool running = fs ? (maxlen > 0) : false;
+  if (!fs) {
+    int any = 0;
+    for (int b = 0; b < B; ++b) any |= !(sm.flag[b] & 1);
+    running = any;
+  }
+
+  while (running) {
+    // ---- J: joint logits for owned columns -> per-CTA partials ----
+    {
+      ASrc A{P.trunk, P.Jp, nullptr, 0};
+      gemv_pass<C2>(sm, P, rg, A, WJ, [&](int rb) {
+        // half-warp per row: lanes 0..7 hold the 8 columns
+        const int nn = n1 - n0;
+        for (int r = (tid >> 3); r < RB; r += 32) {
+          const int b = rb * RB + r, l8 = tid & 7;
+          const int n = n0 + l8;
+          const float x = l8 < nn ? red_sum(sm, r, l8, C2) : -INFINITY;
+          const bool isv = l8 < nn && n < P.V1, isd = l8 < nn && n >= P.V1;
+          float mv = isv ? x : -INFINITY, md = isd ? x : -INFINITY;
+#pragma unroll
+          for (int o = 4; o >= 1; o >>= 1) {
+            mv = fmaxf(mv, __shfl_xor_sync(0xffffffffu, mv, o));
+            md = fmaxf(md, __shfl_xor_sync(0xffffffffu, md, o));
+          }
+          float ev = isv ? expf(x - mv) : 0.0f, ed = isd ? expf(x - md) : 0.0f;
+          float bv = isv ? x : -INFINITY, bd = isd ? x : -INFINITY;
+          int iv = isv ? n : 0x7fffffff, id = isd ? n - P.V1 : 0x7fffffff;
+#pragma unroll
+          for (int o = 4; o >= 1; o >>= 1) {
+            ev += __shfl_xor_sync(0xffffffffu, ev, o);
+            ed += __shfl_xor_sync(0xffffffffu, ed, o);
+            const float obv = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oiv = __shfl_xor_sync(0xffffffffu, iv, o);
+            if (obv > bv || (obv == bv && oiv < iv)) {
+              bv = obv;
+              iv = oiv;
+            }
+            const float obd = __shfl_xor_sync(0xffffffffu, bd, o);
+            const int oid = __shfl_xor_sync(0xffffffffu, id, o);
+            if (obd > bd || (obd == bd && oid < id)) {
+              bd = obd;
+              id = oid;
+            }
+          }
+          if (l8 == 0 && b < B) {
+            P.partv[(size_t)b * G + cta] = make_float4(mv, ev, bv, __int_as_float(iv));
+            if (P.D) P.partd[(size_t)b * G + cta] = make_float4(md, ed, bd, __int_as_float(id));
+          }
+        }
+      });
+    }
+    ++joint_evals;
+    ++iters;
+    mark(0);
+    grid_barrier(P.bar, G);
+    mark(1);
+
+    // ---- D: decisions (identical in every CTA) ----
+    // 8 threads per row merge the row's G vocab partials (lse in log-sum-exp
+    // form, lowest-index argmax; log_softmax_into / argmax_last_into,
+    // tensor.cpp:268-312, 463-480), all loads issued up front.
+    {
+      for (int b0 = 0; b0 < B; b0 += NTH / 8) {
+        const int b = b0 + (tid >> 3), s8 = tid & 7;
+        float Mx = -INFINITY, Sx = 0.0f, best = -INFINITY, bestd = -INFINITY;
+        int bi = 0x7fffffff, bdi = 0x7fffffff;
+        if (b < B) {
+          constexpr int NL = 20;  // up to 160 CTAs
+          float4 pv[NL];
+#pragma unroll
+          for (int i = 0; i < NL; ++i) {
+            const int c = s8 + 8 * i;
+            pv[i] = c < G ? __ldcg(&P.partv[(size_t)b * G + c])
+                          : make_float4(-INFINITY, 0.f, -INFINITY, __int_as_float(0x7fffffff));
+          }
+#pragma unroll
+          for (int i = 0; i < NL; ++i) {
+            const float4 p = pv[i];
+            if (p.x != -INFINITY) {
+              const float nm = fmaxf(Mx, p.x);
+              Sx = (Sx == 0.0f ? 0.0f : Sx * expf(Mx - nm)) + p.y * expf(p.x - nm);
+              Mx = nm;
+              const int pi = __float_as_int(p.w);
+              if (p.z > best || (p.z == best && pi < bi)) {
+                best = p.z;
+                bi = pi;
+              }
+            }
+          }
+          if (P.D)
+            for (int c = P.dc0 + s8; c < P.dc1; c += 8) {
+              const float4 q = __ldcg(&P.partd[(size_t)b * G + c]);
+              const int qi = __float_as_int(q.w);
+              if (q.z > bestd || (q.z == bestd && qi < bdi)) {
+                bestd = q.z;
+                bdi = qi;
+              }
+            }
+        }
+#pragma unroll
+        for (int o = 4; o >= 1; o >>= 1) {
+          const float om = __shfl_xor_sync(0xffffffffu, Mx, o);
+          const float os = __shfl_xor_sync(0xffffffffu, Sx, o);
+          const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          const float nm = fmaxf(Mx, om);
+          Sx = (Sx == 0.0f ? 0.0f : Sx * expf(Mx - nm)) + (os == 0.0f ? 0.0f : os * expf(om - nm));
+          Mx = nm;
+          if (ob > best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+          }
+          const float obd = __shfl_xor_sync(0xffffffffu, bestd, o);
+          const int odi = __shfl_xor_sync(0xffffffffu, bdi, o);
+          if (obd > bestd || (obd == bestd && odi < bdi)) {
+            bestd = obd;
+            bdi = odi;
+          }
+        }
+        if (s8 == 0 && b < B) {
+          sm.kdec[b] = bi;
+          sm.vdec[b] = best - (Mx + logf(Sx));
+          sm.ddec[b] = P.D ? P.durations[bdi] : 0;
+        }
+      }
+      __syncthreads();
+      // decision rules (thread per row), decoders.cpp:261-307 / 432-512
+      int acc_any = 0, live_any = 0;
+      const int t_fs = sm.misc[2];
+      for (int b = tid; b < B; b += NTH) {
+        int f = sm.flag[b] & ~2;
+        const int k = sm.kdec[b];
+        const float v = sm.vdec[b];
+        if (fs) {
+          if (!(f & 1)) {
+            if (k == blank) {
+              f |= 1;
+            } else {
+              if (cta == 0) {
+                const int nb = P.counts[b];
+                if (nb < P.cap) {
+                  const size_t o = (size_t)b * P.cap + nb;
+                  P.tokens[o] = k;
+                  P.frames[o] = t_fs;
+                  P.scores[o] = v;
+                  P.durs[o] = 0;
+                  P.counts[b] = nb + 1;
+                }
+              }
+              sm.label[b] = k;
+              f |= 2;
+            }
+          }
+          live_any |= !(f & 1);
+        } else if (!(f & 1)) {
+          const int len = __ldg(&P.out_len[b]);
+          int t = sm.tb[b], u = sm.ub[b];
+          if (k == blank) {
+            const int d = tdt ? sm.ddec[b] : 1;
+            t += d > 1 ? d : 1;
+            u = 0;
+          } else {
+            const int d = tdt ? sm.ddec[b] : 0;
+            if (cta == 0) {
+              const int nb = P.counts[b];
+              if (nb < P.cap) {
+                const size_t o = (size_t)b * P.cap + nb;
+                P.tokens[o] = k;
+                P.frames[o] = t;
+                P.scores[o] = v;
+                P.durs[o] = d;
+                P.counts[b] = nb + 1;
+              }
+            }
+            sm.label[b] = k;
+            f |= 2;
+            u += 1;
+            if (d > 0) {
+              t += d;
+              u = 0;
+            } else if (u == P.ms) {
+              t += 1;
+              u = 0;
+            }
+          }
+          sm.tb[b] = t;
+          sm.ub[b] = u;
+          if (!(t < len)) f |= 1;
+          live_any |= !(f & 1);
+        }
+        acc_any |= (f >> 1) & 1;
+        sm.flag[b] = f;
+      }
+      acc_any = __syncthreads_or(acc_any);
+      live_any = __syncthreads_or(live_any);
+      bool finish = false;
+      if (fs) {
+        int sym = sm.misc[3] + 1;
+        int t = t_fs;
+        if (!live_any || sym >= P.ms) {  // frame ends (decoders.cpp:297-313)
+          t += 1;
+          sym = 0;
+          ++outer_iters;
+          if (t >= maxlen) finish = true;
+          __syncthreads();
+          for (int b = tid; b < B; b += NTH)
+            sm.flag[b] = (sm.flag[b] & 2) | (t >= __ldg(&P.out_len[b]) ? 1 : 0);
+        }
+        __syncthreads();
+        if (tid == 0) {
+          sm.misc[3] = sym;
+          sm.misc[2] = t;
+        }
+        __syncthreads();
+      } else {
+        finish = !live_any;
+      }
+      if (iters > P.max_iters) {
+        err = ERR_RUNAWAY;
+        finish = true;
+      }
+      if (finish) break;
+      if (acc_any) {
+        pred_step();
+        if (!fs) ++outer_iters;
+      } else {
+        refresh_trunk(false);
+        mark(11);
+        grid_barrier(P.bar, G);
+        mark(12);
+      }
+      for (int b = tid; b < B; b += NTH) sm.flag[b] &= ~2;
+      __syncthreads();
+    }
+  }
+  if (cta == 0 && tid == 0) {
+    Ctrl* c = P.ctrl;
+    c->joint_evals = joint_evals;
+    c->pred_steps = pred_steps;
+    c->outer_iters = outer_iters;
+    c->iters = iters;
+    c->err = err;
+  }
+}
+
+}  // namespace pk
+}  // namespace rnntg

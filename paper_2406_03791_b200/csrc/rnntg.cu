@@ -20,7 +20,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "encproj_tc.cuh"
-#include "persistent.cuh"
+#include "persistent_k5.cuh"
 
 using namespace rnntg;
 
@@ -289,9 +289,15 @@ rnntg_status setup_persistent(rnntg_decoder* d) {
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
   if (G > nsm) return fail(RNNTG_E_VALUE, "model too wide for the persistent executor");
   const int wfloats = Hp * pk::C1 + (M.L == 2 ? 2 * Hp * pk::C1 : 0) + Hp * pk::C2 + Jp * pk::C2;
-  const int ns = 0;
-  if (pk::smem_bytes(wfloats, ns, d->B) > (size_t)optin)
-    return fail(RNNTG_E_VALUE, "persistent executor: weights exceed shared memory");
+  int ns = 0;  // activation ring slots: as many as shared memory allows
+  for (int cand = pk::MAX_NS; cand >= 2 && !ns; --cand)
+    if (pk::smem_bytes(wfloats, cand, d->B) <= (size_t)optin) ns = cand;
+  if (const char* e = std::getenv("RNNTG_NS")) {
+    const int want = std::atoi(e);
+    if (want >= 2 && want <= pk::MAX_NS && pk::smem_bytes(wfloats, want, d->B) <= (size_t)optin)
+      ns = want;
+  }
+  if (!ns) return fail(RNNTG_E_VALUE, "persistent executor: weights exceed shared memory");
   d->psmem = pk::smem_bytes(wfloats, ns, d->B);
   CK(cudaFuncSetAttribute(pk::persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)d->psmem));
