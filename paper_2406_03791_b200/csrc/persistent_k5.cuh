@@ -35,22 +35,21 @@
 namespace rnntg {
 namespace pk {
 
-constexpr int KC = 64;          // k per activation chunk
-constexpr int CH_FLOATS = KC * RB;  // 2048 floats = 8 KB per (row block, chunk)
 constexpr int C1 = 20;          // gate columns per CTA (5 LSTM units / 20 tanh units)
 constexpr int C2 = 8;           // pred_proj / joint columns per CTA
 constexpr int UMAX_LSTM = 5;
 constexpr int UMAX_TANH = 20;
-constexpr int NCW = 8;          // consumer warps
-constexpr int NTH = (NCW + 1) * 32;  // + 1 producer warp
+constexpr int NCW = 8;          // warps; each streams its own k-slice
+constexpr int NTH = NCW * 32;
 constexpr int MAXB = 256;       // rows per decoder in the persistent path
-constexpr int MAX_NS = 4;
+constexpr int MAX_NS = 4;       // slot sizes tried: ns * 8 features (32, 24, 16)
+constexpr int RED_FLOATS = 4 * RB * C1;
 
 struct PParams {
   int G;            // CTAs
   int B, nrb, T, ms, cap, algo, L, cell;
   int H, Hp, J, Jp, V1, D, NJ;   // NJ = V1 + D joint columns
-  int ns;           // ring slots
+  int ns;           // per-warp slot = ns * 8 features x 32 rows (bulk-copy granule)
   int dc0, dc1;     // CTAs owning duration columns: [dc0, dc1)
   long long max_iters;
   int durations[MAXD];
@@ -62,9 +61,9 @@ struct PParams {
   int GH, Gg;           // GH = Gg*Hp
   const float* fp;      // [B*T][Jp]
   const int* out_len;
-  float* h0;            // [nrb][Hp/64][64][32] swizzled chunks
+  float* h0;            // [nrb][Hp][32] k-major, row index swizzled
   float* h1[2];         // same, ping-pong
-  float* trunk;         // [nrb][Jp/64][64][32]
+  float* trunk;         // [nrb][Jp][32]
   float* hh0own;        // [G][B][C1]
   float* cown;          // [G][2][B][UMAX]
   float* gpown;         // [G][B][C2]
@@ -82,29 +81,34 @@ struct PParams {
 
 __host__ __device__ inline int own_lo(int n, int c, int G) { return (int)((long long)n * c / G); }
 
-// Shared-memory layout (bytes): [weights][ring ns x 8KB][red 4 x 32 x C1][ctrl][mbarriers]
+// Shared memory: [weights][per-warp activation slots, reused as the
+// reduction scratch][per-row control][mbarriers]
 struct Smem {
   float* w;
-  float* ring;
-  float* red;
+  float* ring;   // NCW slots of slotk x 32 floats
+  float* red;    // overlays ring
   int* label;
   int* tb;
   int* ub;
-  int* flag;     // bit0 done(FS)/!active(LL), bit1 accept, bit2 need-decision
-  int* kdec;     // decided label per row (this step)
-  float* vdec;   // score
-  int* ddec;     // duration value
-  int* misc;     // [0]=any accept, [1]=any live, [2]=t, [3]=sym, [4]=par, [5]=finish
-  uint64_t* full;
-  uint64_t* empty;
+  int* flag;     // bit0 done(FS) / inactive(LL), bit1 accepted this step
+  int* kdec;
+  float* vdec;
+  int* ddec;
+  int* misc;     // [2]=t, [3]=sym, [4]=par
+  uint64_t* full;  // one per warp
   uint64_t* wbar;
 };
 
+__host__ __device__ inline size_t ring_floats(int ns) {
+  const size_t r = (size_t)NCW * ns * 8 * RB;
+  return r > (size_t)RED_FLOATS ? r : (size_t)RED_FLOATS;
+}
+
 __host__ __device__ inline size_t smem_bytes(int wfloats, int ns, int B) {
-  size_t b = (size_t)wfloats * 4 + (size_t)ns * CH_FLOATS * 4 + 4 * RB * C1 * 4;
+  size_t b = (size_t)wfloats * 4 + ring_floats(ns) * 4;
   b += (size_t)B * 4 * 7 + 64;
   b = (b + 15) / 16 * 16;
-  b += 8 * (2 * MAX_NS + 1);
+  b += 8 * (NCW + 1);
   return b;
 }
 
@@ -112,8 +116,8 @@ __device__ inline Smem carve_p(unsigned char* base, const PParams& P) {
   Smem s;
   s.w = reinterpret_cast<float*>(base);
   s.ring = s.w + P.wfloats;
-  s.red = s.ring + P.ns * CH_FLOATS;
-  int* ip = reinterpret_cast<int*>(s.red + 4 * RB * C1);
+  s.red = s.ring;
+  int* ip = reinterpret_cast<int*>(s.ring + ring_floats(P.ns));
   s.label = ip;
   s.tb = ip + P.B;
   s.ub = ip + 2 * P.B;
@@ -125,8 +129,7 @@ __device__ inline Smem carve_p(unsigned char* base, const PParams& P) {
   size_t off = (size_t)(reinterpret_cast<unsigned char*>(s.misc + 16) - base);
   off = (off + 15) / 16 * 16;
   s.full = reinterpret_cast<uint64_t*>(base + off);
-  s.empty = s.full + MAX_NS;
-  s.wbar = s.empty + MAX_NS;
+  s.wbar = s.full + NCW;
   return s;
 }
 
@@ -161,77 +164,55 @@ __device__ __forceinline__ void bar_wait(unsigned* bar, unsigned old) {
 __device__ __forceinline__ void grid_barrier(unsigned* bar, int G) { bar_wait(bar, bar_arrive(bar, G)); }
 
 // ------------------------------------------------------------ activations
-// Element (row b, feature k) of a chunk-major swizzled activation buffer with
-// K features: [rb][K/64][64][32], row index XOR-swizzled by (k & 3) << 3 so a
-// warp's 32 LDS.128 (8 row quads x 4 k) spread over all banks.
+// Element (row b, feature k) of a k-major activation buffer with K features:
+// [rb][K][32 rows], the row index XOR-swizzled by (k & 3) << 3 so a warp's
+// LDS.128 of 8 row quads x 4 consecutive k hit 8 distinct bank quads per k.
+// Any contiguous feature range is one contiguous block -> one bulk copy.
 __device__ __forceinline__ size_t act_idx(int b, int k, int K) {
-  const int rb = b >> 5, r = b & 31, ch = k >> 6, kk = k & 63;
-  return ((size_t)(rb * (K >> 6) + ch) * KC + kk) * RB + (r ^ ((kk & 3) << 3));
+  const int rb = b >> 5, r = b & 31;
+  return ((size_t)rb * K + k) * RB + (r ^ ((k & 3) << 3));
 }
 
-// A source for a GEMV pass: up to two concatenated buffers.
+__device__ __forceinline__ void store_act(float* buf, int b, int k, int K, float v) {
+  buf[act_idx(b, k, K)] = v;
+}
+
+// A source for a GEMV pass: up to two concatenated buffers (features K0 + K1).
 struct ASrc {
   const float* a0;
-  int k0;  // features in a0
+  int k0;
   const float* a1;
-  int k1;  // features in a1
+  int k1;
 };
 
-// Chunk sequence counter shared by the producer and the consumers.
-struct Ring {
-  unsigned n;  // chunks issued / consumed so far
-};
-
-// Producer: issue all chunks of a pass (row blocks x chunks) into the ring.
-__device__ __forceinline__ void produce(const Smem& sm, const PParams& P, Ring& rg, const ASrc& A) {
-  const int lane = threadIdx.x & 31;
-  const int nch0 = A.k0 >> 6, nch = nch0 + (A.k1 >> 6);
-  for (int rb = 0; rb < P.nrb; ++rb)
-    for (int ch = 0; ch < nch; ++ch) {
-      const unsigned n = rg.n++;
-      const int slot = n % P.ns;
-      if (lane == 0) {
-        if (n >= (unsigned)P.ns) mbar_wait(&sm.empty[slot], ((n / P.ns) - 1) & 1);
-        const float* src = ch < nch0
-                               ? A.a0 + (size_t)(rb * nch0 + ch) * CH_FLOATS
-                               : A.a1 + (size_t)(rb * (A.k1 >> 6) + (ch - nch0)) * CH_FLOATS;
-        mbar_arrive_expect_tx(&sm.full[slot], CH_FLOATS * 4);
-        bulk_g2s(sm.ring + (size_t)slot * CH_FLOATS, src, CH_FLOATS * 4, &sm.full[slot]);
-      }
-    }
-  __syncwarp();
-}
-
-// Consumer inner loop over one chunk: acc[i][c] += A[k][4rq+i] * W[kbase+k][c]
-// for this lane's two k-steps (k = 8*warp + 4*j + ks).
+// acc[i][c] += A[k][4rq+i] * W[k][c] for one k of this lane.
 template <int C>
-__device__ __forceinline__ void mac_chunk(const float* chunk, const float* W, int kbase,
-                                          float (&acc)[4][C]) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rq = lane >> 2, ks = lane & 3;
+__device__ __forceinline__ void mac_step(const float4 a, const float* wr, float (&acc)[4][C]) {
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int k = 8 * warp + 4 * j + ks;
-    const float4 a = lds4(chunk + k * RB + ((4 * rq) ^ (ks << 3)));
-    const float* wr = W + (size_t)(kbase + k) * C;
-#pragma unroll
-    for (int q = 0; q < C / 4; ++q) {
-      const float4 w = lds4(wr + 4 * q);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float av = i == 0 ? a.x : (i == 1 ? a.y : (i == 2 ? a.z : a.w));
-        acc[i][4 * q + 0] = fmaf(av, w.x, acc[i][4 * q + 0]);
-        acc[i][4 * q + 1] = fmaf(av, w.y, acc[i][4 * q + 1]);
-        acc[i][4 * q + 2] = fmaf(av, w.z, acc[i][4 * q + 2]);
-        acc[i][4 * q + 3] = fmaf(av, w.w, acc[i][4 * q + 3]);
-      }
-    }
+  for (int q = 0; q < C / 4; ++q) {
+    const float4 w = lds4(wr + 4 * q);
+    acc[0][4 * q + 0] = fmaf(a.x, w.x, acc[0][4 * q + 0]);
+    acc[0][4 * q + 1] = fmaf(a.x, w.y, acc[0][4 * q + 1]);
+    acc[0][4 * q + 2] = fmaf(a.x, w.z, acc[0][4 * q + 2]);
+    acc[0][4 * q + 3] = fmaf(a.x, w.w, acc[0][4 * q + 3]);
+    acc[1][4 * q + 0] = fmaf(a.y, w.x, acc[1][4 * q + 0]);
+    acc[1][4 * q + 1] = fmaf(a.y, w.y, acc[1][4 * q + 1]);
+    acc[1][4 * q + 2] = fmaf(a.y, w.z, acc[1][4 * q + 2]);
+    acc[1][4 * q + 3] = fmaf(a.y, w.w, acc[1][4 * q + 3]);
+    acc[2][4 * q + 0] = fmaf(a.z, w.x, acc[2][4 * q + 0]);
+    acc[2][4 * q + 1] = fmaf(a.z, w.y, acc[2][4 * q + 1]);
+    acc[2][4 * q + 2] = fmaf(a.z, w.z, acc[2][4 * q + 2]);
+    acc[2][4 * q + 3] = fmaf(a.z, w.w, acc[2][4 * q + 3]);
+    acc[3][4 * q + 0] = fmaf(a.w, w.x, acc[3][4 * q + 0]);
+    acc[3][4 * q + 1] = fmaf(a.w, w.y, acc[3][4 * q + 1]);
+    acc[3][4 * q + 2] = fmaf(a.w, w.z, acc[3][4 * q + 2]);
+    acc[3][4 * q + 3] = fmaf(a.w, w.w, acc[3][4 * q + 3]);
   }
 }
 
-// Reduce acc over the 4 ks lanes and the 8 consumer warps into out[32][C]
-// (smem red, fixed order: ((w0+w4)+(w1+w5))+((w2+w6)+(w3+w7))).  Called by
-// the consumer warps only; uses named barrier 1 (256 threads).
+// Reduce acc over the 4 ks lanes and the 8 warps into sm.red ([4][32][C],
+// summed in fixed order ((w0+w4)+(w1+w5))+((w2+w6)+(w3+w7)) by red_sum).
+// red overlays the activation slots, so everyone must be done with them.
 template <int C>
 __device__ __forceinline__ void reduce_tile(const Smem& sm, float (&acc)[4][C]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -245,19 +226,20 @@ __device__ __forceinline__ void reduce_tile(const Smem& sm, float (&acc)[4][C]) 
       v += __shfl_xor_sync(0xffffffffu, v, 2);
       acc[i][c] = v;
     }
+  __syncthreads();
   float* red = sm.red;
   if (warp < 4 && ks == 0)
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int c = 0; c < C; ++c) red[(warp * RB + 4 * rq + i) * C + c] = acc[i][c];
-  asm volatile("bar.sync 1, 256;" ::: "memory");
+  __syncthreads();
   if (warp >= 4 && ks == 0)
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int c = 0; c < C; ++c) red[((warp - 4) * RB + 4 * rq + i) * C + c] += acc[i][c];
-  asm volatile("bar.sync 1, 256;" ::: "memory");
+  __syncthreads();
 }
 
 __device__ __forceinline__ float red_sum(const Smem& sm, int r, int c, int C) {
@@ -265,40 +247,54 @@ __device__ __forceinline__ float red_sum(const Smem& sm, int r, int c, int C) {
   return (red[r * C + c] + red[(RB + r) * C + c]) + (red[(2 * RB + r) * C + c] + red[(3 * RB + r) * C + c]);
 }
 
-// One GEMV pass over an activation source for every row block.  The producer
-// warp streams chunks; consumers accumulate and call epi(rb) after reducing
-// each row block's tile into sm.red (consumers synchronise on barrier 1).
+// One GEMV pass over an activation source for every row block:
+// out[32 rows][C] = A[32][K] @ W[K][C], W resident in smem ([K][C]).
+// Warp w owns the contiguous feature slice [w*K/8, (w+1)*K/8) and streams it
+// through its own slot with one bulk copy per ns*8 features (bulk copies
+// from one warp serialise, so every warp issues its own:
+// scripts/microbench3.cu).  Lane (rq, ks): rows 4rq..4rq+3, features
+// k = 4j + ks of each slot.  epi(rb) runs after the block reduction.
 template <int C, typename Epi>
-__device__ __forceinline__ void gemv_pass(const Smem& sm, const PParams& P, Ring& rg,
+__device__ __forceinline__ void gemv_pass(const Smem& sm, const PParams& P, unsigned& ph,
                                           const ASrc& A, const float* W, Epi epi) {
-  const int warp = threadIdx.x >> 5;
-  const int nch = (A.k0 + A.k1) >> 6;
-  if (warp == NCW) {
-    produce(sm, P, rg, A);
-    return;
-  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rq = lane >> 2, ks = lane & 3;
+  const int K = A.k0 + A.k1, kw = K / NCW, kbeg = warp * kw;
+  const int slotk = P.ns * 8;
+  float* slot = sm.ring + (size_t)warp * slotk * RB;
+  uint64_t* bar = &sm.full[warp];
+  const bool seg0 = kbeg < A.k0;
+  const float* base = seg0 ? A.a0 : A.a1;
+  const int kseg = seg0 ? A.k0 : A.k1;
+  const int koff = seg0 ? kbeg : kbeg - A.k0;
+  const int aoff = (4 * rq) ^ (ks << 3);
   for (int rb = 0; rb < P.nrb; ++rb) {
     float acc[4][C];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int c = 0; c < C; ++c) acc[i][c] = 0.0f;
-    for (int ch = 0; ch < nch; ++ch) {
-      const unsigned n = rg.n++;
-      const int slot = n % P.ns;
-      mbar_wait(&sm.full[slot], (n / P.ns) & 1);
-      mac_chunk<C>(sm.ring + (size_t)slot * CH_FLOATS, W, ch * KC, acc);
+    for (int kk = 0; kk < kw; kk += slotk) {
+      const int nk = kw - kk < slotk ? kw - kk : slotk;
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(bar, (uint32_t)(nk * RB * 4));
+        bulk_g2s(slot, base + ((size_t)rb * kseg + koff + kk) * RB, (uint32_t)(nk * RB * 4), bar);
+      }
+      mbar_wait(bar, ph);
+      ph ^= 1u;
+      const float* wk = W + (size_t)(kbeg + kk + ks) * C;
+#pragma unroll 4
+      for (int j = 0; j < nk / 4; ++j) {
+        const float4 a = lds4(slot + (4 * j + ks) * RB + aoff);
+        mac_step<C>(a, wk + (size_t)4 * j * C, acc);
+      }
       __syncwarp();
-      if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.empty[slot])) : "memory");
     }
     reduce_tile<C>(sm, acc);
     epi(rb);
-    asm volatile("bar.sync 1, 256;" ::: "memory");
+    __syncthreads();
   }
-}
-
-__device__ __forceinline__ void store_act(float* buf, int b, int k, int K, float v) {
-  buf[act_idx(b, k, K)] = v;
 }
 
 // ------------------------------------------------------------ the kernel
@@ -322,10 +318,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
 
   // ---- one-time setup: barriers, resident weights, control state ----
   if (tid == 0) {
-    for (int i = 0; i < P.ns; ++i) {
-      mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], NCW);
-    }
+    for (int i = 0; i < NCW; ++i) mbar_init(&sm.full[i], 1);
     mbar_init(sm.wbar, 1);
     fence_mbar_init();
   }
@@ -370,7 +363,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
   const float* W1 = sm.w + P.off_w1;
   const float* Wpp = sm.w + P.off_pp;
   const float* WJ = sm.w + P.off_j;
-  Ring rg{0};
+  unsigned ph = 0;  // this warp's slot mbarrier phase
   long long joint_evals = 0, pred_steps = 0, outer_iters = 0, iters = 0;
   unsigned long long t_last = 0;
   auto mark = [&](int id) {
@@ -437,7 +430,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
       // layer 1: [h0' | h1] @ W_1, fused LSTM cell; h1 ping-pong
       {
         ASrc A{P.h0, P.Hp, P.h1[par], P.Hp};
-        gemv_pass<C1>(sm, P, rg, A, W1, [&](int rb) {
+        gemv_pass<C1>(sm, P, ph, A, W1, [&](int rb) {
           for (int o = tid; o < RB * nu; o += 256) {
             const int r = o / nu, lu = o % nu, b = rb * RB + r, u = u0 + lu;
             if (b >= B) continue;
@@ -467,7 +460,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
       // hh0 for the next step: h0' @ W_hh0 (owned gate columns)
       {
         ASrc A{P.h0, P.Hp, nullptr, 0};
-        gemv_pass<C1>(sm, P, rg, A, Whh0, [&](int rb) {
+        gemv_pass<C1>(sm, P, ph, A, Whh0, [&](int rb) {
           for (int o = tid; o < RB * C1; o += 256) {
             const int r = o / C1, c = o % C1, b = rb * RB + r;
             if (b < B && (sm.flag[b] & 2)) hh0own[b * C1 + c] = red_sum(sm, r, c, C1);
@@ -480,7 +473,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
       // pred_proj over h1', trunk
       {
         ASrc A{P.h1[par ^ 1], P.Hp, nullptr, 0};
-        gemv_pass<C2>(sm, P, rg, A, Wpp, [&](int rb) {
+        gemv_pass<C2>(sm, P, ph, A, Wpp, [&](int rb) {
           const int np = p1 - p0;
           for (int o = tid; o < RB * np; o += 256) {
             const int r = o / np, lj = o % np, b = rb * RB + r;
@@ -491,13 +484,13 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
     } else {
       // one layer: pred_proj over h0' plus the next step's hh0 (same chunks)
       ASrc A{P.h0, P.Hp, nullptr, 0};
-      gemv_pass<C1>(sm, P, rg, A, Whh0, [&](int rb) {
+      gemv_pass<C1>(sm, P, ph, A, Whh0, [&](int rb) {
         for (int o = tid; o < RB * C1; o += 256) {
           const int r = o / C1, c = o % C1, b = rb * RB + r;
           if (b < B && (sm.flag[b] & 2)) hh0own[b * C1 + c] = red_sum(sm, r, c, C1);
         }
       });
-      gemv_pass<C2>(sm, P, rg, A, Wpp, [&](int rb) {
+      gemv_pass<C2>(sm, P, ph, A, Wpp, [&](int rb) {
         const int np = p1 - p0;
         for (int o = tid; o < RB * np; o += 256) {
           const int r = o / np, lj = o % np, b = rb * RB + r;
@@ -529,7 +522,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
     // ---- J: joint logits for owned columns -> per-CTA partials ----
     {
       ASrc A{P.trunk, P.Jp, nullptr, 0};
-      gemv_pass<C2>(sm, P, rg, A, WJ, [&](int rb) {
+      gemv_pass<C2>(sm, P, ph, A, WJ, [&](int rb) {
         // half-warp per row: lanes 0..7 hold the 8 columns
         const int nn = n1 - n0;
         for (int r = (tid >> 3); r < RB; r += 32) {

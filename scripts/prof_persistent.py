@@ -14,7 +14,7 @@ from paper_2406_03791_b200._lib import Stats, check, lib  # noqa: E402
 NAMES = {0: "J pass", 1: "B1 wait", 2: "D decide", 3: "cell0", 4: "B2 wait", 5: "hh0 pass",
          6: "P1 pass", 7: "B3 wait", 8: "Pp pass", 9: "trunk", 10: "B4 wait", 11: "trunk(noacc)",
          12: "B(noacc)"}
-os.environ.setdefault("NSLIST", "3")
+os.environ.setdefault("NSLIST", "4,2")
 dims = ModelDims(1024, 640, 640, 640, 1024, (), "lstm", 2)
 m = Model.from_seed(dims, 1)
 L = lib()
