@@ -281,8 +281,16 @@ __device__ __forceinline__ void gemv_pass(const Smem& sm, const PParams& P, unsi
         mbar_arrive_expect_tx(bar, (uint32_t)(nk * RB * 4));
         bulk_g2s(slot, base + ((size_t)rb * kseg + koff + kk) * RB, (uint32_t)(nk * RB * 4), bar);
       }
+      unsigned long long tq0 = 0;
+      if (P.prof && blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tq0));
       mbar_wait(bar, ph);
       ph ^= 1u;
+      if (P.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long tq1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tq1));
+        P.prof[13] += tq1 - tq0;
+        P.prof[14] += 1;
+      }
       const float* wk = W + (size_t)(kbeg + kk + ks) * C;
 #pragma unroll 4
       for (int j = 0; j < nk / 4; ++j) {
@@ -291,9 +299,16 @@ __device__ __forceinline__ void gemv_pass(const Smem& sm, const PParams& P, unsi
       }
       __syncwarp();
     }
+    unsigned long long tr0 = 0;
+    if (P.prof && blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
     reduce_tile<C>(sm, acc);
     epi(rb);
     __syncthreads();
+    if (P.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long tr1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr1));
+      P.prof[15] += tr1 - tr0;
+    }
   }
 }
 

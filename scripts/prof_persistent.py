@@ -37,7 +37,9 @@ for ns in os.environ.get("NSLIST", "2,3").split(","):
     check(L.rnntg_get_stats(d, C.byref(st)))
     steps = st.joint_evals
     print(f"ns={ns}: {st.gpu_ms:.2f} ms, {steps} steps, {1000 * st.gpu_ms / steps:.2f} us/step")
-    tot = sum(prof[i] for i in range(16))
+    tot = sum(prof[i] for i in range(13))
     for i in range(13):
         print(f"   {NAMES[i]:14s} {prof[i] / 1000 / steps:8.2f} us/step  {100 * prof[i] / max(tot, 1):5.1f}%")
+    print(f"   copy wait (warp0): {prof[13] / 1000 / steps:.2f} us/step over {prof[14] / steps:.1f} copies; "
+          f"reduce+epilogue {prof[15] / 1000 / steps:.2f} us/step")
     check(L.rnntg_decoder_destroy(d))
