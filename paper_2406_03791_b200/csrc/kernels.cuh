@@ -1,6 +1,6 @@
 // kernels.cuh — the decoder's sm_100a kernels (graph path).
 //
-//   encproj_simt_kernel   K1 reference-precision encoder projection (fp32 FFMA)
+//   (K1, the tcgen05 3xTF32 encoder projection, lives in encproj_tc.cuh)
 //   prologue_kernel       K0 state / emission / loop-flag initialisation
 //   pred_layer_kernel     K2 one prediction-network layer: gate GEMV fused with
 //                         the tanh / LSTM cell and the predicated state commit
@@ -125,55 +125,6 @@ __device__ __forceinline__ void stage_rows_bulk(const StepSmem& sm, int KS, int 
   __syncwarp();
   bulk_g2s(sm.As + lane * KS + k0, src + (size_t)(row0 + lane) * ld + koff,
            (uint32_t)(kw * sizeof(float)), &sm.bars[warp]);
-}
-
-// -------------------------------------------------------------------------
-// K1 (reference-precision path): fp[m, n] = sum_k x[m, k] * enc[k, n].
-// joint.enc_proj of model.cpp:365-369, hoisted over all B*T frames
-// (bit-neutral hoist).  64x64 tiles, 256 threads, 4x4 each.
-// -------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) encproj_simt_kernel(const float* __restrict__ x,
-                                                           const float* __restrict__ enc,
-                                                           float* __restrict__ out, int M,
-                                                           int F, int Jp) {
-  __shared__ float Xs[16][64 + 4];
-  __shared__ float Ws[16][64];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
-  float acc[4][4] = {};
-  for (int k0 = 0; k0 < F; k0 += 16) {
-    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
-      const int mm = i / 16, kk = i % 16;
-      const int m = m0 + mm, k = k0 + kk;
-      Xs[kk][mm] = (m < M && k < F) ? x[(size_t)m * F + k] : 0.0f;
-    }
-    for (int i = threadIdx.x; i < 16 * 64; i += 256) {
-      const int kk = i / 64, nn = i % 64;
-      const int k = k0 + kk;
-      Ws[kk][nn] = (k < F) ? enc[(size_t)k * Jp + n0 + nn] : 0.0f;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      float a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = Xs[kk][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Ws[kk][tx * 4 + j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int m = m0 + ty * 4 + i;
-    if (m >= M) continue;
-    *reinterpret_cast<float4*>(out + (size_t)m * Jp + n0 + tx * 4) =
-        make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-  }
 }
 
 // -------------------------------------------------------------------------

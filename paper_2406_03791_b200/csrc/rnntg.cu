@@ -86,7 +86,8 @@ struct rnntg_decoder {
   cudaGraphExec_t gexec = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool bound = false, launched = false;
-  float* x_dev = nullptr;
+  float* x_dev = nullptr;  // [B*T][Fp] pitched, zero-padded features
+  EncPlan enc;             // K1 tensor maps over x_dev -> st.fp
   int* len_dev = nullptr;
   // kernel-node argument storage (copied into the nodes at creation)
   DevModel arg_m{};
@@ -601,6 +602,9 @@ rnntg_status rnntg_model_create(int device, const rnntg_dims* dims, const float*
   }
   CKM(set_smem_attrs(M));
   m->tc_ok = encproj_tc_supported(M);
+  if (!m->tc_ok)
+    return fail_free(RNNTG_E_CUDA,
+                     "tcgen05 encoder projection unavailable (needs an sm_100 B200 device)");
   {
     m->host_w.resize(nweights);
     const rnntg_dims& dd = *dims;
@@ -655,14 +659,16 @@ rnntg_status rnntg_decoder_create(rnntg_model* m, int algo, int exec, int batch,
   rnntg_status st = alloc_state(m, d->mem, d->st, algo, batch, max_frames, max_symbols, false);
   cudaError_t e = cudaSuccess;
   if (!st) {
-    if ((e = d->mem.alloc(&d->x_dev, (size_t)batch * max_frames * m->dm.F)) == cudaSuccess &&
+    if ((e = d->mem.alloc(&d->x_dev, (size_t)batch * max_frames * m->dm.Fp)) == cudaSuccess &&
         (e = d->mem.alloc(&d->len_dev, (size_t)batch)) == cudaSuccess &&
         (e = cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking)) == cudaSuccess &&
         (e = cudaEventCreate(&d->ev0)) == cudaSuccess &&
         (e = cudaEventCreate(&d->ev1)) == cudaSuccess) {
       d->st.x = d->x_dev;
       d->st.out_len = d->len_dev;
-      if (exec == RNNTG_EXEC_GRAPH) e = build_graph(d);
+      if (!encproj_plan(d->enc, m->dm, d->x_dev, d->st.fp, batch * max_frames))
+        st = fail(RNNTG_E_CUDA, "cannot encode TMA tensor maps for the encoder projection");
+      else if (exec == RNNTG_EXEC_GRAPH) e = build_graph(d);
       else st = setup_persistent(d);
     }
   }
@@ -705,8 +711,9 @@ rnntg_status rnntg_bind(rnntg_decoder* d, const float* x, const int32_t* out_len
   rnntg_status st = check_lengths(d, out_len);
   if (st) return st;
   CK(cudaSetDevice(d->m->device));
-  CK(cudaMemcpyAsync(d->x_dev, x, sizeof(float) * (size_t)d->B * d->T * d->m->dm.F,
-                     cudaMemcpyHostToDevice, d->stream));
+  const size_t F = d->m->dm.F, Fp = d->m->dm.Fp;
+  CK(cudaMemcpy2DAsync(d->x_dev, Fp * sizeof(float), x, F * sizeof(float), F * sizeof(float),
+                       (size_t)d->B * d->T, cudaMemcpyHostToDevice, d->stream));
   CK(cudaMemcpyAsync(d->len_dev, out_len, sizeof(int32_t) * d->B, cudaMemcpyHostToDevice,
                      d->stream));
   d->bound = true;
@@ -723,8 +730,9 @@ rnntg_status rnntg_bind_device(rnntg_decoder* d, const float* x_dev, const int32
   CK(cudaStreamSynchronize(d->stream));
   rnntg_status st = check_lengths(d, lens.data());
   if (st) return st;
-  CK(cudaMemcpyAsync(d->x_dev, x_dev, sizeof(float) * (size_t)d->B * d->T * d->m->dm.F,
-                     cudaMemcpyDeviceToDevice, d->stream));
+  const size_t F = d->m->dm.F, Fp = d->m->dm.Fp;
+  CK(cudaMemcpy2DAsync(d->x_dev, Fp * sizeof(float), x_dev, F * sizeof(float), F * sizeof(float),
+                       (size_t)d->B * d->T, cudaMemcpyDeviceToDevice, d->stream));
   CK(cudaMemcpyAsync(d->len_dev, len_dev, sizeof(int32_t) * d->B, cudaMemcpyDeviceToDevice,
                      d->stream));
   d->bound = true;
@@ -737,7 +745,7 @@ rnntg_status rnntg_launch(rnntg_decoder* d) {
   CK(cudaSetDevice(d->m->device));
   CK(cudaEventRecord(d->ev0, d->stream));
   if (d->exec == RNNTG_EXEC_PERSISTENT) {
-    CK(launch_encproj(d->m->dm, d->m->tc_ok, d->x_dev, d->st.fp, d->B * d->T, d->stream));
+    CK(encproj_launch(d->enc, d->stream));
     void* args[1] = {&d->pp};
     CK(cudaLaunchCooperativeKernel((const void*)pk::persistent_kernel, dim3(d->pp.G), dim3(pk::NTH),
                                    args, d->psmem, d->stream));
@@ -819,14 +827,17 @@ rnntg_status rnntg_step_joint(rnntg_model* m, int batch, const float* f, const f
   float* xd = nullptr;
   int* lens = nullptr;
   auto run = [&]() -> rnntg_status {
-    CK(mem.alloc(&xd, (size_t)batch * M.F));
+    CK(mem.alloc(&xd, (size_t)batch * M.Fp));
     CK(mem.alloc(&lens, (size_t)batch));
-    CK(cudaMemcpy(xd, f, sizeof(float) * batch * M.F, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy2D(xd, sizeof(float) * M.Fp, f, sizeof(float) * M.F, sizeof(float) * M.F, batch,
+                    cudaMemcpyHostToDevice));
     s.x = xd;
     s.out_len = lens;
     s.use_cond = 0;
     // encoder projection of the B single-frame rows
-    CK(launch_encproj(M, m->tc_ok, xd, s.fp, batch, 0));
+    EncPlan plan;
+    if (!encproj_plan(plan, M, xd, s.fp, batch)) return fail(RNNTG_E_CUDA, "tensor map encode failed");
+    CK(encproj_launch(plan, 0));
     // h_top' rows = g (state parity 0 -> next buffer is 1)
     CK(cudaMemcpy2D(s.h[M.L - 1][1], sizeof(float) * M.Hp, g, sizeof(float) * M.H,
                     sizeof(float) * M.H, batch, cudaMemcpyHostToDevice));
@@ -920,7 +931,7 @@ rnntg_status rnntg_time_kernel(rnntg_decoder* d, int which, int reps, float* avg
   s.max_iters = (long long)1 << 60;
   cudaStream_t st = d->stream;
   auto launch_one = [&]() -> cudaError_t {
-    if (which == 0) return launch_encproj(M, d->m->tc_ok, d->x_dev, s.fp, d->B * d->T, st);
+    if (which == 0) return encproj_launch(d->enc, st);
     if (which == 10) {  // the persistent decode kernel alone (fp already projected)
       if (d->exec != RNNTG_EXEC_PERSISTENT) return cudaErrorInvalidValue;
       void* args[1] = {&d->pp};
@@ -992,10 +1003,13 @@ rnntg_status rnntg_enc_proj(rnntg_model* m, int rows, const float* x, float* fp)
   DevBuf mem;
   float *xd = nullptr, *od = nullptr;
   auto run = [&]() -> rnntg_status {
-    CK(mem.alloc(&xd, (size_t)rows * M.F));
+    CK(mem.alloc(&xd, (size_t)rows * M.Fp));
     CK(mem.alloc(&od, (size_t)rows * M.Jp));
-    CK(cudaMemcpy(xd, x, sizeof(float) * rows * M.F, cudaMemcpyHostToDevice));
-    CK(launch_encproj(M, m->tc_ok, xd, od, rows, 0));
+    CK(cudaMemcpy2D(xd, sizeof(float) * M.Fp, x, sizeof(float) * M.F, sizeof(float) * M.F, rows,
+                    cudaMemcpyHostToDevice));
+    EncPlan plan;
+    if (!encproj_plan(plan, M, xd, od, rows)) return fail(RNNTG_E_CUDA, "tensor map encode failed");
+    CK(encproj_launch(plan, 0));
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy2D(fp, sizeof(float) * M.J, od, sizeof(float) * M.Jp, sizeof(float) * M.J, rows,
                     cudaMemcpyDeviceToHost));
@@ -1012,6 +1026,8 @@ namespace {
 cudaError_t add_encproj(Builder& b, rnntg_decoder* d) {
   const DevModel& M = d->m->dm;
   const int rows = d->B * d->T;
-  return encproj_add_node(b.g, &b.last, &b.last_kernel, M, d->m->tc_ok, d->x_dev, d->st.fp, rows);
+  (void)M;
+  (void)rows;
+  return encproj_add_node(b.g, &b.last, &b.last_kernel, d->enc);
 }
 }  // namespace
