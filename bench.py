@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--exec", default="graph", choices=["graph", "persistent"])
+    ap.add_argument("--exec", default="persistent", choices=["graph", "persistent"],
+                    help="persistent kernel (default, fastest) or the conditional-WHILE CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-compare", action="store_true",
