@@ -300,10 +300,28 @@ def measure_alt_exec(args, L_, model, cfg, xd, ld, Bl, T, frames_all):
         s = Stats()
         check(L_.rnntg_get_stats(dh, C.byref(s)))
         tot += s.gpu_ms
+    idle = measure_idle(L_, dh)
     check(L_.rnntg_decoder_destroy(dh))
     ms = tot / n
     return {"exec": other, "value": frames_all / (ms / 1000.0), "ms_per_step": ms,
-            "us_per_step": 1000.0 * ms / max(s.joint_evals, 1)}
+            "us_per_step": 1000.0 * ms / max(s.joint_evals, 1), "gpu_idle": idle}
+
+
+def measure_idle(L_, dh):
+    """One decode traced with CUPTI kernel activity: GPU idle % over the decode
+    (1 - union of kernel intervals / first-start..last-end span).  Not timed."""
+    from paper_2406_03791_b200._lib import check
+    busy, span, nk = C.c_double(), C.c_double(), C.c_int64()
+    if L_.rnntg_trace_begin() != 0:
+        return None
+    check(L_.rnntg_launch(dh))
+    check(L_.rnntg_sync(dh))
+    check(L_.rnntg_trace_end(C.byref(busy), C.byref(span), C.byref(nk)))
+    if span.value <= 0:
+        return None
+    return {"idle_pct": 100.0 * (1.0 - busy.value / span.value), "busy_ms": busy.value,
+            "span_ms": span.value, "kernels": nk.value,
+            "note": "CUPTI kernel records; a persistent kernel's barrier spin counts as busy"}
 
 
 def config_json(args, cfg):
@@ -426,6 +444,7 @@ def main():
         # verify the e2e decode agrees with the device-input decode
         # (same inputs -> identical counts)
 
+    idle = measure_idle(L_, dh)
     alt = None
     if not args.no_compare:
         alt = measure_alt_exec(args, L_, model, cfg, xd, ld, Bl, T, frames_all)
@@ -452,7 +471,7 @@ def main():
             "inner_steps_per_decode": inner, "pred_steps_per_decode": st.pred_steps,
             "outer_iters_per_decode": st.outer_iters,
             "tokens_per_frame": st.emitted / max(per_rank_frames, 1),
-            "gpu_idle_pct": None,
+            "gpu_idle_pct": idle["idle_pct"] if idle else None, "gpu_idle": idle,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches_per_step * args.steps),
             "clocks": clk, "step_ms": step_ms, "alt_exec": alt,

@@ -162,6 +162,14 @@ rnntg_status rnntg_time_kernel(rnntg_decoder* d, int which, int reps, float* avg
  * the last call; needs RNNTG_PROF=1 at decoder creation). */
 rnntg_status rnntg_debug_profile(rnntg_decoder* d, unsigned long long* out16);
 
+/* GPU idle fraction of the work issued between begin and end, from CUPTI
+ * kernel activity records (graph kernel nodes reported individually):
+ * busy = union of kernel intervals, span = first kernel start -> last end;
+ * idle = 1 - busy / span (the reference's TimingReport.idle_fraction,
+ * engine.cpp:329-366, measured on the device). */
+rnntg_status rnntg_trace_begin(void);
+rnntg_status rnntg_trace_end(double* busy_ms, double* span_ms, int64_t* kernels);
+
 /* Encoder projection only (K1): fp[M,J] = x[M,F] @ enc_proj, host buffers. */
 rnntg_status rnntg_enc_proj(rnntg_model* m, int rows, const float* x, float* fp);
 
