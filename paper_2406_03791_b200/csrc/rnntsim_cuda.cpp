@@ -1,0 +1,204 @@
+// rnntsim_cuda.cpp — the C++ drop-in (include/rnntsim_cuda.hpp) over the C ABI.
+// Compiled against the reference headers (decoders.hpp / model.hpp / tensor.hpp)
+// and linked with the reference library that defines Tensor, Engine and the
+// exception types; see paper_2406_03791_b200/csrc/Makefile target `dropin`.
+#include "rnntsim_cuda.hpp"
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "rnntsim/errors.hpp"
+
+namespace rnntsim {
+namespace cuda {
+namespace {
+
+rnntg_exec g_exec = RNNTG_EXEC_PERSISTENT;
+std::mutex g_mu;
+std::map<const DecoderModel*, rnntg_model*> g_models;
+std::map<const Engine*, int64_t> g_joint_evals;
+
+[[noreturn]] void raise(rnntg_status s) {
+  const std::string msg = rnntg_last_error();
+  switch (s) {
+    case RNNTG_E_VALUE: throw ValueError(msg);
+    case RNNTG_E_DIMENSION: throw DimensionError(msg);
+    case RNNTG_E_DTYPE: throw DtypeError(msg);
+    case RNNTG_E_INDEX: throw IndexError(msg);
+    case RNNTG_E_STATE: throw StateError(msg);
+    case RNNTG_E_STRUCTURE: throw StructureError(msg);
+    case RNNTG_E_RUNAWAY: throw RunawayLoopError(msg);
+    default: throw Error("CUDA: " + msg);
+  }
+}
+
+void check(rnntg_status s) {
+  if (s != RNNTG_OK) raise(s);
+}
+
+rnntg_model* upload(const DecoderModel& model) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_models.find(&model);
+  if (it != g_models.end()) return it->second;
+  rnntg_dims d{};
+  std::vector<const float*> w;
+  if (const auto* nm = dynamic_cast<const NeuralModel*>(&model)) {
+    const RnntParams& p = nm->params();
+    d.vocab = p.dims.vocab;
+    d.embed = p.dims.embed;
+    d.hidden = p.dims.hidden;
+    d.layers = 1;
+    d.cell = RNNTG_CELL_TANH;
+    d.joint = p.dims.joint;
+    d.feature = p.dims.feature;
+    d.num_durations = static_cast<int32_t>(p.dims.durations.size());
+    for (int i = 0; i < d.num_durations; ++i) d.durations[i] = p.dims.durations[i];
+    w = {p.embedding.f32().data(), p.w_ih.f32().data(), p.w_hh.f32().data(),
+         p.bias.f32().data(),      p.enc_proj.f32().data(), p.pred_proj.f32().data(),
+         p.out_proj.f32().data()};
+    if (d.num_durations) w.push_back(p.dur_proj.f32().data());
+  } else if (const auto* ws = dynamic_cast<const CudaWeightSource*>(&model)) {
+    d = ws->cuda_dims();
+    w = ws->cuda_weights();
+  } else {
+    throw StateError("model exports no weights: derive it from rnntsim::cuda::CudaWeightSource");
+  }
+  rnntg_model* m = nullptr;
+  check(rnntg_model_create(0, &d, w.data(), static_cast<int>(w.size()), &m));
+  g_models[&model] = m;
+  return m;
+}
+
+// bind_decode_inputs' validation (decoders.cpp:124-142) on reference Tensors.
+void validate(const Tensor& x, const Tensor& out_len, int batch, int frames, int feature,
+              int max_symbols) {
+  if (max_symbols < 1) throw ValueError("max_symbols must be >= 1");
+  if (x.rank() != 3 || x.dtype() != Dtype::Float32)
+    throw DimensionError("features must be float32 [batch, frames, features]");
+  if (x.dim(0) != batch || x.dim(1) != frames || x.dim(2) != feature)
+    throw DimensionError("feature shape does not match the decode program");
+  if (out_len.rank() != 1 || out_len.dtype() != Dtype::Int32 || out_len.dim(0) != batch)
+    throw DimensionError("out_len must be int32 [batch]");
+  for (int32_t v : out_len.i32())
+    if (v < 0 || v > frames) throw DimensionError("out_len entries must lie in [0, frames]");
+}
+
+struct Handle {
+  rnntg_decoder* d = nullptr;
+  Engine* engine = nullptr;
+  int batch = 0;
+  ~Handle() {
+    if (d) rnntg_decoder_destroy(d);
+  }
+};
+
+Hypotheses read(Handle& h) {
+  const int B = h.batch, cap = rnntg_decoder_capacity(h.d);
+  std::vector<int32_t> cnt(B), tok((size_t)B * cap), frm((size_t)B * cap);
+  std::vector<float> sc((size_t)B * cap);
+  check(rnntg_read(h.d, cnt.data(), tok.data(), frm.data(), sc.data(), nullptr, cap));
+  rnntg_stats st{};
+  check(rnntg_get_stats(h.d, &st));
+  if (h.engine) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_joint_evals[h.engine] = st.joint_evals;
+  }
+  // read_emissions (decoders.cpp:97-122): total_score summed in double
+  Hypotheses out(static_cast<size_t>(B));
+  for (int b = 0; b < B; ++b) {
+    Hypothesis& y = out[static_cast<size_t>(b)];
+    for (int i = 0; i < cnt[b]; ++i) {
+      y.tokens.push_back(tok[(size_t)b * cap + i]);
+      y.frames.push_back(frm[(size_t)b * cap + i]);
+      y.scores.push_back(sc[(size_t)b * cap + i]);
+    }
+    y.total_score = 0.0;
+    for (float s : y.scores) y.total_score += static_cast<double>(s);
+  }
+  return out;
+}
+
+Hypotheses eager(Engine& engine, const DecoderModel& model, DecodeAlgo algo, const Tensor& x,
+                 const Tensor& out_len, int max_symbols) {
+  if (x.rank() != 3) throw DimensionError("features must be rank 3 [batch, frames, features]");
+  CapturedDecoder cap = cuda::build_decode_graph(engine, model, algo, static_cast<int>(x.dim(0)),
+                                                 static_cast<int>(x.dim(1)), max_symbols);
+  return cuda::replay_decode(cap, x, out_len);
+}
+
+}  // namespace
+
+void set_executor(rnntg_exec exec) { g_exec = exec; }
+rnntg_exec executor() { return g_exec; }
+
+CapturedDecoder build_decode_graph(Engine& engine, const DecoderModel& model, DecodeAlgo algo,
+                                   int batch, int max_frames, int max_symbols) {
+  if (batch < 1 || max_frames < 1) throw ValueError("batch and frames must be >= 1");
+  if (max_symbols < 1) throw ValueError("max_symbols must be >= 1");
+  if (algo == DecodeAlgo::TdtLabelLoop && !model.has_duration_head())
+    throw StateError("duration-head decoding needs a model with a duration head");
+  rnntg_model* m = upload(model);
+  auto h = std::make_shared<Handle>();
+  h->engine = &engine;
+  h->batch = batch;
+  const int a = algo == DecodeAlgo::FrameSync ? RNNTG_ALGO_FRAME_SYNC
+                : algo == DecodeAlgo::LabelLoop ? RNNTG_ALGO_LABEL_LOOP
+                                                : RNNTG_ALGO_TDT_LABEL_LOOP;
+  check(rnntg_decoder_create(m, a, g_exec, batch, max_frames, max_symbols, &h->d));
+  CapturedDecoder cap;
+  cap.engine = &engine;
+  cap.algo = algo;
+  cap.batch = batch;
+  cap.max_frames = max_frames;
+  cap.feature_dim = model.feature_dim();
+  cap.max_symbols = max_symbols;
+  const int feature = model.feature_dim();
+  // bind = validate + H2D + one asynchronous launch; read = D2H + unpack.
+  cap.bind_inputs = [h, batch, max_frames, feature, max_symbols](const Tensor& x,
+                                                                 const Tensor& out_len) {
+    validate(x, out_len, batch, max_frames, feature, max_symbols);
+    check(rnntg_bind(h->d, x.f32().data(), out_len.i32().data()));
+    check(rnntg_launch(h->d));
+  };
+  cap.read_hypotheses = [h]() { return read(*h); };
+  return cap;
+}
+
+Hypotheses replay_decode(CapturedDecoder& captured, const Tensor& x, const Tensor& out_len) {
+  if (!captured.engine || !captured.bind_inputs)
+    throw StateError("captured decoder is not initialized");
+  captured.bind_inputs(x, out_len);
+  return captured.read_hypotheses();
+}
+
+Hypotheses greedy_decode_sync_free(Engine& engine, const DecoderModel& model, const Tensor& x,
+                                   const Tensor& out_len, int max_symbols) {
+  return eager(engine, model, DecodeAlgo::FrameSync, x, out_len, max_symbols);
+}
+
+Hypotheses label_looping_decode(Engine& engine, const DecoderModel& model, const Tensor& x,
+                                const Tensor& out_len, int max_symbols) {
+  return eager(engine, model, DecodeAlgo::LabelLoop, x, out_len, max_symbols);
+}
+
+Hypotheses tdt_label_looping_decode(Engine& engine, const DecoderModel& model, const Tensor& x,
+                                    const Tensor& out_len, int max_symbols) {
+  return eager(engine, model, DecodeAlgo::TdtLabelLoop, x, out_len, max_symbols);
+}
+
+int64_t decode_joint_evals(const Engine& engine) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_joint_evals.find(&engine);
+  return it == g_joint_evals.end() ? 0 : it->second;
+}
+
+void release_models() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto& kv : g_models) rnntg_model_destroy(kv.second);
+  g_models.clear();
+}
+
+}  // namespace cuda
+}  // namespace rnntsim

@@ -1,0 +1,178 @@
+// test_dropin.cpp — the reference's own acceptance checks (tests/acceptance.cpp
+// criteria 1-2, test_decoders.cpp) run through the C++ drop-in
+// rnntsim::cuda::* (include/rnntsim_cuda.hpp) against the UNMODIFIED
+// reference decoders, in one binary linked with the reference library
+// (oracle/_ref) and the CUDA library.  Prints PASS/FAIL lines; exit code =
+// number of failures.  Needs a B200.
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "decode_test_util.hpp"
+#include "lstm_model.hpp"
+#include "rnntsim/decoders.hpp"
+#include "rnntsim/errors.hpp"
+#include "rnntsim_cuda.hpp"
+
+using namespace rnntsim;
+
+namespace {
+
+int g_fail = 0;
+
+void report(const char* name, bool ok, const std::string& detail) {
+  std::printf("%s: %s  %s\n", name, ok ? "PASS" : "FAIL", detail.c_str());
+  if (!ok) ++g_fail;
+}
+
+// Tokens and frames exact; scores within 1e-4 relative (denominator
+// max(|ref|, 1e-3)); the GPU fp32 arithmetic differs from the reference's
+// sequential order at the ulp level (SURVEY.md §8c comparator).
+bool same(const Hypotheses& a, const Hypotheses& b, double* max_rel) {
+  if (a.size() != b.size()) return false;
+  for (size_t i = 0; i < a.size(); ++i) {
+    if (a[i].tokens != b[i].tokens || a[i].frames != b[i].frames) return false;
+    for (size_t j = 0; j < a[i].scores.size(); ++j) {
+      const double r = std::fabs((double)a[i].scores[j] - b[i].scores[j]) /
+                       std::max(std::fabs((double)b[i].scores[j]), 1e-3);
+      *max_rel = std::max(*max_rel, r);
+      if (r > 1e-4) return false;
+    }
+  }
+  return true;
+}
+
+class CudaLstm : public oracle::LstmModel, public cuda::CudaWeightSource {
+ public:
+  CudaLstm(const orc_dims& d, std::vector<std::vector<float>> w)
+      : oracle::LstmModel(d, ptrs(w).data()), d_(d), w_(std::move(w)) {}
+  rnntg_dims cuda_dims() const override {
+    rnntg_dims r{};
+    r.vocab = d_.vocab;
+    r.embed = d_.embed;
+    r.hidden = d_.hidden;
+    r.layers = d_.layers;
+    r.cell = RNNTG_CELL_LSTM;
+    r.joint = d_.joint;
+    r.feature = d_.feature;
+    r.num_durations = d_.num_durations;
+    for (int i = 0; i < d_.num_durations; ++i) r.durations[i] = d_.durations[i];
+    return r;
+  }
+  std::vector<const float*> cuda_weights() const override {
+    std::vector<const float*> p;
+    for (const auto& v : w_) p.push_back(v.data());
+    return p;
+  }
+
+ private:
+  static std::vector<const float*> ptrs(const std::vector<std::vector<float>>& w) {
+    std::vector<const float*> p;
+    for (const auto& v : w) p.push_back(v.data());
+    return p;
+  }
+  orc_dims d_;
+  std::vector<std::vector<float>> w_;
+};
+
+}  // namespace
+
+int main() {
+  if (rnntg_device_count() < 1) {
+    std::printf("no CUDA device\n");
+    return 1;
+  }
+  for (rnntg_exec ex : {RNNTG_EXEC_GRAPH, RNNTG_EXEC_PERSISTENT}) {
+    cuda::set_executor(ex);
+    const char* en = ex == RNNTG_EXEC_GRAPH ? "graph" : "persistent";
+    // criterion 1 analogue: 200 random configs x 4 drop-in decoders
+    int mism = 0;
+    double rel = 0.0;
+    for (uint64_t seed = 1; seed <= 200; ++seed) {
+      const testutil::RandomCase c = testutil::make_random_case(seed, false);
+      const Hypotheses expect = testutil::oracle_batch(c.model, c.x, c.out_len, c.max_symbols, false);
+      Engine eng;
+      std::vector<Hypotheses> got;
+      got.push_back(cuda::greedy_decode_sync_free(eng, c.model, c.x, c.out_len, c.max_symbols));
+      got.push_back(cuda::label_looping_decode(eng, c.model, c.x, c.out_len, c.max_symbols));
+      CapturedDecoder cap = cuda::build_decode_graph(eng, c.model, DecodeAlgo::FrameSync,
+                                                     (int)c.x.dim(0), (int)c.x.dim(1), c.max_symbols);
+      got.push_back(cuda::replay_decode(cap, c.x, c.out_len));
+      // the reference's own replay_decode drives the CUDA CapturedDecoder unchanged
+      got.push_back(rnntsim::replay_decode(cap, c.x, c.out_len));
+      for (const auto& g : got)
+        if (!same(g, expect, &rel)) ++mism;
+    }
+    report((std::string("dropin exactness ") + en).c_str(), mism == 0,
+           "200 configs x 4 decoders, " + std::to_string(mism) + " mismatches, max score rel " +
+               std::to_string(rel));
+    // criterion 2 analogue: TDT seeds 1000..1199
+    mism = 0;
+    rel = 0.0;
+    for (uint64_t seed = 1000; seed < 1200; ++seed) {
+      const testutil::RandomCase c = testutil::make_random_case(seed, true);
+      Engine eng;
+      const Hypotheses got = cuda::tdt_label_looping_decode(eng, c.model, c.x, c.out_len, c.max_symbols);
+      if (!same(got, testutil::oracle_batch(c.model, c.x, c.out_len, c.max_symbols, true), &rel)) ++mism;
+    }
+    report((std::string("dropin tdt ") + en).c_str(), mism == 0,
+           "200 configs, " + std::to_string(mism) + " mismatches");
+    // 2-layer LSTM (C2 dims, short) through the unmodified reference decoders vs the drop-in
+    {
+      orc_dims d{};
+      d.vocab = 1024;
+      d.embed = d.hidden = 640;
+      d.layers = 2;
+      d.cell = ORC_CELL_LSTM;
+      d.joint = 640;
+      d.feature = 1024;
+      std::vector<std::vector<float>> w(static_cast<size_t>(orc_num_params(&d)));
+      std::vector<float*> wp;
+      for (int i = 0; i < orc_num_params(&d); ++i) {
+        int64_t r, cc;
+        orc_param_size(&d, i, &r, &cc);
+        w[i].resize(static_cast<size_t>(r * cc));
+        wp.push_back(w[i].data());
+      }
+      orc_init_params(1, &d, wp.data());
+      CudaLstm model(d, w);
+      Tensor x(Dtype::Float32, {3, 6, 1024});
+      orc_fill_uniform(2, -1.0f, 1.0f, x.f32().data(), x.numel());
+      const Tensor lens = Tensor::from_ints({6, 4, 6}, {3});
+      Engine e1, e2;
+      const Hypotheses ref = rnntsim::greedy_decode_sync_free(e1, model, x, lens, 5);
+      const Hypotheses got = cuda::greedy_decode_sync_free(e2, model, x, lens, 5);
+      rel = 0.0;
+      report((std::string("dropin lstm-2x640 ") + en).c_str(), same(got, ref, &rel),
+             "joint evals " + std::to_string(cuda::decode_joint_evals(e2)) + ", max score rel " +
+                 std::to_string(rel));
+    }
+    // error mapping (errors.hpp)
+    {
+      const testutil::RandomCase c = testutil::make_random_case(5, false);
+      Engine eng;
+      bool ok = true;
+      try {
+        cuda::greedy_decode_sync_free(eng, c.model, c.x, c.out_len, 0);
+        ok = false;
+      } catch (const ValueError&) {
+      }
+      try {
+        Tensor bad = Tensor::from_ints(std::vector<int32_t>((size_t)c.x.dim(0), 999), {c.x.dim(0)});
+        cuda::greedy_decode_sync_free(eng, c.model, c.x, bad, 2);
+        ok = false;
+      } catch (const DimensionError&) {
+      }
+      try {
+        cuda::tdt_label_looping_decode(eng, c.model, c.x, c.out_len, 2);
+        ok = false;
+      } catch (const StateError&) {
+      }
+      report((std::string("dropin errors ") + en).c_str(), ok,
+             "ValueError / DimensionError / StateError as in errors.hpp");
+    }
+  }
+  cuda::release_models();
+  return g_fail;
+}
