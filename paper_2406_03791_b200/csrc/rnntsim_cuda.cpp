@@ -5,6 +5,7 @@
 #include "rnntsim_cuda.hpp"
 
 #include <algorithm>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
@@ -17,8 +18,38 @@ namespace {
 
 rnntg_exec g_exec = RNNTG_EXEC_PERSISTENT;
 std::mutex g_mu;
-std::map<const DecoderModel*, rnntg_model*> g_models;
+// Device copies keyed by model object; an entry is reused only while the
+// object at that address still exports the same weights (a new model may be
+// constructed at a freed address), checked by a sampled fingerprint.
+struct Entry {
+  rnntg_model* m = nullptr;
+  uint64_t fp = 0;
+};
+std::map<const DecoderModel*, Entry> g_models;
 std::map<const Engine*, int64_t> g_joint_evals;
+
+uint64_t fingerprint(const rnntg_dims& d, const std::vector<const float*>& w) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&h](uint64_t v) {
+    h ^= v;
+    h *= 1099511628211ull;
+  };
+  const int64_t V1 = d.vocab + 1, H = d.hidden, E = d.embed, J = d.joint, F = d.feature;
+  const int64_t G = d.cell == RNNTG_CELL_LSTM ? 4 * H : H;
+  std::vector<int64_t> n = {V1 * E};
+  for (int l = 0; l < d.layers; ++l) n.insert(n.end(), {(l ? H : E) * G, H * G, G});
+  n.insert(n.end(), {F * J, H * J, J * V1});
+  if (d.num_durations) n.push_back(J * d.num_durations);
+  mix(static_cast<uint64_t>(d.vocab) | (static_cast<uint64_t>(d.hidden) << 20) |
+      (static_cast<uint64_t>(d.cell) << 40) | (static_cast<uint64_t>(d.num_durations) << 48));
+  for (size_t i = 0; i < w.size() && i < n.size(); ++i)
+    for (int64_t e = 0; e < n[i]; e += 97) {
+      uint32_t u;
+      std::memcpy(&u, &w[i][e], 4);
+      mix(u);
+    }
+  return h;
+}
 
 [[noreturn]] void raise(rnntg_status s) {
   const std::string msg = rnntg_last_error();
@@ -40,8 +71,6 @@ void check(rnntg_status s) {
 
 rnntg_model* upload(const DecoderModel& model) {
   std::lock_guard<std::mutex> lk(g_mu);
-  auto it = g_models.find(&model);
-  if (it != g_models.end()) return it->second;
   rnntg_dims d{};
   std::vector<const float*> w;
   if (const auto* nm = dynamic_cast<const NeuralModel*>(&model)) {
@@ -65,9 +94,16 @@ rnntg_model* upload(const DecoderModel& model) {
   } else {
     throw StateError("model exports no weights: derive it from rnntsim::cuda::CudaWeightSource");
   }
+  const uint64_t fp = fingerprint(d, w);
+  auto it = g_models.find(&model);
+  if (it != g_models.end()) {
+    if (it->second.fp == fp) return it->second.m;
+    rnntg_model_destroy(it->second.m);
+    g_models.erase(it);
+  }
   rnntg_model* m = nullptr;
   check(rnntg_model_create(0, &d, w.data(), static_cast<int>(w.size()), &m));
-  g_models[&model] = m;
+  g_models[&model] = Entry{m, fp};
   return m;
 }
 
@@ -196,7 +232,7 @@ int64_t decode_joint_evals(const Engine& engine) {
 
 void release_models() {
   std::lock_guard<std::mutex> lk(g_mu);
-  for (auto& kv : g_models) rnntg_model_destroy(kv.second);
+  for (auto& kv : g_models) rnntg_model_destroy(kv.second.m);
   g_models.clear();
 }
 
