@@ -50,6 +50,7 @@ struct PParams {
   int B, nrb, T, ms, cap, algo, L, cell;
   int H, Hp, J, Jp, V1, D, NJ;   // NJ = V1 + D joint columns
   int ns;           // per-warp slot = ns * 8 features x 32 rows (bulk-copy granule)
+  int own_smem;     // 1: hh0own / cown / gpown live in shared memory
   int dc0, dc1;     // CTAs owning duration columns: [dc0, dc1)
   long long max_iters;
   int durations[MAXD];
@@ -68,7 +69,9 @@ struct PParams {
   float* cown;          // [G][2][B][UMAX]
   float* gpown;         // [G][B][C2]
   float4* partv;        // [B][G]
-  float4* partd;        // [B][G]
+  float4* partd;        // [B][G] (unused: duration argmax goes through dmax)
+  unsigned long long* amax;  // [2][B] packed (orderable logit, ~index) token argmax per step parity
+  unsigned long long* dmax;  // [2][B] same for the duration head
   unsigned long long* prof;  // optional [16] phase times (ns) of CTA 0
   int* tokens;
   int* frames;
@@ -95,6 +98,7 @@ struct Smem {
   float* vdec;
   int* ddec;
   int* misc;     // [2]=t, [3]=sym, [4]=par
+  float* own;    // own-state (hh0 [B][C1], c [2][B][umax], gp [B][C2]) when own_smem
   uint64_t* full;  // one per warp
   uint64_t* wbar;
 };
@@ -104,9 +108,13 @@ __host__ __device__ inline size_t ring_floats(int ns) {
   return r > (size_t)RED_FLOATS ? r : (size_t)RED_FLOATS;
 }
 
-__host__ __device__ inline size_t smem_bytes(int wfloats, int ns, int B) {
+__host__ __device__ inline size_t own_floats(int B, int umax) {
+  return (size_t)B * C1 + 2 * (size_t)B * umax + (size_t)B * C2;
+}
+
+__host__ __device__ inline size_t smem_bytes(int wfloats, int ns, int B, size_t ownf = 0) {
   size_t b = (size_t)wfloats * 4 + ring_floats(ns) * 4;
-  b += (size_t)B * 4 * 7 + 64;
+  b += (size_t)B * 4 * 7 + 64 + ownf * 4;
   b = (b + 15) / 16 * 16;
   b += 8 * (NCW + 1);
   return b;
@@ -126,7 +134,9 @@ __device__ inline Smem carve_p(unsigned char* base, const PParams& P) {
   s.vdec = reinterpret_cast<float*>(ip + 5 * P.B);
   s.ddec = ip + 6 * P.B;
   s.misc = ip + 7 * P.B;
-  size_t off = (size_t)(reinterpret_cast<unsigned char*>(s.misc + 16) - base);
+  s.own = reinterpret_cast<float*>(s.misc + 16);
+  const size_t ownf = P.own_smem ? own_floats(P.B, P.cell == 1 ? UMAX_LSTM : UMAX_TANH) : 0;
+  size_t off = (size_t)(reinterpret_cast<unsigned char*>(s.own + ownf) - base);
   off = (off + 15) / 16 * 16;
   s.full = reinterpret_cast<uint64_t*>(base + off);
   s.wbar = s.full + NCW;
@@ -171,6 +181,18 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, int G) { bar_wait(ba
 __device__ __forceinline__ size_t act_idx(int b, int k, int K) {
   const int rb = b >> 5, r = b & 31;
   return ((size_t)rb * K + k) * RB + (r ^ ((k & 3) << 3));
+}
+
+// 64-bit key whose unsigned max is the lowest-index argmax of float values:
+// (order-preserving float bits << 32) | (~index).  Merged with red.max.u64,
+// which is order-independent, so the decision stays deterministic.
+__device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
+  unsigned u = __float_as_uint(v);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ((unsigned long long)u << 32) | (unsigned long long)(0xffffffffu - (unsigned)idx);
+}
+__device__ __forceinline__ int argmax_key_index(unsigned long long k) {
+  return (int)(0xffffffffu - (unsigned)(k & 0xffffffffull));
 }
 
 __device__ __forceinline__ void store_act(float* buf, int b, int k, int K, float v) {
@@ -326,9 +348,10 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
   const int n0 = own_lo(P.NJ, cta, G), n1 = own_lo(P.NJ, cta + 1, G);
   const int blank = P.V1 - 1;
   const bool fs = P.algo == ALGO_FS, tdt = P.algo == ALGO_TDT;
-  float* hh0own = P.hh0own + (size_t)cta * B * C1;
-  float* cown = P.cown + (size_t)cta * 2 * B * umax;
-  float* gpown = P.gpown + (size_t)cta * B * C2;
+  float* hh0own = P.own_smem ? sm.own : P.hh0own + (size_t)cta * B * C1;
+  float* cown = P.own_smem ? sm.own + (size_t)B * C1 : P.cown + (size_t)cta * 2 * B * umax;
+  float* gpown = P.own_smem ? sm.own + (size_t)B * C1 + 2 * (size_t)B * umax
+                            : P.gpown + (size_t)cta * B * C2;
   const float* bias = P.bias + (size_t)cta * 2 * C1;
 
   // ---- one-time setup: barriers, resident weights, control state ----
@@ -355,7 +378,13 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
     sm.ub[b] = 0;
     const int len = P.out_len[b];
     sm.flag[b] = (fs ? (0 >= len) : !(0 < len)) | 2;  // accept all for P0
-    if (cta == 0) P.counts[b] = 0;
+    if (b % G == cta) P.counts[b] = 0;
+    if (cta == 0) {
+      P.amax[b] = 0ull;
+      P.amax[B + b] = 0ull;
+      P.dmax[b] = 0ull;
+      P.dmax[B + b] = 0ull;
+    }
   }
   for (int b = 0; b < B; ++b) maxlen = max(maxlen, __ldg(&P.out_len[b]));
   // zero own state: h0/h1 (both parities) for owned units, c, hh0 (= 0 @ W), gp
@@ -534,6 +563,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
   }
 
   while (running) {
+    const int jpar = (int)(joint_evals & 1);
     // ---- J: joint logits for owned columns -> per-CTA partials ----
     {
       ASrc A{P.trunk, P.Jp, nullptr, 0};
@@ -573,7 +603,8 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
           }
           if (l8 == 0 && b < B) {
             P.partv[(size_t)b * G + cta] = make_float4(mv, ev, bv, __int_as_float(iv));
-            if (P.D) P.partd[(size_t)b * G + cta] = make_float4(md, ed, bd, __int_as_float(id));
+            if (bv != -INFINITY) atomicMax(&P.amax[jpar * B + b], argmax_key(bv, iv));
+            if (P.D && bd != -INFINITY) atomicMax(&P.dmax[jpar * B + b], argmax_key(bd, id));
           }
         }
       });
@@ -585,71 +616,44 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
     mark(1);
 
     // ---- D: decisions (identical in every CTA) ----
-    // 8 threads per row merge the row's G vocab partials (lse in log-sum-exp
-    // form, lowest-index argmax; log_softmax_into / argmax_last_into,
-    // tensor.cpp:268-312, 463-480), all loads issued up front.
+    // The argmax of every row (argmax_last_into, tensor.cpp:268-312: lowest
+    // index on ties) arrives merged in amax/dmax; every CTA reads them and
+    // applies the same rules.  Only the owner CTA of a row (b mod G) merges
+    // that row's per-CTA (max, sumexp) partials into lse (log_softmax_into,
+    // tensor.cpp:463-480) for the emitted score and writes the emission.
     {
-      for (int b0 = 0; b0 < B; b0 += NTH / 8) {
-        const int b = b0 + (tid >> 3), s8 = tid & 7;
-        float Mx = -INFINITY, Sx = 0.0f, best = -INFINITY, bestd = -INFINITY;
-        int bi = 0x7fffffff, bdi = 0x7fffffff;
-        if (b < B) {
-          constexpr int NL = 20;  // up to 160 CTAs
-          float4 pv[NL];
-#pragma unroll
-          for (int i = 0; i < NL; ++i) {
-            const int c = s8 + 8 * i;
-            pv[i] = c < G ? __ldcg(&P.partv[(size_t)b * G + c])
-                          : make_float4(-INFINITY, 0.f, -INFINITY, __int_as_float(0x7fffffff));
-          }
-#pragma unroll
-          for (int i = 0; i < NL; ++i) {
-            const float4 p = pv[i];
+      for (int b = tid; b < B; b += NTH) {
+        sm.kdec[b] = argmax_key_index(__ldcg(&P.amax[jpar * B + b]));
+        sm.ddec[b] = P.D ? P.durations[argmax_key_index(__ldcg(&P.dmax[jpar * B + b]))] : 0;
+      }
+      if (cta == 0)
+        for (int b = tid; b < B; b += NTH) {
+          P.amax[(jpar ^ 1) * B + b] = 0ull;
+          if (P.D) P.dmax[(jpar ^ 1) * B + b] = 0ull;
+        }
+      {
+        const int warp = tid >> 5, lane = tid & 31;
+        for (int b = cta + G * warp; b < B; b += G * NCW) {
+          float Mx = -INFINITY, Sx = 0.0f, best = -INFINITY;
+          for (int c = lane; c < G; c += 32) {
+            const float4 p = __ldcg(&P.partv[(size_t)b * G + c]);
             if (p.x != -INFINITY) {
               const float nm = fmaxf(Mx, p.x);
               Sx = (Sx == 0.0f ? 0.0f : Sx * expf(Mx - nm)) + p.y * expf(p.x - nm);
               Mx = nm;
-              const int pi = __float_as_int(p.w);
-              if (p.z > best || (p.z == best && pi < bi)) {
-                best = p.z;
-                bi = pi;
-              }
+              best = fmaxf(best, p.z);
             }
           }
-          if (P.D)
-            for (int c = P.dc0 + s8; c < P.dc1; c += 8) {
-              const float4 q = __ldcg(&P.partd[(size_t)b * G + c]);
-              const int qi = __float_as_int(q.w);
-              if (q.z > bestd || (q.z == bestd && qi < bdi)) {
-                bestd = q.z;
-                bdi = qi;
-              }
-            }
-        }
 #pragma unroll
-        for (int o = 4; o >= 1; o >>= 1) {
-          const float om = __shfl_xor_sync(0xffffffffu, Mx, o);
-          const float os = __shfl_xor_sync(0xffffffffu, Sx, o);
-          const float ob = __shfl_xor_sync(0xffffffffu, best, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          const float nm = fmaxf(Mx, om);
-          Sx = (Sx == 0.0f ? 0.0f : Sx * expf(Mx - nm)) + (os == 0.0f ? 0.0f : os * expf(om - nm));
-          Mx = nm;
-          if (ob > best || (ob == best && oi < bi)) {
-            best = ob;
-            bi = oi;
+          for (int o = 16; o >= 1; o >>= 1) {
+            const float om = __shfl_xor_sync(0xffffffffu, Mx, o);
+            const float os = __shfl_xor_sync(0xffffffffu, Sx, o);
+            best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+            const float nm = fmaxf(Mx, om);
+            Sx = (Sx == 0.0f ? 0.0f : Sx * expf(Mx - nm)) + (os == 0.0f ? 0.0f : os * expf(om - nm));
+            Mx = nm;
           }
-          const float obd = __shfl_xor_sync(0xffffffffu, bestd, o);
-          const int odi = __shfl_xor_sync(0xffffffffu, bdi, o);
-          if (obd > bestd || (obd == bestd && odi < bdi)) {
-            bestd = obd;
-            bdi = odi;
-          }
-        }
-        if (s8 == 0 && b < B) {
-          sm.kdec[b] = bi;
-          sm.vdec[b] = best - (Mx + logf(Sx));
-          sm.ddec[b] = P.D ? P.durations[bdi] : 0;
+          if (lane == 0) sm.vdec[b] = best - (Mx + logf(Sx));
         }
       }
       __syncthreads();
@@ -665,7 +669,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
             if (k == blank) {
               f |= 1;
             } else {
-              if (cta == 0) {
+              if (b % G == cta) {
                 const int nb = P.counts[b];
                 if (nb < P.cap) {
                   const size_t o = (size_t)b * P.cap + nb;
@@ -690,7 +694,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
             u = 0;
           } else {
             const int d = tdt ? sm.ddec[b] : 0;
-            if (cta == 0) {
+            if (b % G == cta) {
               const int nb = P.counts[b];
               if (nb < P.cap) {
                 const size_t o = (size_t)b * P.cap + nb;

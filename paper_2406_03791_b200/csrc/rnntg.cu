@@ -290,16 +290,28 @@ rnntg_status setup_persistent(rnntg_decoder* d) {
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
   if (G > nsm) return fail(RNNTG_E_VALUE, "model too wide for the persistent executor");
   const int wfloats = Hp * pk::C1 + (M.L == 2 ? 2 * Hp * pk::C1 : 0) + Hp * pk::C2 + Jp * pk::C2;
-  int ns = 0;  // activation ring slots: as many as shared memory allows
+  // Per-warp activation slot (ns*8 features) and the CTA-private own-state:
+  // prefer own-state in shared memory (saves L2 round trips in every
+  // epilogue), then the largest slot that still fits.
+  const size_t ownf = pk::own_floats(d->B, umax);
+  int ns = 0, own = 0;
+  for (int o = 1; o >= 0 && !ns; --o)
+    for (int cand = pk::MAX_NS; cand >= 3 && !ns; --cand)
+      if (pk::smem_bytes(wfloats, cand, d->B, o ? ownf : 0) <= (size_t)optin) {
+        ns = cand;
+        own = o;
+      }
   for (int cand = pk::MAX_NS; cand >= 2 && !ns; --cand)
     if (pk::smem_bytes(wfloats, cand, d->B) <= (size_t)optin) ns = cand;
   if (const char* e = std::getenv("RNNTG_NS")) {
     const int want = std::atoi(e);
-    if (want >= 2 && want <= pk::MAX_NS && pk::smem_bytes(wfloats, want, d->B) <= (size_t)optin)
+    if (want >= 2 && want <= pk::MAX_NS &&
+        pk::smem_bytes(wfloats, want, d->B, own ? ownf : 0) <= (size_t)optin)
       ns = want;
   }
+  if (env_flag("RNNTG_OWN_GLOBAL", false)) own = 0;
   if (!ns) return fail(RNNTG_E_VALUE, "persistent executor: weights exceed shared memory");
-  d->psmem = pk::smem_bytes(wfloats, ns, d->B);
+  d->psmem = pk::smem_bytes(wfloats, ns, d->B, own ? ownf : 0);
   CK(cudaFuncSetAttribute(pk::persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)d->psmem));
   int per_sm = 0;
@@ -359,6 +371,7 @@ rnntg_status setup_persistent(rnntg_decoder* d) {
   pp.D = D;
   pp.NJ = NJ;
   pp.ns = ns;
+  pp.own_smem = own;
   pp.max_iters = d->st.max_iters;
   for (int i = 0; i < D; ++i) pp.durations[i] = dd.durations[i];
   pp.wfloats = wfloats;
@@ -384,6 +397,8 @@ rnntg_status setup_persistent(rnntg_decoder* d) {
   CK(d->mem.alloc(&pp.gpown, (size_t)G * d->B * pk::C2));
   CK(d->mem.alloc(&pp.partv, (size_t)G * d->B));
   CK(d->mem.alloc(&pp.partd, (size_t)G * d->B));
+  CK(d->mem.alloc(&pp.amax, (size_t)2 * d->B));
+  CK(d->mem.alloc(&pp.dmax, (size_t)2 * d->B));
   CK(d->mem.alloc(&pp.bar, 2));
   if (env_flag("RNNTG_PROF", false)) CK(d->mem.alloc(&pp.prof, 16));
   // CTAs owning duration-head columns (joint columns >= V1)
