@@ -99,6 +99,7 @@ struct Smem {
   int* ddec;
   int* misc;     // [2]=t, [3]=sym, [4]=par
   float* own;    // own-state (hh0 [B][C1], c [2][B][umax], gp [B][C2]) when own_smem
+  unsigned long long* prof;  // [16] phase-time accumulators (CTA 0, thread 0)
   uint64_t* full;  // one per warp
   uint64_t* wbar;
 };
@@ -114,7 +115,7 @@ __host__ __device__ inline size_t own_floats(int B, int umax) {
 
 __host__ __device__ inline size_t smem_bytes(int wfloats, int ns, int B, size_t ownf = 0) {
   size_t b = (size_t)wfloats * 4 + ring_floats(ns) * 4;
-  b += (size_t)B * 4 * 7 + 64 + ownf * 4;
+  b += (size_t)B * 4 * 7 + 64 + ownf * 4 + 16 * 8;
   b = (b + 15) / 16 * 16;
   b += 8 * (NCW + 1);
   return b;
@@ -138,6 +139,8 @@ __device__ inline Smem carve_p(unsigned char* base, const PParams& P) {
   const size_t ownf = P.own_smem ? own_floats(P.B, P.cell == 1 ? UMAX_LSTM : UMAX_TANH) : 0;
   size_t off = (size_t)(reinterpret_cast<unsigned char*>(s.own + ownf) - base);
   off = (off + 15) / 16 * 16;
+  s.prof = reinterpret_cast<unsigned long long*>(base + off);
+  off += 16 * 8;
   s.full = reinterpret_cast<uint64_t*>(base + off);
   s.wbar = s.full + NCW;
   return s;
@@ -310,8 +313,8 @@ __device__ __forceinline__ void gemv_pass(const Smem& sm, const PParams& P, unsi
       if (P.prof && blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long tq1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tq1));
-        P.prof[13] += tq1 - tq0;
-        P.prof[14] += 1;
+        sm.prof[13] += tq1 - tq0;
+        sm.prof[14] += 1;
       }
       const float* wk = W + (size_t)(kbeg + kk + ks) * C;
 #pragma unroll 4
@@ -329,7 +332,7 @@ __device__ __forceinline__ void gemv_pass(const Smem& sm, const PParams& P, unsi
     if (P.prof && blockIdx.x == 0 && threadIdx.x == 0) {
       unsigned long long tr1;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr1));
-      P.prof[15] += tr1 - tr0;
+      sm.prof[15] += tr1 - tr0;
     }
   }
 }
@@ -410,11 +413,12 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
   unsigned ph = 0;  // this warp's slot mbarrier phase
   long long joint_evals = 0, pred_steps = 0, outer_iters = 0, iters = 0;
   unsigned long long t_last = 0;
+  if (tid < 16) sm.prof[tid] = 0ull;
   auto mark = [&](int id) {
     if (P.prof && cta == 0 && tid == 0) {
       unsigned long long now;
-      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
-      if (t_last) P.prof[id] += now - t_last;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (t_last) sm.prof[id] += now - t_last;
       t_last = now;
     }
   };
@@ -766,6 +770,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
       __syncthreads();
     }
   }
+  if (P.prof && cta == 0 && tid < 16) P.prof[tid] += sm.prof[tid];
   if (cta == 0 && tid == 0) {
     Ctrl* c = P.ctrl;
     c->joint_evals = joint_evals;
