@@ -97,6 +97,7 @@ struct Smem {
   int* kdec;
   float* vdec;
   int* ddec;
+  int* cnt;      // emitted count per row (replicated; the owner writes global counts)
   int* misc;     // [2]=t, [3]=sym, [4]=par
   float* own;    // own-state (hh0 [B][C1], c [2][B][umax], gp [B][C2]) when own_smem
   unsigned long long* prof;  // [16] phase-time accumulators (CTA 0, thread 0)
@@ -115,7 +116,7 @@ __host__ __device__ inline size_t own_floats(int B, int umax) {
 
 __host__ __device__ inline size_t smem_bytes(int wfloats, int ns, int B, size_t ownf = 0) {
   size_t b = (size_t)wfloats * 4 + ring_floats(ns) * 4;
-  b += (size_t)B * 4 * 7 + 64 + ownf * 4 + 16 * 8;
+  b += (size_t)B * 4 * 8 + 64 + ownf * 4 + 16 * 8;
   b = (b + 15) / 16 * 16;
   b += 8 * (NCW + 1);
   return b;
@@ -134,7 +135,8 @@ __device__ inline Smem carve_p(unsigned char* base, const PParams& P) {
   s.kdec = ip + 4 * P.B;
   s.vdec = reinterpret_cast<float*>(ip + 5 * P.B);
   s.ddec = ip + 6 * P.B;
-  s.misc = ip + 7 * P.B;
+  s.cnt = ip + 7 * P.B;
+  s.misc = ip + 8 * P.B;
   s.own = reinterpret_cast<float*>(s.misc + 16);
   const size_t ownf = P.own_smem ? own_floats(P.B, P.cell == 1 ? UMAX_LSTM : UMAX_TANH) : 0;
   size_t off = (size_t)(reinterpret_cast<unsigned char*>(s.own + ownf) - base);
@@ -381,6 +383,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
     sm.ub[b] = 0;
     const int len = P.out_len[b];
     sm.flag[b] = (fs ? (0 >= len) : !(0 < len)) | 2;  // accept all for P0
+    sm.cnt[b] = 0;
     if (b % G == cta) P.counts[b] = 0;
     if (cta == 0) {
       P.amax[b] = 0ull;
@@ -626,7 +629,9 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
     // that row's per-CTA (max, sumexp) partials into lse (log_softmax_into,
     // tensor.cpp:463-480) for the emitted score and writes the emission.
     {
-      for (int b = tid; b < B; b += NTH) {
+      // argmax reads by the high warps, lse merges by the low warps: the two
+      // L2 round trips overlap
+      for (int b = NTH - 1 - tid; b >= 0 && b < B; b -= NTH) {
         sm.kdec[b] = argmax_key_index(__ldcg(&P.amax[jpar * B + b]));
         sm.ddec[b] = P.D ? P.durations[argmax_key_index(__ldcg(&P.dmax[jpar * B + b]))] : 0;
       }
@@ -674,7 +679,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
               f |= 1;
             } else {
               if (b % G == cta) {
-                const int nb = P.counts[b];
+                const int nb = sm.cnt[b];
                 if (nb < P.cap) {
                   const size_t o = (size_t)b * P.cap + nb;
                   P.tokens[o] = k;
@@ -684,6 +689,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
                   P.counts[b] = nb + 1;
                 }
               }
+              sm.cnt[b] += 1;
               sm.label[b] = k;
               f |= 2;
             }
@@ -699,7 +705,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
           } else {
             const int d = tdt ? sm.ddec[b] : 0;
             if (b % G == cta) {
-              const int nb = P.counts[b];
+              const int nb = sm.cnt[b];
               if (nb < P.cap) {
                 const size_t o = (size_t)b * P.cap + nb;
                 P.tokens[o] = k;
@@ -709,6 +715,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
                 P.counts[b] = nb + 1;
               }
             }
+            sm.cnt[b] += 1;
             sm.label[b] = k;
             f |= 2;
             u += 1;
