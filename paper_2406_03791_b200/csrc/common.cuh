@@ -31,10 +31,10 @@ struct DevModel {
   int NCHT;  // + duration chunk
   int durations[MAXD];
   const float* table0;          // [V1][GH]   embedding @ W_ih0 (exact, sequential k)
-  const float* w[MAXL];         // l=0: [Hp][GH] (W_hh0); l>0: [2Hp][GH] ([W_ih;W_hh])
+  const float* w[MAXL];         // tiled [GH/16][K][16]; K = Hp (W_hh0) or 2Hp ([W_ih;W_hh])
   const float* bias[MAXL];      // [GH]
-  const float* pred_proj;       // [Hp][Jp]
-  const float* out_ext;         // [Jp][NOUT]
+  const float* pred_proj;       // tiled [Jp/16][Hp][16]
+  const float* out_ext;         // tiled [NOUT/16][Jp][16] (out_proj || dur_proj)
   const float* enc;             // [Fp][Jp]
   const float* enc_hi;          // tcgen05 operands: enc^T split into tf32 hi/lo,
   const float* enc_lo;          // K-major [Jp][Fp]

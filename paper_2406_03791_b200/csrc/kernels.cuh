@@ -25,34 +25,46 @@ namespace rnntg {
 //   lane = (rg = lane>>2 : rows rg, rg+8, rg+16, rg+24) x (cg = lane&3 : cols 4cg..4cg+3)
 // A rows come from shared memory (row stride KS, KS % 32 == 4 so the 8 row
 // groups hit 8 distinct bank quads: one wavefront per LDS.128, broadcast over
-// cg); W comes from global/L2 as 64-byte row segments, software-pipelined two
-// 4-k groups ahead.  kw must be a multiple of 8.
+// cg).  W is stored tiled ([tile][K][16], contiguous per warp slice) and is
+// streamed through the warp's own shared-memory slot by bulk copies of WCH
+// k-rows (4 KB): bulk copies issued by one warp serialise, so every warp
+// issues its own (scripts/microbench3.cu), and the first chunk is requested
+// before griddepcontrol.wait because weights never depend on the previous
+// kernel.  kw must be a multiple of 8.
 // -------------------------------------------------------------------------
+constexpr int WCH = 64;  // W k-rows per bulk copy (64 x 16 floats = 4 KB)
+
+__device__ __forceinline__ void w_chunk_issue(const float* Wslice, int kc, int nk, float* wslot,
+                                              uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_arrive_expect_tx(bar, (uint32_t)(nk * CT * sizeof(float)));
+  bulk_g2s(wslot, Wslice + (size_t)kc * CT, (uint32_t)(nk * CT * sizeof(float)), bar);
+}
+
 __device__ __forceinline__ void warp_gemv_32x16(const float* __restrict__ As, int KS,
-                                                const float* __restrict__ W, int ldw, int col0,
-                                                int k0, int kw, float (&acc)[4][4]) {
+                                                const float* __restrict__ Wslice, int k0, int kw,
+                                                float* wslot, uint64_t* wbar, bool first_issued,
+                                                float (&acc)[4][4]) {
   const int lane = threadIdx.x & 31, rg = lane >> 2, cg = lane & 3;
-  const float* wp = W + (size_t)k0 * ldw + col0 + 4 * cg;
   const float* ap = As + rg * KS + k0;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
-  float4 wc[8], wn[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) wc[q] = ldg4(wp + (size_t)q * ldw);
-  for (int k = 0; k < kw; k += 8) {
-    if (k + 8 < kw) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) wn[q] = ldg4(wp + (size_t)(k + 8 + q) * ldw);
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
+  uint32_t ph = 0;
+  for (int kc = 0; kc < kw; kc += WCH) {
+    const int nk = kw - kc < WCH ? kw - kc : WCH;
+    if (lane == 0 && !(kc == 0 && first_issued)) w_chunk_issue(Wslice, kc, nk, wslot, wbar);
+    mbar_wait(wbar, ph);
+    ph ^= 1u;
+    const float* wr = wslot + 4 * cg;
+#pragma unroll 2
+    for (int k = 0; k < nk; k += 4) {
+      const float4 w0 = lds4(wr + (k + 0) * CT), w1 = lds4(wr + (k + 1) * CT),
+                   w2 = lds4(wr + (k + 2) * CT), w3 = lds4(wr + (k + 3) * CT);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const float4 a = lds4(ap + i * 8 * KS + k + 4 * h);
-        const float4 w0 = wc[4 * h + 0], w1 = wc[4 * h + 1], w2 = wc[4 * h + 2],
-                     w3 = wc[4 * h + 3];
+        const float4 a = lds4(ap + i * 8 * KS + kc + k);
         acc[i][0] = fmaf(a.x, w0.x, acc[i][0]);
         acc[i][1] = fmaf(a.x, w0.y, acc[i][1]);
         acc[i][2] = fmaf(a.x, w0.z, acc[i][2]);
@@ -71,8 +83,7 @@ __device__ __forceinline__ void warp_gemv_32x16(const float* __restrict__ As, in
         acc[i][3] = fmaf(a.w, w3.w, acc[i][3]);
       }
     }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) wc[q] = wn[q];
+    __syncwarp();
   }
 }
 
@@ -94,23 +105,46 @@ __device__ __forceinline__ float reduce_partial(const float* red, int r, int c) 
   return s;
 }
 
-// Shared-memory carve-up of the step kernels: [NW mbarriers][As 32 x KS][red].
+// Shared-memory carve-up of the step kernels:
+// [NW A-mbarriers][NW W-mbarriers][flag][As 32 x KS][red][NW W slots].
 struct StepSmem {
   uint64_t* bars;
+  uint64_t* wbars;
   float* As;
   float* red;
+  float* wslots;
   int* flag;
 };
 __device__ __forceinline__ StepSmem carve(void* base, int KS) {
   StepSmem s;
   s.bars = reinterpret_cast<uint64_t*>(base);
-  s.flag = reinterpret_cast<int*>(s.bars + NW);
-  s.As = reinterpret_cast<float*>(reinterpret_cast<char*>(base) + 128);
+  s.wbars = s.bars + NW;
+  s.flag = reinterpret_cast<int*>(s.wbars + NW);
+  s.As = reinterpret_cast<float*>(reinterpret_cast<char*>(base) + 256);
   s.red = s.As + RB * KS;
+  s.wslots = s.red + NW * RB * CT;
   return s;
 }
 __host__ __device__ inline size_t step_smem_bytes(int K) {
-  return 128 + sizeof(float) * ((size_t)RB * (K + 4) + (size_t)NW * RB * CT);
+  return 256 + sizeof(float) * ((size_t)RB * (K + 4) + (size_t)NW * RB * CT + (size_t)NW * WCH * CT);
+}
+
+// Per-warp W slot and the first-chunk prefetch (issued before the PDL wait).
+__device__ __forceinline__ float* warp_wslot(const StepSmem& sm) {
+  return sm.wslots + (threadIdx.x >> 5) * WCH * CT;
+}
+__device__ __forceinline__ void init_step_barriers(const StepSmem& sm) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    mbar_init(&sm.bars[warp], 1);
+    mbar_init(&sm.wbars[warp], 1);
+  }
+  fence_mbar_init();
+  __syncwarp();
+}
+__device__ __forceinline__ void prefetch_w(const StepSmem& sm, const float* Wslice, int kw) {
+  if ((threadIdx.x & 31) == 0)
+    w_chunk_issue(Wslice, 0, kw < WCH ? kw : WCH, warp_wslot(sm), &sm.wbars[threadIdx.x >> 5]);
 }
 
 // Stage this warp's k-slice of 32 activation rows with the bulk-copy (TMA)
@@ -235,21 +269,21 @@ __global__ void __launch_bounds__(NT) pred_layer_kernel(DevModel M, DevState S, 
   StepSmem sm = carve(smem_raw, KS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x, rb = blockIdx.y, row0 = rb * RB, col0 = tile * CT;
-  if (lane == 0) mbar_init(&sm.bars[warp], 1);
-  fence_mbar_init();
-  __syncwarp();
+  const int kw = K / NW, k0 = warp * kw;
+  const float* wslice = M.w[l] + ((size_t)tile * K + k0) * CT;  // tiled [tile][K][16]
+  init_step_barriers(sm);
+  prefetch_w(sm, wslice, kw);
   pdl_trigger();
   pdl_wait();
   const int par = ld_volatile(&S.ctrl->par);
   const int cur = par, nxt = par ^ 1;
-  const int kw = K / NW, k0 = warp * kw;
   if (l == 0)
     stage_rows_bulk(sm, KS, row0, S.h[0][cur], S.h[0][cur], K, M.Hp, k0, kw);
   else
     stage_rows_bulk(sm, KS, row0, S.h[l - 1][nxt], S.h[l][cur], M.Hp, M.Hp, k0, kw);
   mbar_wait(&sm.bars[warp], 0);
   float acc[4][4];
-  warp_gemv_32x16(sm.As, KS, M.w[l], M.GH, col0, k0, kw, acc);
+  warp_gemv_32x16(sm.As, KS, wslice, k0, kw, warp_wslot(sm), &sm.wbars[warp], true, acc);
   store_partial(sm.red, acc);
   __syncthreads();
   const float* bias = M.bias[l];
@@ -345,18 +379,19 @@ __global__ void __launch_bounds__(NT) pred_proj_kernel(DevModel M, DevState S) {
   StepSmem sm = carve(smem_raw, KS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x, rb = blockIdx.y, row0 = rb * RB, col0 = tile * CT;
-  if (lane == 0) mbar_init(&sm.bars[warp], 1);
-  fence_mbar_init();
-  __syncwarp();
+  const int kw = K / NW, k0 = warp * kw;
+  const float* wslice = M.pred_proj + ((size_t)tile * K + k0) * CT;  // tiled [tile][Hp][16]
+  (void)lane;
+  init_step_barriers(sm);
+  prefetch_w(sm, wslice, kw);
   pdl_trigger();
   pdl_wait();
   const int nxt = ld_volatile(&S.ctrl->par) ^ 1;
-  const int kw = K / NW, k0 = warp * kw;
   const float* htop = S.h[M.L - 1][nxt];
   stage_rows_bulk(sm, KS, row0, htop, htop, K, M.Hp, k0, kw);
   mbar_wait(&sm.bars[warp], 0);
   float acc[4][4];
-  warp_gemv_32x16(sm.As, KS, M.pred_proj, M.Jp, col0, k0, kw, acc);
+  warp_gemv_32x16(sm.As, KS, wslice, k0, kw, warp_wslot(sm), &sm.wbars[warp], true, acc);
   store_partial(sm.red, acc);
   __syncthreads();
   for (int o = threadIdx.x; o < RB * CT; o += NT) {
@@ -470,12 +505,15 @@ __global__ void __launch_bounds__(NT) joint_kernel(DevModel M, DevState S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int chunk = blockIdx.x, rb = blockIdx.y, row0 = rb * RB, col0 = chunk * CT;
   const bool dur_chunk = chunk >= M.NCH;
+  const int kw = K / NW, k0 = warp * kw, kq = kw / 4;
+  const float* wslice = M.out_ext + ((size_t)chunk * K + k0) * CT;  // tiled [chunk][Jp][16]
+  init_step_barriers(sm);
+  prefetch_w(sm, wslice, kw);
   pdl_trigger();
   pdl_wait();
   const bool fs = S.algo == ALGO_FS;
   const int tf = fs ? ld_volatile(&S.ctrl->t) : 0;
   // ---- stage trunk rows (this warp's k-slice) ----
-  const int kw = K / NW, k0 = warp * kw, kq = kw / 4;
   for (int p = lane; p < RB * kq; p += 32) {
     const int r = p / kq, q = p % kq, b = row0 + r;
     const int k = k0 + 4 * q;
@@ -495,7 +533,7 @@ __global__ void __launch_bounds__(NT) joint_kernel(DevModel M, DevState S) {
   }
   __syncwarp();
   float acc[4][4];
-  warp_gemv_32x16(sm.As, KS, M.out_ext, M.NOUT, col0, k0, kw, acc);
+  warp_gemv_32x16(sm.As, KS, wslice, k0, kw, warp_wslot(sm), &sm.wbars[warp], true, acc);
   store_partial(sm.red, acc);
   __syncthreads();
   // ---- per-row chunk statistics: half-warp per row ----

@@ -125,6 +125,17 @@ rnntg_status validate_dims(const rnntg_dims* d) {
 
 int num_weights(const rnntg_dims* d) { return 1 + 3 * d->layers + 3 + (d->num_durations > 0); }
 
+// [K][N] row-major -> [N/CT][K][CT]: each step-GEMV tile's weights (and every
+// warp's k-slice of them) become one contiguous block for bulk copies.
+std::vector<float> tile16(const std::vector<float>& W, int K, int N) {
+  std::vector<float> T(W.size());
+  for (int t = 0; t < N / CT; ++t)
+    for (int k = 0; k < K; ++k)
+      for (int c = 0; c < CT; ++c)
+        T[((size_t)t * K + k) * CT + c] = W[(size_t)k * N + t * CT + c];
+  return T;
+}
+
 template <typename T>
 cudaError_t upload(DevBuf& mem, T** dst, const std::vector<T>& src) {
   cudaError_t e = mem.alloc(dst, src.size());
@@ -548,7 +559,7 @@ rnntg_status rnntg_model_create(int device, const rnntg_dims* dims, const float*
       for (int k = 0; k < H; ++k)
         for (int c = 0; c < gcols; ++c) W[(size_t)k * GH + gcol(c)] = w_ih[(size_t)k * gcols + c];
     float* dw = nullptr;
-    CKM(upload(m->mem, &dw, W));
+    CKM(upload(m->mem, &dw, tile16(W, rows, GH)));
     M.w[l] = dw;
     std::vector<float> bv(GH, 0.0f);
     for (int c = 0; c < gcols; ++c) bv[gcol(c)] = bias[c];
@@ -575,7 +586,7 @@ rnntg_status rnntg_model_create(int device, const rnntg_dims* dims, const float*
     for (int k = 0; k < H; ++k)
       for (int j = 0; j < J; ++j) pp[(size_t)k * Jp + j] = weights[base + 1][(size_t)k * J + j];
     float* dp = nullptr;
-    CKM(upload(m->mem, &dp, pp));
+    CKM(upload(m->mem, &dp, tile16(pp, Hp, Jp)));
     M.pred_proj = dp;
   }
   {
@@ -586,7 +597,7 @@ rnntg_status rnntg_model_create(int device, const rnntg_dims* dims, const float*
         oe[(size_t)k * M.NOUT + M.V1p + c] = weights[base + 3][(size_t)k * M.D + c];
     }
     float* dp = nullptr;
-    CKM(upload(m->mem, &dp, oe));
+    CKM(upload(m->mem, &dp, tile16(oe, Jp, M.NOUT)));
     M.out_ext = dp;
   }
   {
