@@ -155,10 +155,19 @@ __device__ __forceinline__ void stage_rows_bulk(const StepSmem& sm, int KS, int 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float* src = k0 < seg_k ? src0 : src1;
   const int koff = k0 < seg_k ? k0 : k0 - seg_k;
-  if (lane == 0) mbar_arrive_expect_tx(&sm.bars[warp], (uint32_t)(RB * kw * sizeof(float)));
+  // Rows are not contiguous in global memory, so a per-row bulk copy would
+  // issue 32 serialised copies per warp; 16-byte cp.async from every lane
+  // keeps all of them in flight instead.
+  (void)warp;
+  const int q4 = kw / 4;
+  for (int p = lane; p < RB * q4; p += 32) {
+    const int r = p / q4, q = p % q4;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sm.As + r * KS + k0 + 4 * q)),
+                 "l"(src + (size_t)(row0 + r) * ld + koff + 4 * q)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
   __syncwarp();
-  bulk_g2s(sm.As + lane * KS + k0, src + (size_t)(row0 + lane) * ld + koff,
-           (uint32_t)(kw * sizeof(float)), &sm.bars[warp]);
 }
 
 // -------------------------------------------------------------------------
@@ -281,7 +290,6 @@ __global__ void __launch_bounds__(NT) pred_layer_kernel(DevModel M, DevState S, 
     stage_rows_bulk(sm, KS, row0, S.h[0][cur], S.h[0][cur], K, M.Hp, k0, kw);
   else
     stage_rows_bulk(sm, KS, row0, S.h[l - 1][nxt], S.h[l][cur], M.Hp, M.Hp, k0, kw);
-  mbar_wait(&sm.bars[warp], 0);
   float acc[4][4];
   warp_gemv_32x16(sm.As, KS, wslice, k0, kw, warp_wslot(sm), &sm.wbars[warp], true, acc);
   store_partial(sm.red, acc);
@@ -389,7 +397,6 @@ __global__ void __launch_bounds__(NT) pred_proj_kernel(DevModel M, DevState S) {
   const int nxt = ld_volatile(&S.ctrl->par) ^ 1;
   const float* htop = S.h[M.L - 1][nxt];
   stage_rows_bulk(sm, KS, row0, htop, htop, K, M.Hp, k0, kw);
-  mbar_wait(&sm.bars[warp], 0);
   float acc[4][4];
   warp_gemv_32x16(sm.As, KS, wslice, k0, kw, warp_wslot(sm), &sm.wbars[warp], true, acc);
   store_partial(sm.red, acc);
