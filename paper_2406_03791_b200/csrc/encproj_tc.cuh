@@ -267,9 +267,9 @@ inline bool encproj_tc_supported(const DevModel& M) {
   if (major != 10 || minor != 0) return false;
   if (!get_encode_tiled()) return false;
   if (M.Fp % tc::BK != 0 || M.Jp % 64 != 0) return false;
-  const int BN = M.Jp % 128 == 0 ? 128 : 64;
+  // the attribute is per function, shared by every model: set the largest tile's need
   return cudaFuncSetAttribute(tc::encproj_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)tc::smem_bytes(BN)) == cudaSuccess;
+                              (int)tc::smem_bytes(128)) == cudaSuccess;
 }
 
 // x: [rows][Fp] (pitched, zero-padded), out: [rows][Jp].

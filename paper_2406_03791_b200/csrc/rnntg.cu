@@ -192,8 +192,18 @@ size_t layer_smem(const DevModel& M, int l) { return step_smem_bytes(l == 0 ? M.
 size_t pp_smem(const DevModel& M) { return step_smem_bytes(M.Hp); }
 
 cudaError_t set_smem_attrs(const DevModel& M) {
-  const int big = (int)std::max({joint_smem(M), layer_smem(M, 1), layer_smem(M, 0), pp_smem(M)});
-  cudaError_t e;
+  // The attribute belongs to the kernel, not to a model: set the device
+  // maximum so a smaller model created later cannot lower it below what an
+  // earlier, larger model's launches need.
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) !=
+      cudaSuccess)
+    return e;
+  const int need = (int)std::max({joint_smem(M), layer_smem(M, 1), layer_smem(M, 0), pp_smem(M)});
+  if (need > optin) return cudaErrorInvalidValue;
+  const int big = optin;
   if ((e = cudaFuncSetAttribute(pred_layer_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 big)) != cudaSuccess)
     return e;
@@ -323,8 +333,9 @@ rnntg_status setup_persistent(rnntg_decoder* d) {
   if (env_flag("RNNTG_OWN_GLOBAL", false)) own = 0;
   if (!ns) return fail(RNNTG_E_VALUE, "persistent executor: weights exceed shared memory");
   d->psmem = pk::smem_bytes(wfloats, ns, d->B, own ? ownf : 0);
+  // per-kernel attribute shared by all decoders: set the device maximum
   CK(cudaFuncSetAttribute(pk::persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)d->psmem));
+                          optin));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pk::persistent_kernel, pk::NTH,
                                                    d->psmem));
