@@ -43,7 +43,7 @@ constexpr int NCW = 8;          // warps; each streams its own k-slice
 constexpr int NTH = NCW * 32;
 constexpr int MAXB = 256;       // rows per decoder in the persistent path
 constexpr int MAX_NS = 4;       // slot sizes tried: ns * 8 features (32, 24, 16)
-constexpr int RED_FLOATS = 4 * RB * C1;
+constexpr int RED_FLOATS = NCW * RB * C1;
 
 struct PParams {
   int G;            // CTAs
@@ -237,41 +237,44 @@ __device__ __forceinline__ void mac_step(const float4 a, const float* wr, float 
   }
 }
 
-// Reduce acc over the 4 ks lanes and the 8 warps into sm.red ([4][32][C],
-// summed in fixed order ((w0+w4)+(w1+w5))+((w2+w6)+(w3+w7)) by red_sum).
+// Reduce acc over the 4 ks lanes and the 8 warps.  Across ks a butterfly
+// reduce-scatter (2C + C shuffles instead of 8C for an all-reduce) leaves lane
+// ks holding row 4rq+ks's C sums; every warp then writes them to
+// sm.red[warp][32][C] and red_sum adds the 8 warps in fixed order.
 // red overlays the activation slots, so everyone must be done with them.
 template <int C>
 __device__ __forceinline__ void reduce_tile(const Smem& sm, float (&acc)[4][C]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rq = lane >> 2, ks = lane & 3;
+  const bool hi2 = (ks & 2) != 0, hi1 = (ks & 1) != 0;
+  float h[2][C];  // step A (partner lane ^ 2): keep rows {0,1} or {2,3}
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-      float v = acc[i][c];
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
-      v += __shfl_xor_sync(0xffffffffu, v, 2);
-      acc[i][c] = v;
+      const float keep = hi2 ? acc[2 + i][c] : acc[i][c];
+      const float send = hi2 ? acc[i][c] : acc[2 + i][c];
+      h[i][c] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
     }
-  __syncthreads();
-  float* red = sm.red;
-  if (warp < 4 && ks == 0)
+  float q[C];  // step B (partner lane ^ 1): keep row (ks & 1) of the pair
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+  for (int c = 0; c < C; ++c) {
+    const float keep = hi1 ? h[1][c] : h[0][c];
+    const float send = hi1 ? h[0][c] : h[1][c];
+    q[c] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+  }
+  __syncthreads();  // all warps are done reading their activation slots
+  float* dst = sm.red + ((size_t)warp * RB + 4 * rq + ks) * C;
 #pragma unroll
-      for (int c = 0; c < C; ++c) red[(warp * RB + 4 * rq + i) * C + c] = acc[i][c];
-  __syncthreads();
-  if (warp >= 4 && ks == 0)
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int c = 0; c < C; ++c) red[((warp - 4) * RB + 4 * rq + i) * C + c] += acc[i][c];
+  for (int c = 0; c < C; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(q[c], q[c + 1], q[c + 2], q[c + 3]);
   __syncthreads();
 }
 
 __device__ __forceinline__ float red_sum(const Smem& sm, int r, int c, int C) {
-  const float* red = sm.red;
-  return (red[r * C + c] + red[(RB + r) * C + c]) + (red[(2 * RB + r) * C + c] + red[(3 * RB + r) * C + c]);
+  const float* red = sm.red + r * C + c;
+  const int ws = RB * C;
+  return ((red[0] + red[ws]) + (red[2 * ws] + red[3 * ws])) +
+         ((red[4 * ws] + red[5 * ws]) + (red[6 * ws] + red[7 * ws]));
 }
 
 // One GEMV pass over an activation source for every row block:
