@@ -101,7 +101,7 @@ struct Smem {
   int* misc;     // [2]=t, [3]=sym, [4]=par
   float* own;    // own-state (hh0 [B][C1], c [2][B][umax], gp [B][C2]) when own_smem
   unsigned long long* prof;  // [16] phase-time accumulators (CTA 0, thread 0)
-  uint64_t* full;  // two per warp (double-buffered activation slots)
+  uint64_t* full;  // one per warp
   uint64_t* wbar;
 };
 
@@ -118,7 +118,7 @@ __host__ __device__ inline size_t smem_bytes(int wfloats, int ns, int B, size_t 
   size_t b = (size_t)wfloats * 4 + ring_floats(ns) * 4;
   b += (size_t)B * 4 * 8 + 64 + ownf * 4 + 16 * 8;
   b = (b + 15) / 16 * 16;
-  b += 8 * (2 * NCW + 1);
+  b += 8 * (NCW + 1);
   return b;
 }
 
@@ -144,7 +144,7 @@ __device__ inline Smem carve_p(unsigned char* base, const PParams& P) {
   s.prof = reinterpret_cast<unsigned long long*>(base + off);
   off += 16 * 8;
   s.full = reinterpret_cast<uint64_t*>(base + off);
-  s.wbar = s.full + 2 * NCW;
+  s.wbar = s.full + NCW;
   return s;
 }
 
@@ -290,42 +290,31 @@ __device__ __forceinline__ void gemv_pass(const Smem& sm, const PParams& P, unsi
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rq = lane >> 2, ks = lane & 3;
   const int K = A.k0 + A.k1, kw = K / NCW, kbeg = warp * kw;
-  // two slots of ns*4 features per warp: chunk c+1 is in flight while chunk c
-  // is consumed (copies from one warp serialise, so one warp never has more
-  // than one in flight anyway)
-  const int slotk = P.ns * 4;
-  float* slots = sm.ring + (size_t)warp * 2 * slotk * RB;
-  uint64_t* bars = &sm.full[2 * warp];
+  const int slotk = P.ns * 8;
+  float* slot = sm.ring + (size_t)warp * slotk * RB;
+  uint64_t* bar = &sm.full[warp];
   const bool seg0 = kbeg < A.k0;
   const float* base = seg0 ? A.a0 : A.a1;
   const int kseg = seg0 ? A.k0 : A.k1;
   const int koff = seg0 ? kbeg : kbeg - A.k0;
   const int aoff = (4 * rq) ^ (ks << 3);
-  const int nc = (kw + slotk - 1) / slotk;
-  auto issue = [&](int rb, int c) {
-    if (lane == 0) {
-      const int kk = c * slotk, nk = kw - kk < slotk ? kw - kk : slotk;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect_tx(&bars[c & 1], (uint32_t)(nk * RB * 4));
-      bulk_g2s(slots + (size_t)(c & 1) * slotk * RB, base + ((size_t)rb * kseg + koff + kk) * RB,
-               (uint32_t)(nk * RB * 4), &bars[c & 1]);
-    }
-  };
   for (int rb = 0; rb < P.nrb; ++rb) {
     float acc[4][C];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int c = 0; c < C; ++c) acc[i][c] = 0.0f;
-    issue(rb, 0);
-    for (int c = 0; c < nc; ++c) {
-      if (c + 1 < nc) issue(rb, c + 1);
-      const int kk = c * slotk, nk = kw - kk < slotk ? kw - kk : slotk;
-      const float* slot = slots + (size_t)(c & 1) * slotk * RB;
+    for (int kk = 0; kk < kw; kk += slotk) {
+      const int nk = kw - kk < slotk ? kw - kk : slotk;
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(bar, (uint32_t)(nk * RB * 4));
+        bulk_g2s(slot, base + ((size_t)rb * kseg + koff + kk) * RB, (uint32_t)(nk * RB * 4), bar);
+      }
       unsigned long long tq0 = 0;
       if (P.prof && blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tq0));
-      mbar_wait(&bars[c & 1], (ph >> (c & 1)) & 1u);
-      ph ^= 1u << (c & 1);
+      mbar_wait(bar, ph);
+      ph ^= 1u;
       if (P.prof && blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long tq1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tq1));
@@ -375,7 +364,7 @@ __global__ void __launch_bounds__(NTH, 1) persistent_kernel(PParams P) {
 
   // ---- one-time setup: barriers, resident weights, control state ----
   if (tid == 0) {
-    for (int i = 0; i < 2 * NCW; ++i) mbar_init(&sm.full[i], 1);
+    for (int i = 0; i < NCW; ++i) mbar_init(&sm.full[i], 1);
     mbar_init(sm.wbar, 1);
     fence_mbar_init();
   }
