@@ -351,11 +351,21 @@ def main():
     from paper_2406_03791_b200._lib import Stats, check, lib
 
     algo, B, T, ms, durs, L, H, J, V, F, scaling = cfg
+    # RNNTG_BENCH_SHARE_GPU=1 maps ranks onto the visible GPUs modulo their
+    # count (functional check of the N>1 path on a 1-GPU box; gloo plumbing)
+    share = os.environ.get("RNNTG_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dist = None
+    coll_dev = "cuda"
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+            coll_dev = "cpu"
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     b0, b1 = shard(cfg, rank, world)
     Bl = b1 - b0
     dims = ModelDims(V, H, H, J, F, durs, "lstm", L)
@@ -396,7 +406,7 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = float(sum(step_ms))
     if dist:
-        t = torch.tensor([total_ms], device="cuda")
+        t = torch.tensor([total_ms], device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
         dist.barrier()
@@ -438,7 +448,7 @@ def main():
             e2e_once()
         el = time.perf_counter() - t0
         if dist:
-            t = torch.tensor([el], device="cuda", dtype=torch.float64)
+            t = torch.tensor([el], device=coll_dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
         e2e = {"value": frames_all * args.steps / el, "unit": "frames/s",
