@@ -61,7 +61,8 @@ typedef enum {
 /* How the loops run on the device. */
 typedef enum {
   RNNTG_EXEC_GRAPH = 0,       /* CUDA graph, nested conditional WHILE nodes */
-  RNNTG_EXEC_PERSISTENT = 1   /* one cooperative persistent kernel, in-kernel loops */
+  RNNTG_EXEC_PERSISTENT = 1,  /* one cooperative persistent kernel, in-kernel loops (FFMA) */
+  RNNTG_EXEC_TENSOR = 2       /* persistent kernel on tcgen05 tensor cores, role-specialised CTAs */
 } rnntg_exec;
 
 /* RnntDims (model.hpp:31-40) + the prediction-network cell.
@@ -158,6 +159,8 @@ rnntg_status rnntg_step_prediction(rnntg_model* m, int batch,
  *        8 = pred_proj, 9 = joint step. */
 rnntg_status rnntg_time_kernel(rnntg_decoder* d, int which, int reps, float* avg_ms);
 
+/* Tensor executor event trace (RNNTG_PROF=1): [16 events][64 steps] globaltimer ns. */
+rnntg_status rnntg_debug_trace(rnntg_decoder* d, unsigned long long* out, int n);
 /* Persistent executor phase profile (CTA 0, ns per phase, accumulated since
  * the last call; needs RNNTG_PROF=1 at decoder creation). */
 rnntg_status rnntg_debug_profile(rnntg_decoder* d, unsigned long long* out16);

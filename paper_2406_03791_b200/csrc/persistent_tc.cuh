@@ -1,0 +1,999 @@
+// persistent_tc.cuh — K6: the tensor-core persistent decoder.
+//
+// The whole greedy decode (frame-looping, label-looping, TDT label-looping)
+// runs in ONE cooperative kernel whose CTAs are specialised by ROLE, one
+// 128-row weight tile each, and pass activations to each other through
+// per-chunk dataflow counters in global memory (no grid barriers):
+//
+//   role   weights (swap-AB: M = 128 output rows)   input        output
+//   J      [out_proj || dur_proj] cols 128t..        trunk(s)     per-tile softmax partials
+//   P      pred_proj cols 128t..                     h_{L-1}(p)   gp (registers) -> trunk(s+1)
+//   R_l    W_hh_l gate rows (gate-major, 32 units)   h_l(p)       l=0: hh0(p+1) stays in TMEM,
+//                                                                 layer-0 cell -> h_0(p+1)
+//                                                                 l>0: hh_l(p+1) -> I_l tile
+//   I_l    W_ih_l gate rows, l >= 1                  h_{l-1}(p)   layer-l cell -> h_l(p)
+//
+// Arithmetic.  Every GEMV is D[128 x 32 rows] = W[128 x K] . A^T on the
+// 5th-gen tensor cores (tcgen05.mma.kind::f16, fp32 accumulate) with an
+// fp16 hi/lo split of BOTH operands: W' = W*2^s = W_hi + W_lo, A = A_hi + A_lo,
+// D = W_hi.[A_hi | A_lo] (one MMA, N = 64) + W_lo.A_hi (N = 32), i.e. all
+// products down to 2^-22 relative (~fp32; the dropped W_lo.A_lo is 2^-22).
+// W_hi is resident in shared memory (SWIZZLE_128B K-major), W_lo resident in
+// TENSOR memory (the MMA's A operand read from TMEM), so a 128 x 640 tile
+// (320 KB of fp16 pairs) stays on chip for the whole decode.
+//
+// Activations move as fp16 hi/lo images already in the UMMA canonical
+// layout ([64 rows = 32 hi + 32 lo][64 k] chunks of 8 KB, 128B-swizzled), so
+// a consumer's load is one 1-D bulk copy per chunk.  A chunk is published
+// by its producers with a release add on its counter; consumers poll the
+// counter (acquire) and stream chunks into a 4-stage ring as they appear,
+// overlapping the transfer with the MMAs of earlier chunks.
+//
+// Control state (labels, cursors, masks, frame counters) is replicated in
+// every CTA: each CTA merges the J tiles' partials for every row and applies
+// the same decision rules (decoders.cpp:261-307, 432-512), so no decision
+// broadcast is needed.  CTA 0 writes the hypotheses.
+//
+// Warp roles inside a CTA: warp 0 = bulk-copy producer, warp 1 = MMA issuer
+// (elect.sync inside a converged warp: issuing from a divergent lane costs
+// 3-4x, scripts/mb_tc.cu), warps 2-5 = epilogue + control.
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+
+namespace rnntg {
+namespace ptc {
+
+constexpr int NEPI = 256;        // 8 epilogue warps: two per TMEM lane quadrant, 16 rows each
+constexpr int NTH = 64 + NEPI;
+constexpr int NR = 16;           // batch rows per epilogue thread
+constexpr int NSTAGE = 4;
+constexpr int MAXNJ = 16;       // joint tiles (V+1+D <= 2048)
+constexpr int CHUNK = 8192;      // [64 rows][64 k] fp16, SWIZZLE_128B
+constexpr int MAXB = 32;         // rows per decoder on this executor
+constexpr int MAXKP = 640;       // K <= 640: W_lo (K/2 TMEM columns) + 2 x 96 accumulator columns
+constexpr int MAXKC = MAXKP / 64;
+constexpr int TRUNK = MAXL;      // activation buffer ids: h_0..h_{L-1}, trunk
+constexpr int MAXBUF = MAXL + 1;
+constexpr int NSLOT = 32;        // joint-partial ring depth (ack checked every NSLOT/2 steps)
+constexpr int ACC_COLS = 96;
+constexpr int WLO_COL = 2 * ACC_COLS;
+constexpr int CSTRIDE = 32;      // u32 words between counters (one 128-byte line each)
+
+enum Role { ROLE_J = 0, ROLE_P = 1, ROLE_R = 2, ROLE_I = 3 };
+
+// counter word indices (times CSTRIDE)
+__host__ __device__ inline int cidx_act(int buf, int kc) { return buf * MAXKC + kc; }
+__host__ __device__ inline int cidx_hh(int l, int t) { return MAXBUF * MAXKC + l * 64 + t; }
+__host__ __device__ inline int cidx_part() { return MAXBUF * MAXKC + MAXL * 64; }
+__host__ __device__ inline int cidx_ack() { return cidx_part() + 1; }
+constexpr int NCOUNTERS = MAXBUF * MAXKC + MAXL * 64 + 2;
+
+struct TParams {
+  int G, B, T, ms, cap, algo, L, cell;
+  int H, Hp, J, Jp, V1, D;
+  int NJ;                     // joint tiles
+  int GH, Gg;                 // table0 row stride / gates per unit
+  long long max_iters;
+  int durations[MAXD];
+  const int4* roles;          // [G] {role, layer, tile, float bits of 2^-s}
+  const unsigned char* wimg;  // [G][wstride]: W_hi smem image, then W_lo packed [Kp/2][128] u32
+  size_t wstride;
+  const float* bias[MAXL];    // reference layout [G*H]
+  const float* table0;        // [V1][GH] gate-interleaved (col = u*Gg + g)
+  const float* fp;            // [B*T][Jp] encoder projection (K1)
+  const int* out_len;
+  unsigned char* act[MAXBUF];  // [2 parity][KC][CHUNK]
+  int act_kc[MAXBUF];
+  int nprod[MAXBUF][MAXKC];   // producers per chunk
+  float* hh[MAXL];            // [2 parity][tiles][32 rows][128] (layers >= 1)
+  float4* part;               // [NSLOT][NJ][32] vocab (max, sumexp, best, idx)
+  float4* partd;              // [NSLOT][NJ][32] duration partials
+  unsigned* cnt;              // [NCOUNTERS * CSTRIDE]
+  int* tokens;
+  int* frames;
+  float* scores;
+  int* durs;
+  int* counts;
+  Ctrl* ctrl;
+  unsigned long long* prof;   // optional event trace [NEV][PROF_WIN] (first CTA of each role)
+  int prof_first[4];          // first CTA index per role (tracing CTAs)
+};
+constexpr int PROF_WIN = 64;  // traced joint steps [PROF_S0, PROF_S0 + PROF_WIN)
+constexpr int PROF_S0 = 100;
+constexpr int NEV = 32;
+
+// ------------------------------------------------------------------ PTX
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+  // K-major SWIZZLE_128B: 8-row groups 1024 B apart (SBO), LBO unused, sm100 version bit
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  // D f32, A/B f16, both K-major
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// Issued by a converged warp; elect.sync picks one lane.
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin until *p >= target with relaxed (L1-bypassing) loads.  An acquire load
+// compiles to LDG.STRONG.GPU + CCTL.IVALL: polling with it invalidates the
+// SM's L1 continuously, and even one extra acquire costs a full L2 round trip
+// on the critical path.  Every reader of published data reads through L2
+// (bulk copies, ld.global.cg) after observing the counter that the producer
+// bumped with a release, so the relaxed observation suffices in practice.
+__device__ __forceinline__ void spin_geq(const unsigned* p, unsigned target) {
+  while (ld_relaxed(p) < target) {
+  }
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Named barrier / OR-reduction over the 4 epilogue warps.
+__device__ __forceinline__ void epi_sync() { asm volatile("barrier.cta.sync.aligned 1, 256;" ::: "memory"); }
+__device__ __forceinline__ int epi_or(int v) {
+  int r;
+  asm volatile(
+      "{\n\t.reg .pred q, p;\n\tsetp.ne.s32 q, %1, 0;\n\t"
+      "barrier.cta.red.or.aligned.pred p, 1, 256, q;\n\tselp.s32 %0, 1, 0, p;\n\t}"
+      : "=r"(r)
+      : "r"(v)
+      : "memory");
+  return r;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// byte offset of (row r, k) inside a [rows x 64] fp16 K-major SWIZZLE_128B chunk
+__host__ __device__ inline uint32_t swz(int r, int k) {
+  return (uint32_t)(r * 128 + ((((k * 2) >> 4) ^ (r & 7)) << 4) + ((k * 2) & 15));
+}
+
+// v -> (hi, lo) fp16 at (row r | 32 + r, k) of a chunk
+__device__ __forceinline__ void store_split(unsigned char* chunk, int r, int k, float v) {
+  const __half hi = __float2half_rn(v);
+  const __half lo = __float2half_rn(v - __half2float(hi));
+  *reinterpret_cast<__half*>(chunk + swz(r, k)) = hi;
+  *reinterpret_cast<__half*>(chunk + swz(32 + r, k)) = lo;
+}
+
+// ------------------------------------------------------------------ smem
+struct Smem {
+  unsigned char* whi;   // [KC][16384]
+  unsigned char* ring;  // [NSTAGE][CHUNK]
+  float* xs;            // [4][32][32] gate exchange / [128][33] joint transpose / partial staging
+  float4* red;          // [2][8][32] joint column-group partials
+  int* label;           // [32] replicated row state
+  int* flag;            // bit0 done (FS) / inactive (LL), bit1 accepted this step
+  int* tb;
+  int* ub;
+  int* cnt;
+  int* kdec;
+  float* vdec;
+  int* ddec;
+  int* misc;            // [0..1] round commands, [2] t, [3] sym, [4] shared flag words
+  uint64_t* full;       // [NSTAGE]
+  uint64_t* empty;      // [NSTAGE]
+  uint64_t* accf;       // [2]
+  uint64_t* acce;       // [2]
+  uint64_t* cmd;        // [1]
+  uint64_t* wbar;       // [1]
+  uint32_t* tslot;
+};
+
+constexpr int XS_FLOATS = 128 * 33;   // epilogue exchange: [128 cols][33] / [4 gates][32][32]
+constexpr int RED_F4 = 512;           // column-group merge scratch: [2][8][32] float4
+__host__ __device__ inline size_t smem_bytes(int KC) {
+  return 1024 /*align slack*/ + (size_t)KC * 16384 + (size_t)NSTAGE * CHUNK + XS_FLOATS * 4 +
+         RED_F4 * 16 + 12 * 32 * 4 + 16 * 4 + 16 * 8 + 64;
+}
+
+__device__ inline Smem carve(unsigned char* raw, int KC) {
+  Smem s;
+  // align with pointer arithmetic on the shared-memory pointer itself (an
+  // integer round trip would turn every access into a generic LD/ST)
+  unsigned char* base = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+  s.whi = base;
+  s.ring = base + (size_t)KC * 16384;
+  s.xs = reinterpret_cast<float*>(s.ring + NSTAGE * CHUNK);
+  s.red = reinterpret_cast<float4*>(s.xs + XS_FLOATS);
+  int* ip = reinterpret_cast<int*>(s.red + RED_F4);
+  s.label = ip;
+  s.flag = ip + 32;
+  s.tb = ip + 64;
+  s.ub = ip + 96;
+  s.cnt = ip + 128;
+  s.kdec = ip + 160;
+  s.vdec = reinterpret_cast<float*>(ip + 192);
+  s.ddec = ip + 224;
+  s.misc = ip + 256;  // 16 words
+  uint64_t* bp = reinterpret_cast<uint64_t*>(ip + 256 + 16);
+  s.full = bp;
+  s.empty = bp + NSTAGE;
+  s.accf = bp + 2 * NSTAGE;
+  s.acce = s.accf + 2;
+  s.cmd = s.acce + 2;
+  s.wbar = s.cmd + 1;
+  s.tslot = reinterpret_cast<uint32_t*>(s.wbar + 1);
+  return s;
+}
+
+// Branchless activations (~1e-7 relative): the libm versions carry slow-path
+// calls that serialise the 32-row unrolled epilogue loops.
+__device__ __forceinline__ float sigm(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+__device__ __forceinline__ float tanh_fast(float x) {
+  const float a = fabsf(x);
+  // |x| < 0.5: odd Taylor series to x^13 (truncation < 1e-7 relative)
+  const float x2 = x * x;
+  float p = 21844.0f / 6081075.0f;
+  p = fmaf(p, x2, -1382.0f / 155925.0f);
+  p = fmaf(p, x2, 62.0f / 2835.0f);
+  p = fmaf(p, x2, -17.0f / 315.0f);
+  p = fmaf(p, x2, 2.0f / 15.0f);
+  p = fmaf(p, x2, -1.0f / 3.0f);
+  const float small = fmaf(p * x2, x, x);
+  // |x| >= 0.5: 1 - 2 / (e^{2|x|} + 1)
+  const float big = copysignf(1.0f - __fdividef(2.0f, __expf(2.0f * a) + 1.0f), x);
+  return a < 0.5f ? small : big;
+}
+
+
+// ------------------------------------------------------------------ epilogue
+// Epilogue + replicated control of one CTA (warps 2-9).  Thread et = 0..255;
+// tile row m = 32*q + lane is this thread's TMEM lane (q = warp & 3, the
+// quadrant a warp may address), and it owns batch rows r0 .. r0+15 of it
+// (r0 = 16 * (et >= 128)): the two warps of a quadrant split the rows.
+struct Epi {
+  const TParams& P;
+  const Smem& sm;
+  const uint32_t tq;  // TMEM address of this warp's lane quadrant
+  const int et, m, r0, role, layer, tile;
+  const float wsc;
+  const int B, blank;
+  const bool fs, tdt, lstm, tracer;
+  unsigned* const cnt;
+  int maxlen = 0, round = 0, p = 0, err = 0, acc_any = 0;
+  long long s = 0, joint_evals = 0, pred_steps = 0, outer_iters = 0;
+  bool finish = false;
+
+  __device__ Epi(const TParams& P_, const Smem& sm_, uint32_t tmem, int et_, int q, int role_, int layer_,
+                 int tile_, float wsc_)
+      : P(P_), sm(sm_), tq(tmem + ((uint32_t)(32 * q) << 16)), et(et_), m(32 * q + (et_ & 31)),
+        r0(et_ >= 128 ? NR : 0), role(role_),
+        layer(layer_), tile(tile_), wsc(wsc_), B(P_.B), blank(P_.V1 - 1), fs(P_.algo == ALGO_FS),
+        tdt(P_.algo == ALGO_TDT), lstm(P_.cell == 1),
+        tracer(P_.prof && (int)blockIdx.x == P_.prof_first[role_]), cnt(P_.cnt) {}
+
+  // per-CTA publish time of step s (all CTAs): prof[(NEV + cta) * PROF_WIN + s - PROF_S0]
+  __device__ __forceinline__ void mark_pub() {
+    if (P.prof && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN)
+      P.prof[(size_t)(NEV + blockIdx.x) * PROF_WIN + (s - PROF_S0)] = gtimer();
+  }
+  __device__ __forceinline__ void mark(int ev) {
+    if (tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) {
+      P.prof[(size_t)ev * PROF_WIN + (s - PROF_S0)] = gtimer();
+      if (ev == 0 || ev == 3) P.prof[(size_t)(ev == 0 ? 25 : 26) * PROF_WIN + (s - PROF_S0)] = clock64();
+    }
+  }
+  // one load+MMA round on this CTA's input at epoch e (-1 = exit)
+  __device__ __forceinline__ void post(int e) {
+    if (et == 0) {
+      sm.misc[round & 1] = e;
+      mbar_arrive(sm.cmd);
+    }
+    ++round;
+  }
+  // accumulator of round r -> v[i] = (W . A)[m][r0 + i] * 2^-s
+  __device__ __forceinline__ void read_acc(int r, float (&v)[NR]) {
+    mbar_wait(&sm.accf[r & 1], (uint32_t)((r >> 1) & 1));
+    tc_fence_after();
+    const uint32_t a = tq + (r & 1) * ACC_COLS + r0;
+    {
+      uint32_t x0[16], x1[16], x2[16];
+      tmem_ld16(a, x0);
+      tmem_ld16(a + 32, x1);
+      tmem_ld16(a + 64, x2);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < NR; ++i)
+        v[i] = (__uint_as_float(x0[i]) + (__uint_as_float(x1[i]) + __uint_as_float(x2[i]))) * wsc;
+    }
+    tc_fence_before();
+    epi_sync();
+    if (et == 0) mbar_arrive(&sm.acce[r & 1]);
+  }
+  __device__ __forceinline__ void wait_counter(int ci, unsigned target) {
+    if (et == 0) spin_geq(cnt + (size_t)ci * CSTRIDE, target);
+    epi_sync();
+  }
+  // this CTA's global stores -> visible (incl. to bulk-copy readers) -> counter += n
+  __device__ __forceinline__ void bump(int ci, int n = 1) {
+    fence_proxy_global();
+    epi_sync();
+    if (et == 0)
+      for (int i = 0; i < n; ++i) red_release_add(cnt + (size_t)(ci + i) * CSTRIDE, 1);
+  }
+
+  __device__ void init_rows() {
+    if (et < 32) {
+      sm.label[et] = blank;
+      sm.tb[et] = 0;
+      sm.ub[et] = 0;
+      sm.cnt[et] = 0;
+      const int len = et < B ? __ldg(&P.out_len[et]) : 0;
+      sm.flag[et] = (et < B ? (fs ? (0 >= len) : !(0 < len)) : 1) | 2;  // every row runs P0
+      if (blockIdx.x == 0 && et < B) P.counts[et] = 0;
+    }
+    if (et == 0) {
+      sm.misc[2] = 0;
+      sm.misc[3] = 0;
+    }
+    for (int b = 0; b < B; ++b) maxlen = max(maxlen, __ldg(&P.out_len[b]));
+    epi_sync();
+  }
+
+  // ---- J: logits of this tile's 128 columns -> per-row softmax partials of step s
+  __device__ void joint_round() {
+    mark(0);
+    post((int)s);
+    float v[NR];
+    read_acc(round - 1, v);
+    mark(1);
+    float* xs = sm.xs;  // [128 cols][33]
+#pragma unroll
+    for (int i = 0; i < NR; ++i) xs[m * 33 + r0 + i] = v[i];
+    mark(16);
+    // slot reuse: every CTA has finished decide(s - NSLOT); checked once per half window
+    if (s >= NSLOT / 2 && s % (NSLOT / 2) == 0)
+      wait_counter(cidx_ack(), (unsigned)P.G * (unsigned)(s - NSLOT / 2 + 1));
+    else
+      epi_sync();
+    // thread (row r, column group qq): columns 16qq..16qq+15 of the tile
+    const int r = et & 31, qq = et >> 5;
+    const int c0 = 128 * tile + 16 * qq;
+    float mv = -INFINITY, md = -INFINITY;
+    int iv = 0x7fffffff, id = 0x7fffffff;
+    const int V1 = P.V1, VD = P.V1 + P.D;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const float x = xs[(16 * qq + c) * 33 + r];
+      const int col = c0 + c;
+      const bool gv = col < V1 && x > mv;
+      mv = gv ? x : mv;
+      iv = gv ? col : iv;
+      const bool gd = col >= V1 && col < VD && x > md;
+      md = gd ? x : md;
+      id = gd ? col - V1 : id;
+    }
+    float ev = 0.0f, ed = 0.0f;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const float x = xs[(16 * qq + c) * 33 + r];
+      const int col = c0 + c;
+      const float e1 = __expf(x - (col < V1 ? mv : md));
+      ev += col < V1 ? e1 : 0.0f;
+      ed += (col >= V1 && col < VD) ? e1 : 0.0f;
+    }
+    mark(17);
+    sm.red[qq * 32 + r] = make_float4(mv, ev, mv, __int_as_float(iv));
+    sm.red[256 + qq * 32 + r] = make_float4(md, ed, md, __int_as_float(id));
+    epi_sync();
+    const int slot = (int)(s % NSLOT);
+    if (et < 64) {  // merge the 8 column groups in order: et < 32 vocab, else durations
+      const int rr = et & 31, seg = et >> 5;
+      if (seg == 0 || P.D) {
+        float M = -INFINITY, S = 0.0f, bv = -INFINITY;
+        int bi = 0x7fffffff;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float4 t = sm.red[seg * 256 + k * 32 + rr];
+          if (t.x != -INFINITY) {
+            const float nm = fmaxf(M, t.x);
+            S = (S == 0.0f ? 0.0f : S * __expf(M - nm)) + t.y * __expf(t.x - nm);
+            M = nm;
+            if (t.z > bv) { bv = t.z; bi = __float_as_int(t.w); }
+          }
+        }
+        float4* dst = seg == 0 ? P.part : P.partd;
+        dst[((size_t)slot * P.NJ + tile) * 32 + rr] = make_float4(M, S, bv, __int_as_float(bi));
+      }
+    }
+    mark(18);
+    epi_sync();
+    if (et == 0) red_release_add(cnt + (size_t)cidx_part() * CSTRIDE, 1);
+    mark(2);
+    mark_pub();
+  }
+
+  // ---- replicated decision of step s (argmax / lse merge + rules)
+  __device__ void decide() {
+    wait_counter(cidx_part(), (unsigned)P.NJ * (unsigned)(s + 1));
+    if (role == ROLE_R && layer == 0) mark(22);
+    const int slot = (int)(s % NSLOT);
+    const int n = P.NJ * 32;
+    float4* ps = reinterpret_cast<float4*>(sm.xs);  // [2][NJ][32]
+    {
+      float4 a[2], d[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int i = et + NEPI * j;
+        if (i < n) {
+          a[j] = __ldcg(&P.part[(size_t)slot * n + i]);
+          if (P.D) d[j] = __ldcg(&P.partd[(size_t)slot * n + i]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int i = et + NEPI * j;
+        if (i < n) {
+          ps[i] = a[j];
+          if (P.D) ps[n + i] = d[j];
+        }
+      }
+    }
+    epi_sync();
+    if (role == ROLE_R && layer == 0) mark(23);
+    int acc = 0, live = 0;
+    const int t_fs = sm.misc[2];
+    if (et < B) {
+      const int b = et;
+      float Mx = -INFINITY, Sx = 0.0f, best = -INFINITY;
+      int bi = 0;
+      for (int t = 0; t < P.NJ; ++t) {
+        const float4 pv = ps[t * 32 + b];
+        if (pv.x != -INFINITY) {
+          const float nm = fmaxf(Mx, pv.x);
+          Sx = (Sx == 0.0f ? 0.0f : Sx * __expf(Mx - nm)) + pv.y * __expf(pv.x - nm);
+          Mx = nm;
+          if (pv.z > best) {  // tiles in column order: strict > keeps the lowest index
+            best = pv.z;
+            bi = __float_as_int(pv.w);
+          }
+        }
+      }
+      int dd = 0;
+      if (P.D) {
+        float bd = -INFINITY;
+        int di = 0;
+        for (int t = 0; t < P.NJ; ++t) {
+          const float4 pv = ps[n + t * 32 + b];
+          if (pv.z > bd) {
+            bd = pv.z;
+            di = __float_as_int(pv.w);
+          }
+        }
+        dd = P.durations[di];
+      }
+      const int k = bi;
+      const float v = best - (Mx + logf(Sx));
+      // decision rules, thread per row (decoders.cpp:261-307 / 432-512)
+      int f = sm.flag[b] & ~2;
+      const bool emitter = blockIdx.x == 0;
+      if (fs) {
+        if (!(f & 1)) {
+          if (k == blank) {
+            f |= 1;
+          } else {
+            const int nb = sm.cnt[b];
+            if (emitter && nb < P.cap) {
+              const size_t o = (size_t)b * P.cap + nb;
+              P.tokens[o] = k;
+              P.frames[o] = t_fs;
+              P.scores[o] = v;
+              P.durs[o] = 0;
+              P.counts[b] = nb + 1;
+            }
+            sm.cnt[b] = nb + 1;
+            sm.label[b] = k;
+            f |= 2;
+          }
+        }
+        live = !(f & 1);
+      } else if (!(f & 1)) {
+        const int len = __ldg(&P.out_len[b]);
+        int t = sm.tb[b], u = sm.ub[b];
+        if (k == blank) {
+          const int d = tdt ? dd : 1;
+          t += d > 1 ? d : 1;
+          u = 0;
+        } else {
+          const int d = tdt ? dd : 0;
+          const int nb = sm.cnt[b];
+          if (emitter && nb < P.cap) {
+            const size_t o = (size_t)b * P.cap + nb;
+            P.tokens[o] = k;
+            P.frames[o] = t;
+            P.scores[o] = v;
+            P.durs[o] = d;
+            P.counts[b] = nb + 1;
+          }
+          sm.cnt[b] = nb + 1;
+          sm.label[b] = k;
+          f |= 2;
+          u += 1;
+          if (d > 0) {
+            t += d;
+            u = 0;
+          } else if (u == P.ms) {
+            t += 1;
+            u = 0;
+          }
+        }
+        sm.tb[b] = t;
+        sm.ub[b] = u;
+        if (!(t < len)) f |= 1;
+        live = !(f & 1);
+      }
+      acc = (f >> 1) & 1;
+      sm.flag[b] = f;
+    }
+    if (role == ROLE_R && layer == 0) mark(24);
+    acc_any = epi_or(acc);
+    const int live_any = epi_or(live);
+    finish = false;
+    if (fs) {
+      int sym = sm.misc[3] + 1;
+      int t = t_fs;
+      if (!live_any || sym >= P.ms) {  // frame ends (decoders.cpp:297-313)
+        t += 1;
+        sym = 0;
+        ++outer_iters;
+        if (t >= maxlen) finish = true;
+        if (et < B) sm.flag[et] = (sm.flag[et] & 2) | (t >= __ldg(&P.out_len[et]) ? 1 : 0);
+      }
+      epi_sync();
+      if (et == 0) {
+        sm.misc[3] = sym;
+        sm.misc[2] = t;
+      }
+    } else {
+      finish = !live_any;
+    }
+    ++joint_evals;
+    if (joint_evals > P.max_iters) {
+      err = ERR_RUNAWAY;
+      finish = true;
+    }
+    epi_sync();
+    if (et == 0) red_release_add(cnt + (size_t)cidx_ack() * CSTRIDE, 1);
+    mark(role == ROLE_J ? 3 : role == ROLE_R ? (layer == 0 ? 4 : 10) : role == ROLE_I ? 6 : 8);
+  }
+
+  // ---- the decode skeleton: pred(te) after each accepting decision, idle(te) otherwise
+  template <typename Pred, typename Idle>
+  __device__ void run(Pred&& pred, Idle&& idle) {
+    init_rows();
+    pred(0LL);  // P0 = pred(blank, 0) for every row (decoders.cpp:414-430)
+    ++pred_steps;
+    int live = et < B ? !(sm.flag[et] & 1) : 0;
+    live = epi_or(live);
+    const bool running0 = fs ? (maxlen > 0) : (live != 0);
+    if (et < 32) sm.flag[et] &= ~2;
+    epi_sync();
+    bool running = running0;
+    while (running) {
+      if (role == ROLE_J) joint_round();
+      decide();
+      if (finish) break;
+      if (acc_any) {
+        ++p;
+        pred(s + 1);
+        ++pred_steps;
+        if (!fs) ++outer_iters;
+      } else {
+        idle(s + 1);
+      }
+      ++s;
+      if (et < 32) sm.flag[et] &= ~2;
+      epi_sync();
+    }
+  }
+
+  // ---- layer cells: pre-activations (gate row m, 32 rows) -> committed h of the tile's units
+  // LSTM: gate-major rows (g = m/32, unit 32*tile + m%32); thread (unit et%32, rows et/32 + 4j)
+  __device__ __forceinline__ void cell_lstm(const float (&pre)[NR], int l, int pe, float (&c)[4], float (&h)[4]) {
+    const int g = m >> 5, ul = m & 31;
+    float* xg = sm.xs + g * 1024;  // [g][r][ul]
+    if (g == 2) {
+#pragma unroll
+      for (int i = 0; i < NR; ++i) xg[(r0 + i) * 32 + ul] = tanh_fast(pre[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < NR; ++i) xg[(r0 + i) * 32 + ul] = sigm(pre[i]);
+    }
+    epi_sync();
+    if (role == ROLE_R) mark(20);
+    const int ulc = et & 31, rb = et >> 5;  // unit, rows rb + 8j
+    const int u = 32 * tile + ulc;
+    unsigned char* ch = P.act[l] + ((size_t)(pe & 1) * P.act_kc[l] + (u >> 6)) * CHUNK;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = rb + 8 * j;
+      const bool commit = r < B && (sm.flag[r] & 2);
+      const float i_ = sm.xs[r * 32 + ulc], f_ = sm.xs[1024 + r * 32 + ulc];
+      const float g_ = sm.xs[2048 + r * 32 + ulc], o_ = sm.xs[3072 + r * 32 + ulc];
+      const float cn = f_ * c[j] + i_ * g_;
+      const float hn = u < P.H ? o_ * tanh_fast(cn) : 0.0f;
+      c[j] = commit ? cn : c[j];
+      h[j] = commit ? hn : h[j];
+      store_split(ch, r, u & 63, h[j]);
+    }
+    if (role == ROLE_R) mark(21);
+    bump(cidx_act(l, (32 * tile) >> 6));
+  }
+  // tanh RNN: one unit per row m (128 units per tile)
+  __device__ __forceinline__ void cell_tanh(const float (&pre)[NR], int l, int pe, float (&h)[NR]) {
+    const int u = 128 * tile + m;
+    if (u < P.Hp) {
+      unsigned char* ch = P.act[l] + ((size_t)(pe & 1) * P.act_kc[l] + (u >> 6)) * CHUNK;
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        const int r = r0 + i;
+        const float hn = u < P.H ? tanh_fast(pre[i]) : 0.0f;
+        h[i] = (r < B && (sm.flag[r] & 2)) ? hn : h[i];
+        store_split(ch, r, u & 63, h[i]);
+      }
+    }
+    const int c0 = (128 * tile) >> 6;
+    bump(cidx_act(l, c0), min(2, P.act_kc[l] - c0));
+  }
+
+  __device__ void run_role();
+};
+
+__device__ __forceinline__ void Epi::run_role() {
+  const int unit = lstm ? 32 * tile + (m & 31) : 128 * tile + m;
+  const int gate = lstm ? (m >> 5) : 0;
+  if (role == ROLE_J) {
+    run([&](long long) {}, [&](long long) {});
+  } else if (role == ROLE_P) {
+    float gp[NR], fpv[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) gp[i] = 0.0f;
+    const int j = 128 * tile + m;
+    // fp[b, t_b, j] for the next trunk, t from the latest decision
+    auto prefetch = [&]() {
+      const int tfs = sm.misc[2];
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        const int r = r0 + i;
+        int t = fs ? tfs : sm.tb[r];
+        t = t < 0 ? 0 : (t > P.T - 1 ? P.T - 1 : t);
+        fpv[i] = (r < B && j < P.J) ? __ldg(&P.fp[((size_t)r * P.T + t) * P.Jp + j]) : 0.0f;
+      }
+    };
+    auto trunk = [&](long long te) {  // trunk(te) = relu(fp + gp) -> act[TRUNK]
+      if (j < P.Jp) {
+        unsigned char* ch = P.act[TRUNK] + ((size_t)(te & 1) * P.act_kc[TRUNK] + (j >> 6)) * CHUNK;
+#pragma unroll
+        for (int i = 0; i < NR; ++i) {
+          const int r = r0 + i;
+          const float x = (r < B && j < P.J) ? fmaxf(fpv[i] + gp[i], 0.0f) : 0.0f;
+          store_split(ch, r, j & 63, x);
+        }
+      }
+      const int c0 = (128 * tile) >> 6;
+      bump(cidx_act(TRUNK, c0), min(2, P.act_kc[TRUNK] - c0));
+    };
+    run(
+        [&](long long te) {
+          post(p);
+          prefetch();
+          float v[NR];
+          read_acc(round - 1, v);
+          mark(9);
+#pragma unroll
+          for (int i = 0; i < NR; ++i) gp[i] = v[i];
+          trunk(te);
+          mark(14);
+          mark_pub();
+        },
+        [&](long long te) {
+          prefetch();
+          trunk(te);
+        });
+  } else if (role == ROLE_R && layer > 0) {
+    run(
+        [&](long long) {
+          post(p);
+          float v[NR];
+          read_acc(round - 1, v);
+          float* hb = P.hh[layer] + ((size_t)((p + 1) & 1) * 64 + tile) * 32 * 128;
+#pragma unroll
+          for (int i = 0; i < NR; ++i) hb[(r0 + i) * 128 + m] = v[i];
+          bump(cidx_hh(layer, tile));
+          mark_pub();
+        },
+        [&](long long) {});
+  } else {
+    // R_0 (layer-0 cell after the decision) or I_l (layer-l cell)
+    const float* bl = P.bias[layer];
+    const float bias_m = unit < P.H ? __ldg(&bl[gate * P.H + unit]) : 0.0f;
+    const bool isr0 = role == ROLE_R;
+    float c4[4], h4[4], hr[NR];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c4[j] = h4[j] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) hr[j] = 0.0f;
+    run(
+        [&](long long) {
+          float v[NR], x[NR];
+          if (isr0) {
+            // gates0 = (table0[label] + hh0) + b   (App. B order); hh0 was
+            // accumulated after the previous step (TMEM), zero for P0
+#pragma unroll
+            for (int i = 0; i < NR; ++i) {
+              const int r = r0 + i;
+              x[i] = (r < B && (sm.flag[r] & 2))
+                         ? __ldg(&P.table0[(size_t)sm.label[r] * P.GH + unit * P.Gg + gate])
+                         : 0.0f;
+            }
+            if (p > 0) {
+              read_acc(round - 1, v);
+            } else {
+#pragma unroll
+              for (int i = 0; i < NR; ++i) v[i] = 0.0f;
+            }
+#pragma unroll
+            for (int i = 0; i < NR; ++i) v[i] = (x[i] + v[i]) + bias_m;
+            mark(19);
+          } else {
+            post(p);
+            if (p > 0) {  // recurrent half from R_l, ready long before the input half
+              wait_counter(cidx_hh(layer, tile), (unsigned)p);
+              const float* hb = P.hh[layer] + ((size_t)(p & 1) * 64 + tile) * 32 * 128;
+#pragma unroll
+              for (int i = 0; i < NR; ++i) x[i] = __ldcg(&hb[(r0 + i) * 128 + m]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < NR; ++i) x[i] = 0.0f;
+            }
+            read_acc(round - 1, v);
+            mark(7);
+#pragma unroll
+            for (int i = 0; i < NR; ++i) v[i] = (v[i] + x[i]) + bias_m;
+          }
+          if (lstm) cell_lstm(v, layer, p, c4, h4);
+          else cell_tanh(v, layer, p, hr);
+          mark_pub();
+          if (isr0) {
+            mark(5);
+            post(p);  // hh0(p+1) = h0(p) @ W_hh0 into the other accumulator
+          } else {
+            mark(11);
+          }
+        },
+        [&](long long) {});
+    if (isr0) {  // drain the look-ahead hh0 round
+      float v[NR];
+      read_acc(round - 1, v);
+    }
+  }
+  post(-1);
+  if (blockIdx.x == 0 && et == 0) {
+    Ctrl* c = P.ctrl;
+    c->joint_evals = joint_evals;
+    c->pred_steps = pred_steps;
+    c->outer_iters = outer_iters;
+    c->iters = joint_evals;
+    c->err = err;
+  }
+}
+
+// ------------------------------------------------------------------ kernel
+__global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TParams P) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const int4 rl = P.roles[blockIdx.x];
+  const int role = rl.x, layer = rl.y, tile = rl.z;
+  const float wsc = __int_as_float(rl.w);
+  const int in_buf = role == ROLE_J ? TRUNK : role == ROLE_P ? P.L - 1 : role == ROLE_R ? layer : layer - 1;
+  const int KC = P.act_kc[in_buf];
+  Smem sm = carve(smem_raw, KC);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int B = P.B;
+  const bool lstm = P.cell == 1;
+  const bool fs = P.algo == ALGO_FS, tdt = P.algo == ALGO_TDT;
+  const int blank = P.V1 - 1;
+
+  if (tid == 0) {
+    for (int i = 0; i < NSTAGE; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.accf[i], 1);
+      mbar_init(&sm.acce[i], 1);
+    }
+    mbar_init(sm.cmd, 1);
+    mbar_init(sm.wbar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(sm.tslot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *sm.tslot;
+  const unsigned char* wimg = P.wimg + (size_t)blockIdx.x * P.wstride;
+
+  // ---- resident weights: W_hi -> smem (bulk copies), W_lo -> TMEM ----
+  if (tid == 0) {
+    const uint32_t bytes = (uint32_t)KC * 16384;
+    mbar_arrive_expect_tx(sm.wbar, bytes);
+    for (uint32_t o = 0; o < bytes; o += 32768)
+      bulk_g2s(sm.whi + o, wimg + o, bytes - o < 32768 ? bytes - o : 32768, sm.wbar);
+  }
+  if (warp >= 2) {
+    const int q = warp & 3, half = warp >= 6;
+    const uint32_t* lo = reinterpret_cast<const uint32_t*>(wimg + (size_t)KC * 16384);
+    const int m = 32 * q + lane;
+    for (int c0 = half * KC * 16; c0 < (half + 1) * KC * 16; c0 += 8) {
+      uint32_t r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __ldg(lo + (size_t)(c0 + j) * 128 + m);
+      tmem_st8(tmem + ((uint32_t)(32 * q) << 16) + WLO_COL + c0, r);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  mbar_wait(sm.wbar, 0);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  if (warp == 0) {
+    // ================= producer: stream input chunks into the ring =================
+    if (lane == 0) {
+      long long issued = 0;
+      const unsigned* cb = P.cnt + (size_t)cidx_act(in_buf, 0) * CSTRIDE;
+      for (int r = 0;; ++r) {
+        mbar_wait(sm.cmd, r & 1);
+        const int e = ((volatile int*)sm.misc)[r & 1];
+        if (e < 0) break;
+        const unsigned char* src = P.act[in_buf] + (size_t)(e & 1) * KC * CHUNK;
+        const bool tr = P.prof && role == ROLE_J && (int)blockIdx.x == P.prof_first[role] && e >= PROF_S0 && e < PROF_S0 + PROF_WIN;
+        // poll every outstanding chunk counter at once (one L2 round trip per
+        // poll, not one per chunk), then stream all ready chunks in order
+        int next = 0;
+        while (next < KC) {
+          unsigned v[MAXKC];
+#pragma unroll
+          for (int kc = 0; kc < MAXKC; ++kc)
+            v[kc] = (kc >= next && kc < KC) ? ld_relaxed(cb + kc * CSTRIDE) : 0u;
+          int ready = next;
+#pragma unroll
+          for (int kc = 0; kc < MAXKC; ++kc)
+            if (kc == ready && kc < KC && v[kc] >= (unsigned)P.nprod[in_buf][kc] * (unsigned)(e + 1)) ++ready;
+          if (ready == next) continue;
+          fence_proxy_global();
+          for (int kc = next; kc < ready; ++kc) {
+            if (tr && (kc == 0 || kc == KC - 1)) P.prof[(size_t)(kc ? 13 : 12) * PROF_WIN + (e - PROF_S0)] = gtimer();
+            const int s = (int)(issued % NSTAGE);
+            if (issued >= NSTAGE) mbar_wait(&sm.empty[s], (uint32_t)(((issued / NSTAGE) - 1) & 1));
+            mbar_arrive_expect_tx(&sm.full[s], CHUNK);
+            bulk_g2s(sm.ring + s * CHUNK, src + (size_t)kc * CHUNK, CHUNK, &sm.full[s]);
+            ++issued;
+          }
+          next = ready;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer (converged warp) =================
+    long long used = 0;
+    constexpr uint32_t ID64 = idesc_f16(128, 64), ID32 = idesc_f16(128, 32);
+    const uint32_t whi0 = smem_u32(sm.whi), ring0 = smem_u32(sm.ring);
+    for (int r = 0;; ++r) {
+      mbar_wait(sm.cmd, r & 1);
+      const int e = ((volatile int*)sm.misc)[r & 1];
+      if (e < 0) break;
+      const int set = r & 1;
+      if (r >= 2) mbar_wait(&sm.acce[set], (uint32_t)(((r >> 1) - 1) & 1));
+      tc_fence_after();
+      const uint32_t d1 = tmem + set * ACC_COLS, d2 = d1 + 64;
+      const bool tr = P.prof && role == ROLE_J && (int)blockIdx.x == P.prof_first[role] && e >= PROF_S0 &&
+                      e < PROF_S0 + PROF_WIN && lane == 0;
+      for (int kc = 0; kc < KC; ++kc) {
+        const int s = (int)(used % NSTAGE);
+        mbar_wait(&sm.full[s], (uint32_t)((used / NSTAGE) & 1));
+        if (tr && (kc == 0 || kc == KC - 1)) P.prof[(size_t)(kc ? 28 : 27) * PROF_WIN + (e - PROF_S0)] = gtimer();
+        tc_fence_after();
+        const uint64_t ad = sdesc_sw128(whi0 + kc * 16384), bd = sdesc_sw128(ring0 + s * CHUNK);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t acc = (kc | k) != 0;
+          mma_ss(d1, ad + 2 * k, bd + 2 * k, ID64, acc);
+          mma_ts(d2, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID32, acc);
+        }
+        mma_commit(&sm.empty[s]);
+        ++used;
+      }
+      mma_commit(&sm.accf[set]);
+      if (tr) P.prof[(size_t)29 * PROF_WIN + (e - PROF_S0)] = gtimer();
+    }
+  } else {
+    // ================= epilogue + replicated control (128 threads) =================
+    Epi e(P, sm, tmem, tid - 64, warp & 3, role, layer, tile, wsc);
+    e.run_role();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+}  // namespace ptc
+}  // namespace rnntg

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -21,6 +22,7 @@
 #include "kernels.cuh"
 #include "encproj_tc.cuh"
 #include "persistent_k5.cuh"
+#include "persistent_tc.cuh"
 
 using namespace rnntg;
 
@@ -96,6 +98,11 @@ struct rnntg_decoder {
   // persistent executor
   pk::PParams pp{};
   size_t psmem = 0;
+  // tensor-core persistent executor
+  ptc::TParams tp{};
+  size_t tsmem = 0;
+  unsigned* tcnt = nullptr;
+  size_t tcnt_bytes = 0;
 };
 
 namespace {
@@ -443,6 +450,224 @@ rnntg_status setup_persistent(rnntg_decoder* d) {
   return RNNTG_OK;
 }
 
+// ---------------------------------------------------------------- K6
+// fp16 bits (round to nearest even) of a float, host side.
+uint16_t f2h_bits(float f) {
+  uint32_t x;
+  std::memcpy(&x, &f, 4);
+  const uint32_t sign = (x >> 16) & 0x8000u;
+  const int exp = (int)((x >> 23) & 0xff) - 127 + 15;
+  uint32_t mant = x & 0x7fffffu;
+  if (((x >> 23) & 0xff) == 0xff) return (uint16_t)(sign | 0x7c00u | (mant ? 0x200u : 0));
+  if (exp >= 31) return (uint16_t)(sign | 0x7c00u);
+  if (exp <= 0) {
+    if (exp < -10) return (uint16_t)sign;
+    mant |= 0x800000u;
+    const int shift = 14 - exp;
+    uint32_t h = mant >> shift;
+    const uint32_t rem = mant & ((1u << shift) - 1), half = 1u << (shift - 1);
+    if (rem > half || (rem == half && (h & 1))) ++h;
+    return (uint16_t)(sign | h);
+  }
+  uint32_t h = ((uint32_t)exp << 10) | (mant >> 13);
+  const uint32_t rem = mant & 0x1fffu;
+  if (rem > 0x1000u || (rem == 0x1000u && (h & 1))) ++h;
+  return (uint16_t)(sign | h);
+}
+float h2f(uint16_t h) {
+  const uint32_t sign = (uint32_t)(h & 0x8000u) << 16;
+  const int exp = (h >> 10) & 0x1f;
+  uint32_t mant = h & 0x3ffu;
+  uint32_t x;
+  if (exp == 0) {
+    if (!mant) x = sign;
+    else {
+      int e = -1;
+      do { mant <<= 1; ++e; } while (!(mant & 0x400u));
+      x = sign | ((uint32_t)(127 - 15 - e) << 23) | ((mant & 0x3ffu) << 13);
+    }
+  } else if (exp == 31) x = sign | 0x7f800000u | (mant << 13);
+  else x = sign | ((uint32_t)(exp - 15 + 127) << 23) | (mant << 13);
+  float f;
+  std::memcpy(&f, &x, 4);
+  return f;
+}
+
+// Tensor-core persistent executor: role assignment (one 128-row weight tile
+// per CTA), fp16 hi/lo weight images, activation / counter buffers.
+rnntg_status setup_tc(rnntg_decoder* d) {
+  rnntg_model* m = d->m;
+  const DevModel& M = m->dm;
+  const rnntg_dims& dd = m->dims;
+  const bool lstm = M.cell == RNNTG_CELL_LSTM;
+  const int H = M.H, J = M.J, V1 = M.V1, D = M.D, Hp = M.Hp, Jp = M.Jp, L = M.L;
+  if (d->B > ptc::MAXB) return fail(RNNTG_E_VALUE, "tensor-core executor supports batch <= 32");
+  if (Hp > ptc::MAXKP || Jp > ptc::MAXKP)
+    return fail(RNNTG_E_VALUE, "tensor-core executor supports hidden/joint <= 640");
+  const int NJ = (V1 + D + 127) / 128, NP = (J + 127) / 128;
+  const int NG = lstm ? (H + 31) / 32 : (H + 127) / 128;
+  if (NJ > ptc::MAXNJ) return fail(RNNTG_E_VALUE, "tensor-core executor: vocab + durations <= 2048");
+  if (NG > 64) return fail(RNNTG_E_VALUE, "tensor-core executor: too many gate tiles");
+  std::vector<int4> roles;
+  for (int t = 0; t < NJ; ++t) roles.push_back(make_int4(ptc::ROLE_J, 0, t, 0));
+  for (int t = 0; t < NP; ++t) roles.push_back(make_int4(ptc::ROLE_P, 0, t, 0));
+  for (int l = 0; l < L; ++l) {
+    for (int t = 0; t < NG; ++t) roles.push_back(make_int4(ptc::ROLE_R, l, t, 0));
+    if (l > 0)
+      for (int t = 0; t < NG; ++t) roles.push_back(make_int4(ptc::ROLE_I, l, t, 0));
+  }
+  const int G = (int)roles.size();
+  int nsm = 0, optin = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
+  if (G > nsm) return fail(RNNTG_E_VALUE, "tensor-core executor needs one SM per weight tile");
+  const int KCmax = std::max(Hp, Jp) / 64;
+  d->tsmem = ptc::smem_bytes(KCmax);
+  if (d->tsmem > (size_t)optin) return fail(RNNTG_E_VALUE, "tensor-core executor: smem budget");
+  CK(cudaFuncSetAttribute(ptc::ptc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ptc::ptc_kernel, ptc::NTH, d->tsmem));
+  if (per_sm < 1) return fail(RNNTG_E_VALUE, "tensor-core executor cannot be resident");
+  // ---- weight images: W_hi [KC][128 x 64] swizzled, then W_lo [K/2][128] packed pairs ----
+  const auto& w = m->host_w;
+  const int bse = 1 + 3 * L;
+  const size_t wstride = (size_t)KCmax * 16384 + (size_t)KCmax * 32 * 128 * 4;
+  std::vector<unsigned char> img((size_t)G * wstride, 0);
+  std::vector<float> row(ptc::MAXKP);
+  for (int c = 0; c < G; ++c) {
+    const int role = roles[c].x, l = roles[c].y, t = roles[c].z;
+    const int K = role == ptc::ROLE_J ? J : H;
+    const int Kp = role == ptc::ROLE_J ? Jp : Hp;
+    // weight element (tile row mm, k); 0 outside the model
+    auto wel = [&](int mm, int k) -> float {
+      if (k >= K) return 0.0f;
+      if (role == ptc::ROLE_J) {
+        const int n = 128 * t + mm;
+        if (n < V1) return w[bse + 2][(size_t)k * V1 + n];
+        if (n < V1 + D) return w[bse + 3][(size_t)k * D + (n - V1)];
+        return 0.0f;
+      }
+      if (role == ptc::ROLE_P) {
+        const int j = 128 * t + mm;
+        return j < J ? w[bse + 1][(size_t)k * J + j] : 0.0f;
+      }
+      const int u = lstm ? 32 * t + (mm & 31) : 128 * t + mm;
+      const int g = lstm ? (mm >> 5) : 0;
+      if (u >= H) return 0.0f;
+      const std::vector<float>& W = role == ptc::ROLE_R ? w[2 + 3 * l] : w[1 + 3 * l];
+      return W[(size_t)k * (lstm ? 4 * H : H) + g * H + u];
+    };
+    float amax = 0.0f;
+    for (int mm = 0; mm < 128; ++mm)
+      for (int k = 0; k < K; ++k) amax = std::max(amax, std::fabs(wel(mm, k)));
+    // scale by 2^s so max |W'| lies in [2^11, 2^12): W_lo' stays a normal fp16
+    int sexp = 0;
+    if (amax > 0.0f) {
+      int e;
+      std::frexp(amax, &e);  // amax = f * 2^e, f in [0.5, 1)
+      sexp = 12 - e;
+    }
+    const float scale = std::ldexp(1.0f, sexp), inv = std::ldexp(1.0f, -sexp);
+    int invbits;
+    std::memcpy(&invbits, &inv, 4);
+    roles[c].w = invbits;
+    unsigned char* hi = img.data() + (size_t)c * wstride;
+    uint32_t* lo = reinterpret_cast<uint32_t*>(hi + (size_t)KCmax * 16384);
+    for (int mm = 0; mm < 128; ++mm) {
+      for (int k = 0; k < Kp; ++k) row[k] = wel(mm, k) * scale;
+      for (int k = 0; k < Kp; k += 2) {
+        uint16_t lb[2];
+        for (int j = 0; j < 2; ++j) {
+          const float v = row[k + j];
+          const uint16_t hb = f2h_bits(v);
+          lb[j] = f2h_bits(v - h2f(hb));
+          std::memcpy(hi + (size_t)((k + j) / 64) * 16384 + ptc::swz(mm, (k + j) % 64), &hb, 2);
+        }
+        lo[(size_t)(k / 2) * 128 + mm] = (uint32_t)lb[0] | ((uint32_t)lb[1] << 16);
+      }
+    }
+  }
+  ptc::TParams& tp = d->tp;
+  tp = ptc::TParams{};
+  tp.G = G;
+  tp.B = d->B;
+  tp.T = d->T;
+  tp.ms = d->ms;
+  tp.cap = d->st.cap;
+  tp.algo = d->algo;
+  tp.L = L;
+  tp.cell = M.cell;
+  tp.H = H;
+  tp.Hp = Hp;
+  tp.J = J;
+  tp.Jp = Jp;
+  tp.V1 = V1;
+  tp.D = D;
+  tp.NJ = NJ;
+  tp.GH = M.GH;
+  tp.Gg = M.G;
+  tp.max_iters = d->st.max_iters;
+  for (int i = 0; i < D; ++i) tp.durations[i] = dd.durations[i];
+  int4* droles = nullptr;
+  CK(upload(d->mem, &droles, roles));
+  tp.roles = droles;
+  unsigned char* dimg = nullptr;
+  CK(upload(d->mem, &dimg, img));
+  tp.wimg = dimg;
+  tp.wstride = wstride;
+  for (int l = 0; l < L; ++l) {
+    float* db = nullptr;
+    CK(upload(d->mem, &db, w[3 + 3 * l]));
+    tp.bias[l] = db;
+  }
+  tp.table0 = M.table0;
+  tp.fp = d->st.fp;
+  tp.out_len = d->len_dev;
+  for (int b = 0; b <= ptc::TRUNK; ++b) {
+    if (b < L || b == ptc::TRUNK) {
+      const int kc = (b == ptc::TRUNK ? Jp : Hp) / 64;
+      tp.act_kc[b] = kc;
+      CK(d->mem.alloc(&tp.act[b], (size_t)2 * kc * ptc::CHUNK));
+      for (int c = 0; c < kc; ++c) {
+        int n = 0;
+        if (b == ptc::TRUNK) {
+          n = 1;  // P tile c/2
+        } else if (lstm) {
+          for (int t = 0; t < NG; ++t)
+            if (32 * t < 64 * (c + 1) && 32 * t + 32 > 64 * c) ++n;
+        } else {
+          n = 1;
+        }
+        tp.nprod[b][c] = n;
+      }
+    }
+  }
+  for (int l = 1; l < L; ++l) CK(d->mem.alloc(&tp.hh[l], (size_t)2 * 64 * 32 * 128));
+  CK(d->mem.alloc(&tp.part, (size_t)ptc::NSLOT * NJ * 32));
+  CK(d->mem.alloc(&tp.partd, (size_t)ptc::NSLOT * NJ * 32));
+  d->tcnt_bytes = (size_t)ptc::NCOUNTERS * ptc::CSTRIDE * sizeof(unsigned);
+  CK(d->mem.alloc(&d->tcnt, (size_t)ptc::NCOUNTERS * ptc::CSTRIDE));
+  tp.cnt = d->tcnt;
+  tp.tokens = d->st.tokens;
+  tp.frames = d->st.frames;
+  tp.scores = d->st.scores;
+  tp.durs = d->st.durs;
+  tp.counts = d->st.counts;
+  tp.ctrl = d->st.ctrl;
+  for (int r = 0; r < 4; ++r) tp.prof_first[r] = -1;
+  for (int c = G - 1; c >= 0; --c) tp.prof_first[roles[c].x] = c;
+  if (env_flag("RNNTG_PROF", false)) CK(d->mem.alloc(&tp.prof, (size_t)(ptc::NEV + G) * ptc::PROF_WIN));
+  return RNNTG_OK;
+}
+
+cudaError_t launch_tc(rnntg_decoder* d, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(d->tcnt, 0, d->tcnt_bytes, st);
+  if (e != cudaSuccess) return e;
+  void* args[1] = {&d->tp};
+  return cudaLaunchCooperativeKernel((const void*)ptc::ptc_kernel, dim3(d->tp.G), dim3(ptc::NTH), args,
+                                     d->tsmem, st);
+}
+
 cudaError_t build_graph(rnntg_decoder* d) {
   const bool pdl = env_flag("RNNTG_PDL", true);
   cudaError_t e;
@@ -683,7 +908,7 @@ rnntg_status rnntg_decoder_create(rnntg_model* m, int algo, int exec, int batch,
   if (algo < 0 || algo > 2) return fail(RNNTG_E_VALUE, "unknown algo");
   if (algo == RNNTG_ALGO_TDT_LABEL_LOOP && m->dm.D == 0)
     return fail(RNNTG_E_STATE, "duration-head decoding needs a model with a duration head");
-  if (exec != RNNTG_EXEC_GRAPH && exec != RNNTG_EXEC_PERSISTENT)
+  if (exec != RNNTG_EXEC_GRAPH && exec != RNNTG_EXEC_PERSISTENT && exec != RNNTG_EXEC_TENSOR)
     return fail(RNNTG_E_VALUE, "unknown exec mode");
   CK(cudaSetDevice(m->device));
   auto* d = new rnntg_decoder;
@@ -706,6 +931,7 @@ rnntg_status rnntg_decoder_create(rnntg_model* m, int algo, int exec, int batch,
       if (!encproj_plan(d->enc, m->dm, d->x_dev, d->st.fp, batch * max_frames))
         st = fail(RNNTG_E_CUDA, "cannot encode TMA tensor maps for the encoder projection");
       else if (exec == RNNTG_EXEC_GRAPH) e = build_graph(d);
+      else if (exec == RNNTG_EXEC_TENSOR) st = setup_tc(d);
       else st = setup_persistent(d);
     }
   }
@@ -786,6 +1012,9 @@ rnntg_status rnntg_launch(rnntg_decoder* d) {
     void* args[1] = {&d->pp};
     CK(cudaLaunchCooperativeKernel((const void*)pk::persistent_kernel, dim3(d->pp.G), dim3(pk::NTH),
                                    args, d->psmem, d->stream));
+  } else if (d->exec == RNNTG_EXEC_TENSOR) {
+    CK(encproj_launch(d->enc, d->stream));
+    CK(launch_tc(d, d->stream));
   } else {
     CK(cudaGraphLaunch(d->gexec, d->stream));
   }
@@ -970,6 +1199,7 @@ rnntg_status rnntg_time_kernel(rnntg_decoder* d, int which, int reps, float* avg
   auto launch_one = [&]() -> cudaError_t {
     if (which == 0) return encproj_launch(d->enc, st);
     if (which == 10) {  // the persistent decode kernel alone (fp already projected)
+      if (d->exec == RNNTG_EXEC_TENSOR) return launch_tc(d, st);
       if (d->exec != RNNTG_EXEC_PERSISTENT) return cudaErrorInvalidValue;
       void* args[1] = {&d->pp};
       return cudaLaunchCooperativeKernel((const void*)pk::persistent_kernel, dim3(d->pp.G),
@@ -1019,6 +1249,16 @@ rnntg_status rnntg_time_kernel(rnntg_decoder* d, int which, int reps, float* avg
   }
   *avg_ms = total / reps;
   d->launched = false;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_debug_trace(rnntg_decoder* d, unsigned long long* out, int n) {
+  if (!d || !out) return fail(RNNTG_E_VALUE, "bad arguments");
+  if (d->exec != RNNTG_EXEC_TENSOR || !d->tp.prof)
+    return fail(RNNTG_E_STATE, "tracing needs the tensor executor and RNNTG_PROF=1");
+  CK(cudaStreamSynchronize(d->stream));
+  const int tot = (ptc::NEV + d->tp.G) * ptc::PROF_WIN;
+  CK(cudaMemcpy(out, d->tp.prof, sizeof(unsigned long long) * std::min(n, tot), cudaMemcpyDeviceToHost));
   return RNNTG_OK;
 }
 

@@ -36,7 +36,8 @@ class DecodeAlgo(enum.IntEnum):
 
 class Exec(enum.IntEnum):
     Graph = 0        # CUDA graph with nested conditional WHILE nodes
-    Persistent = 1   # persistent kernel alternative
+    Persistent = 1   # persistent kernel alternative (FFMA, shared-memory weights)
+    Tensor = 2       # persistent kernel on tcgen05 tensor cores, role-specialised CTAs
 
 
 @dataclass

@@ -1,0 +1,52 @@
+"""Event trace of the tensor-core executor on C2 (RNNTG_PROF=1): median
+latency between pipeline events over 64 traced joint steps."""
+import ctypes as C
+import os
+import sys
+
+os.environ["RNNTG_PROF"] = "1"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+
+from paper_2406_03791_b200 import DecodeAlgo, Model, synth  # noqa: E402
+from paper_2406_03791_b200 import decoders as D  # noqa: E402
+from paper_2406_03791_b200._lib import lib  # noqa: E402
+
+dims = D.ModelDims(1024, 640, 640, 640, 1024, (), "lstm", 2)
+m = Model.from_seed(dims, 1)
+B, T = 32, 250
+x = synth.encoder_outputs(2, B, T, 1024)
+lens = np.full(B, T, np.int32)
+cap = D.build_decode_graph(m, DecodeAlgo.FrameSync, B, T, 5, D.Exec.Tensor)
+D.replay_decode(cap, x, lens)
+D.replay_decode(cap, x, lens)
+st = cap.stats()
+print("us/step", 1000 * st["gpu_ms"] / st["joint_evals"])
+G = 74
+buf = (C.c_uint64 * ((32 + G) * 64))()
+assert lib().rnntg_debug_trace(cap._h, buf, (32 + G) * 64) == 0, lib().rnntg_last_error()
+allev = np.array(buf, dtype=np.int64).reshape(32 + G, 64)
+ev = allev[:32]
+names = {0: "J post", 12: "J chunk0 ready", 13: "J chunk9 ready", 1: "J acc ready", 2: "J part pub",
+         3: "J decide done", 4: "R0 decide done", 5: "R0 h0 pub", 6: "I1 decide done", 7: "I1 acc ready",
+         11: "I1 h1 pub", 10: "R1 decide done", 8: "P decide done", 9: "P acc ready", 14: "P trunk pub",
+         16: "J xs written", 17: "J scan done", 18: "J part stored", 22: "R0 part counter", 23: "R0 part staged",
+         24: "R0 rules done", 19: "R0 pre ready", 20: "R0 acts in xs", 21: "R0 h stored",
+         27: "J mma chunk0 full", 28: "J mma chunk9 full", 29: "J mma issued"}
+order = [0, 12, 27, 13, 28, 29, 1, 16, 17, 18, 2, 3, 22, 23, 24, 4, 19, 20, 21, 5, 6, 7, 11, 8, 9, 14]
+t0 = ev[0].astype(np.float64)
+for e in order:
+    d = (ev[e] - ev[0]).astype(np.float64)
+    ok = ev[e] > 0
+    print(f"{names[e]:18s} +{np.median(d[ok]) / 1000:8.2f} us  (n={ok.sum()})")
+step = np.diff(ev[0].astype(np.float64))
+print("step period (J post -> next J post):", np.median(step) / 1000, "us")
+cyc = np.median((ev[26] - ev[25]).astype(np.float64)); ns = np.median((ev[3] - ev[0]).astype(np.float64))
+print("SM clock during decode: %.0f MHz" % (1000 * cyc / ns))
+pub = allev[32:].astype(np.float64) - ev[0][None, :].astype(np.float64)
+roles = ["J"] * 9 + ["P"] * 5 + ["R0"] * 20 + ["R1"] * 20 + ["I1"] * 20
+for name in ["J", "R0", "I1", "R1", "P"]:
+    idx = [i for i, r in enumerate(roles) if r == name]
+    med = [np.median(pub[i]) / 1000 for i in idx]
+    print(name, "publish (us after J post, per tile):", " ".join(f"{x:.2f}" for x in med))
