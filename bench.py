@@ -2,7 +2,7 @@
 """Benchmark: decoded encoder frames/s of the B200 RNN-T greedy decoder.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c2|c3|c4|c5|c1] [--exec graph|persistent]
+                    [--config c2|c3|c4|c5|c1] [--exec tensor|persistent|graph]
 
 A "step" is one decode of one batch through the captured program (K1 encoder
 projection + the device-resident decode loops).  Default workload (N=1) is
@@ -45,6 +45,7 @@ CONFIGS = {
     "c5": ("fs", 256, 500, 5, (), 2, 640, 640, 1024, 1024, "strong"),
 }
 ALGO_ID = {"fs": 0, "ll": 1, "tdt": 2}
+EXEC_ID = {"graph": 0, "persistent": 1, "tensor": 2}
 ALGO_NAME = {"fs": "frame-looping", "ll": "label-looping", "tdt": "TDT label-looping"}
 METRIC = "decoded encoder frames/sec (Parakeet-1.1B dec, B=32); GPU idle %; µs/step"
 
@@ -56,12 +57,14 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--exec", default="persistent", choices=["graph", "persistent"],
-                    help="persistent kernel (default, fastest) or the conditional-WHILE CUDA graph")
+    ap.add_argument("--exec", default="tensor", choices=["tensor", "graph", "persistent"],
+                    help="tensor: persistent kernel on tcgen05 tensor cores (default, fastest; falls "
+                         "back to persistent when the shape does not fit it), persistent: FFMA "
+                         "persistent kernel, graph: conditional-WHILE CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-compare", action="store_true",
-                    help="skip timing the other executor (graph vs persistent)")
+                    help="skip timing the other executors")
     ap.add_argument("--blank-bias", type=float, default=0.0)
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="target duration of the bounded CPU reference sample")
@@ -262,8 +265,22 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent):
     step_bytes = (st.pred_steps * pred_w + st.joint_evals * joint_w) / steps
     step_flops = (st.pred_steps * pred_f + st.joint_evals * joint_f) / steps
     t_step = ms_per_step * 1000.0 / steps
-    t_roof = max(step_bytes / (hbm_peak * 1e3), step_flops / (fp32_peak * 1e6))
-    return {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+    tensor = args.exec == "tensor"
+    tc_peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1378.6)))
+    # tensor executor: the fp32 GEMVs run as 3 fp16 tcgen05 products (hi.hi, hi.lo,
+    # lo.hi), so the compute bound is 3x the FLOPs at the dense fp16 tensor peak;
+    # the FFMA executors are bound by the FP32 CUDA-core peak
+    t_flops = step_flops * 3 / (tc_peak * 1e6) if tensor else step_flops / (fp32_peak * 1e6)
+    t_roof = max(step_bytes / (hbm_peak * 1e3), t_flops)
+    kname = {"persistent": "ptc_kernel" if tensor else "persistent_kernel"}.get(dom, dom)
+    extra = {}
+    if tensor and dom == "persistent":
+        tc_ach = 3 * flops_per[dom] / (kern[dom] / 1000.0) / 1e12
+        extra["tensor"] = {"achieved_tflops": tc_ach, "peak_tflops": tc_peak, "frac": tc_ach / tc_peak,
+                           "note": "3 fp16 tcgen05 products per fp32 MAC (hi/lo split) vs "
+                                   "MEASURED_PEAKS bf16_tflops_sustained; weights resident in "
+                                   "smem/TMEM, so the hbm line is the equivalent streaming rate"}
+    return {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": hbm_peak, "unit": "GB/s", **extra,
             "frac": ach / hbm_peak, "traffic": None,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)",
             "algorithmic_bytes_per_launch": bytes_per[dom],
@@ -278,13 +295,16 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent):
 
 
 def measure_alt_exec(args, L_, model, cfg, xd, ld, Bl, T, frames_all):
-    """Time the other executor (graph <-> persistent) on the same inputs."""
-    import torch
+    """Time the other executors on the same inputs."""
+    return [measure_exec(other, L_, model, cfg, xd, ld, Bl, T, frames_all)
+            for other in ("tensor", "persistent", "graph") if other != args.exec]
+
+
+def measure_exec(other, L_, model, cfg, xd, ld, Bl, T, frames_all):
     from paper_2406_03791_b200._lib import Stats, check
     algo = cfg[0]
-    other = "graph" if args.exec == "persistent" else "persistent"
     dh = C.c_void_p()
-    rc = L_.rnntg_decoder_create(model.handle, ALGO_ID[algo], 0 if other == "graph" else 1, Bl, T,
+    rc = L_.rnntg_decoder_create(model.handle, ALGO_ID[algo], EXEC_ID[other], Bl, T,
                                  cfg[3], C.byref(dh))
     if rc != 0:
         return {"exec": other, "unavailable": L_.rnntg_last_error().decode()}
@@ -372,8 +392,15 @@ def main():
     model = Model.from_seed(dims, 1, device=local, blank_bias=args.blank_bias)
     L_ = lib()
     dh = C.c_void_p()
-    check(L_.rnntg_decoder_create(model.handle, ALGO_ID[algo], 0 if args.exec == "graph" else 1,
-                                  Bl, T, ms, C.byref(dh)))
+    rc = L_.rnntg_decoder_create(model.handle, ALGO_ID[algo], EXEC_ID[args.exec], Bl, T, ms,
+                                 C.byref(dh))
+    if rc != 0 and args.exec == "tensor":  # shape outside the tensor executor: FFMA persistent
+        print(f"tensor executor unavailable ({L_.rnntg_last_error().decode()}); using persistent",
+              file=sys.stderr)
+        args.exec = "persistent"
+        rc = L_.rnntg_decoder_create(model.handle, ALGO_ID[algo], EXEC_ID[args.exec], Bl, T, ms,
+                                     C.byref(dh))
+    check(rc)
     x, lens = make_inputs(cfg, b0, b1)
     xd = torch.from_numpy(x).cuda()
     ld = torch.from_numpy(lens).cuda()
@@ -417,7 +444,7 @@ def main():
     ms_per_step = total_ms / args.steps
     per_rank_frames = Bl * T
     fs = algo == "fs"
-    persistent = args.exec == "persistent"
+    persistent = args.exec in ("persistent", "tensor")
     if persistent:
         launches_per_step = 2
     else:

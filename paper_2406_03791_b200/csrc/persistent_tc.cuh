@@ -62,7 +62,8 @@ constexpr int ACC_COLS = 96;
 constexpr int WLO_COL = 2 * ACC_COLS;
 constexpr int CSTRIDE = 32;      // u32 words between counters (one 128-byte line each)
 
-enum Role { ROLE_J = 0, ROLE_P = 1, ROLE_R = 2, ROLE_I = 3 };
+enum Role { ROLE_J = 0, ROLE_P = 1, ROLE_R = 2, ROLE_I = 3, ROLE_E = 4 };  // E: emitter (no weights)
+constexpr int NROLES = 5;
 
 // counter word indices (times CSTRIDE)
 __host__ __device__ inline int cidx_act(int buf, int kc) { return buf * MAXKC + kc; }
@@ -89,8 +90,8 @@ struct TParams {
   int act_kc[MAXBUF];
   int nprod[MAXBUF][MAXKC];   // producers per chunk
   float* hh[MAXL];            // [2 parity][tiles][32 rows][128] (layers >= 1)
-  float4* part;               // [NSLOT][NJ][32] vocab (max, sumexp, best, idx)
-  float4* partd;              // [NSLOT][NJ][32] duration partials
+  unsigned long long* pw;     // [NSLOT][2][NJ][32] argmax words {best f32 | idx << 8 | tag}, vocab / duration
+  float2* ps;                 // [NSLOT][NJ][32] vocab (row max, sumexp) for the emitted score
   unsigned* cnt;              // [NCOUNTERS * CSTRIDE]
   int* tokens;
   int* frames;
@@ -99,7 +100,7 @@ struct TParams {
   int* counts;
   Ctrl* ctrl;
   unsigned long long* prof;   // optional event trace [NEV][PROF_WIN] (first CTA of each role)
-  int prof_first[4];          // first CTA index per role (tracing CTAs)
+  int prof_first[NROLES];     // first CTA index per role (tracing CTAs)
 };
 constexpr int PROF_WIN = 64;  // traced joint steps [PROF_S0, PROF_S0 + PROF_WIN)
 constexpr int PROF_S0 = 100;
@@ -213,6 +214,21 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// Self-validating argmax word: 8-byte single-copy-atomic {value, idx << 8 | tag}.
+// Readers spin on the words themselves (no counter, no release round trip).
+__device__ __forceinline__ unsigned step_tag(long long s) { return (unsigned)(s % 255) + 1u; }
+__device__ __forceinline__ unsigned long long pack_arg(float v, int idx, unsigned tag) {
+  return (unsigned long long)__float_as_uint(v) | ((unsigned long long)(((unsigned)idx << 8) | tag) << 32);
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // byte offset of (row r, k) inside a [rows x 64] fp16 K-major SWIZZLE_128B chunk
 __host__ __device__ inline uint32_t swz(int r, int k) {
   return (uint32_t)(r * 128 + ((((k * 2) >> 4) ^ (r & 7)) << 4) + ((k * 2) & 15));
@@ -322,6 +338,7 @@ struct Epi {
   const bool fs, tdt, lstm, tracer;
   unsigned* const cnt;
   int maxlen = 0, round = 0, p = 0, err = 0, acc_any = 0;
+  float ih[NR];  // R_0: table0[label] rows prefetched during the decision
   long long s = 0, joint_evals = 0, pred_steps = 0, outer_iters = 0;
   bool finish = false;
 
@@ -368,8 +385,8 @@ struct Epi {
         v[i] = (__uint_as_float(x0[i]) + (__uint_as_float(x1[i]) + __uint_as_float(x2[i]))) * wsc;
     }
     tc_fence_before();
-    epi_sync();
-    if (et == 0) mbar_arrive(&sm.acce[r & 1]);
+    __syncwarp();
+    if ((et & 31) == 0) mbar_arrive(&sm.acce[r & 1]);  // one arrival per epilogue warp
   }
   __device__ __forceinline__ void wait_counter(int ci, unsigned target) {
     if (et == 0) spin_geq(cnt + (size_t)ci * CSTRIDE, target);
@@ -391,7 +408,7 @@ struct Epi {
       sm.cnt[et] = 0;
       const int len = et < B ? __ldg(&P.out_len[et]) : 0;
       sm.flag[et] = (et < B ? (fs ? (0 >= len) : !(0 < len)) : 1) | 2;  // every row runs P0
-      if (blockIdx.x == 0 && et < B) P.counts[et] = 0;
+      if (role == ROLE_E && et < B) P.counts[et] = 0;
     }
     if (et == 0) {
       sm.misc[2] = 0;
@@ -401,7 +418,8 @@ struct Epi {
     epi_sync();
   }
 
-  // ---- J: logits of this tile's 128 columns -> per-row softmax partials of step s
+  // ---- J: logits of this tile's 128 columns -> per-row argmax words (critical),
+  // then the per-row (max, sumexp) partials for the emitted score (off the path)
   __device__ void joint_round() {
     mark(0);
     post((int)s);
@@ -434,198 +452,234 @@ struct Epi {
       md = gd ? x : md;
       id = gd ? col - V1 : id;
     }
-    float ev = 0.0f, ed = 0.0f;
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      const float x = xs[(16 * qq + c) * 33 + r];
-      const int col = c0 + c;
-      const float e1 = __expf(x - (col < V1 ? mv : md));
-      ev += col < V1 ? e1 : 0.0f;
-      ed += (col >= V1 && col < VD) ? e1 : 0.0f;
-    }
     mark(17);
-    sm.red[qq * 32 + r] = make_float4(mv, ev, mv, __int_as_float(iv));
-    sm.red[256 + qq * 32 + r] = make_float4(md, ed, md, __int_as_float(id));
+    sm.red[qq * 32 + r] = make_float4(mv, 0.0f, 0.0f, __int_as_float(iv));
+    sm.red[256 + qq * 32 + r] = make_float4(md, 0.0f, 0.0f, __int_as_float(id));
     epi_sync();
     const int slot = (int)(s % NSLOT);
-    if (et < 64) {  // merge the 8 column groups in order: et < 32 vocab, else durations
+    const unsigned tg = step_tag(s);
+    if (et < 64) {  // merge the 8 column groups in column order: et < 32 vocab, else durations
       const int rr = et & 31, seg = et >> 5;
-      if (seg == 0 || P.D) {
-        float M = -INFINITY, S = 0.0f, bv = -INFINITY;
-        int bi = 0x7fffffff;
+      float bv = -INFINITY;
+      int bi = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float4 t = sm.red[seg * 256 + k * 32 + rr];
-          if (t.x != -INFINITY) {
-            const float nm = fmaxf(M, t.x);
-            S = (S == 0.0f ? 0.0f : S * __expf(M - nm)) + t.y * __expf(t.x - nm);
-            M = nm;
-            if (t.z > bv) { bv = t.z; bi = __float_as_int(t.w); }
-          }
+      for (int k = 0; k < 8; ++k) {
+        const float4 t = sm.red[seg * 256 + k * 32 + rr];
+        if (t.x > bv) {  // strict: the lowest column wins ties (argmax_last_into)
+          bv = t.x;
+          bi = __float_as_int(t.w);
         }
-        float4* dst = seg == 0 ? P.part : P.partd;
-        dst[((size_t)slot * P.NJ + tile) * 32 + rr] = make_float4(M, S, bv, __int_as_float(bi));
       }
+      if (seg == 0 || P.D)
+        st_relaxed_u64(&P.pw[(((size_t)slot * 2 + seg) * P.NJ + tile) * 32 + rr], pack_arg(bv, bi, tg));
+      if (seg == 0) sm.vdec[rr] = bv;  // this tile's row max, for the sumexp pass
     }
     mark(18);
+    mark_pub();
+    epi_sync();
+    // sumexp over the vocab columns relative to the tile's row max
+    {
+      const float M = sm.vdec[r];
+      float ev = 0.0f;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const float x = xs[(16 * qq + c) * 33 + r];
+        ev += (c0 + c < V1) ? __expf(x - M) : 0.0f;
+      }
+      sm.red[qq * 32 + r].y = ev;
+    }
+    epi_sync();
+    if (et < 32) {
+      float S = 0.0f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) S += sm.red[k * 32 + et].y;
+      P.ps[((size_t)slot * P.NJ + tile) * 32 + et] = make_float2(sm.vdec[et], S);
+    }
     epi_sync();
     if (et == 0) red_release_add(cnt + (size_t)cidx_part() * CSTRIDE, 1);
     mark(2);
-    mark_pub();
   }
 
-  // ---- replicated decision of step s (argmax / lse merge + rules)
+  // ---- replicated decision of step s.  The first epilogue warp (lane = row)
+  // spins on the J tiles' tagged argmax words, applies the rules and reduces
+  // the row flags with ballots; ONE barrier then publishes the outcome.
+  // The emitter also merges the (max, sumexp) partials for the score.
   __device__ void decide() {
-    wait_counter(cidx_part(), (unsigned)P.NJ * (unsigned)(s + 1));
-    if (role == ROLE_R && layer == 0) mark(22);
-    const int slot = (int)(s % NSLOT);
-    const int n = P.NJ * 32;
-    float4* ps = reinterpret_cast<float4*>(sm.xs);  // [2][NJ][32]
-    {
-      float4 a[2], d[2];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int i = et + NEPI * j;
-        if (i < n) {
-          a[j] = __ldcg(&P.part[(size_t)slot * n + i]);
-          if (P.D) d[j] = __ldcg(&P.partd[(size_t)slot * n + i]);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int i = et + NEPI * j;
-        if (i < n) {
-          ps[i] = a[j];
-          if (P.D) ps[n + i] = d[j];
-        }
-      }
-    }
-    epi_sync();
-    if (role == ROLE_R && layer == 0) mark(23);
-    int acc = 0, live = 0;
-    const int t_fs = sm.misc[2];
-    if (et < B) {
+    if (et < 32) {
       const int b = et;
-      float Mx = -INFINITY, Sx = 0.0f, best = -INFINITY;
-      int bi = 0;
-      for (int t = 0; t < P.NJ; ++t) {
-        const float4 pv = ps[t * 32 + b];
-        if (pv.x != -INFINITY) {
-          const float nm = fmaxf(Mx, pv.x);
-          Sx = (Sx == 0.0f ? 0.0f : Sx * __expf(Mx - nm)) + pv.y * __expf(pv.x - nm);
-          Mx = nm;
-          if (pv.z > best) {  // tiles in column order: strict > keeps the lowest index
-            best = pv.z;
-            bi = __float_as_int(pv.w);
-          }
-        }
-      }
-      int dd = 0;
-      if (P.D) {
+      const bool valid = b < B;
+      const int slot = (int)(s % NSLOT);
+      const unsigned tg = step_tag(s);
+      const bool emitter = role == ROLE_E;
+      int kk = blank, dd = 0;
+      float best = 0.0f;
+      if (valid) {
+        const unsigned long long* wv = P.pw + ((size_t)slot * 2 * P.NJ) * 32 + b;
+        const unsigned long long* wd = wv + (size_t)P.NJ * 32;
+        unsigned long long a[MAXNJ], d[MAXNJ];
+#pragma unroll
+        for (int t = 0; t < MAXNJ; ++t) a[t] = d[t] = 0ull;
+        // every tile's word in flight at once; only R_0 consumes the decision
+        // on the critical path, the other roles back off
+        const bool lazy = !(role == ROLE_R && layer == 0);
+        bool ok;
+        do {
+          ok = true;
+#pragma unroll
+          for (int t = 0; t < MAXNJ; ++t)
+            if (t < P.NJ) {
+              if ((unsigned)(a[t] >> 32 & 0xffu) != tg) a[t] = ld_relaxed_u64(wv + t * 32);
+              if (P.D && (unsigned)(d[t] >> 32 & 0xffu) != tg) d[t] = ld_relaxed_u64(wd + t * 32);
+            }
+#pragma unroll
+          for (int t = 0; t < MAXNJ; ++t)
+            if (t < P.NJ)
+              ok = ok && (unsigned)(a[t] >> 32 & 0xffu) == tg && (!P.D || (unsigned)(d[t] >> 32 & 0xffu) == tg);
+          if (!ok && lazy) __nanosleep(500);
+        } while (!ok);
+        best = -INFINITY;
         float bd = -INFINITY;
         int di = 0;
-        for (int t = 0; t < P.NJ; ++t) {
-          const float4 pv = ps[n + t * 32 + b];
-          if (pv.z > bd) {
-            bd = pv.z;
-            di = __float_as_int(pv.w);
+#pragma unroll
+        for (int t = 0; t < MAXNJ; ++t)
+          if (t < P.NJ) {
+            const float x = __uint_as_float((unsigned)a[t]);
+            if (x > best) {  // tiles in column order: strict > keeps the lowest index
+              best = x;
+              kk = (int)((unsigned)(a[t] >> 32) >> 8);
+            }
+            if (P.D) {
+              const float y = __uint_as_float((unsigned)d[t]);
+              if (y > bd) {
+                bd = y;
+                di = (int)((unsigned)(d[t] >> 32) >> 8);
+              }
+            }
           }
-        }
-        dd = P.durations[di];
+        dd = P.D ? P.durations[di] : 0;
       }
-      const int k = bi;
-      const float v = best - (Mx + logf(Sx));
-      // decision rules, thread per row (decoders.cpp:261-307 / 432-512)
+      sm.kdec[b] = kk;
+      if (role == ROLE_R && layer == 0) mark(22);
+      float v = 0.0f;
+      if (emitter) {
+        if (b == 0) spin_geq(cnt + (size_t)cidx_part() * CSTRIDE, (unsigned)P.NJ * (unsigned)(s + 1));
+        __syncwarp();
+        if (valid) {
+          float Mx = -INFINITY, Sx = 0.0f;
+          for (int t = 0; t < P.NJ; ++t) {
+            const float2 pv = __ldcg(&P.ps[((size_t)slot * P.NJ + t) * 32 + b]);
+            if (pv.x != -INFINITY) {
+              const float nm = fmaxf(Mx, pv.x);
+              Sx = (Sx == 0.0f ? 0.0f : Sx * __expf(Mx - nm)) + pv.y * __expf(pv.x - nm);
+              Mx = nm;
+            }
+          }
+          v = best - (Mx + logf(Sx));  // logp of the argmax (log_softmax_into, tensor.cpp:463-480)
+        }
+      }
+      // decision rules, lane per row (decoders.cpp:261-307 / 432-512)
+      const int t_fs = sm.misc[2];
       int f = sm.flag[b] & ~2;
-      const bool emitter = blockIdx.x == 0;
-      if (fs) {
-        if (!(f & 1)) {
+      if (valid) {
+        const int k = kk;
+        if (fs) {
+          if (!(f & 1)) {
+            if (k == blank) {
+              f |= 1;
+            } else {
+              const int nb = sm.cnt[b];
+              if (emitter && nb < P.cap) {
+                const size_t o = (size_t)b * P.cap + nb;
+                P.tokens[o] = k;
+                P.frames[o] = t_fs;
+                P.scores[o] = v;
+                P.durs[o] = 0;
+                P.counts[b] = nb + 1;
+              }
+              sm.cnt[b] = nb + 1;
+              sm.label[b] = k;
+              f |= 2;
+            }
+          }
+        } else if (!(f & 1)) {
+          const int len = __ldg(&P.out_len[b]);
+          int t = sm.tb[b], u = sm.ub[b];
           if (k == blank) {
-            f |= 1;
+            const int d = tdt ? dd : 1;
+            t += d > 1 ? d : 1;
+            u = 0;
           } else {
+            const int d = tdt ? dd : 0;
             const int nb = sm.cnt[b];
             if (emitter && nb < P.cap) {
               const size_t o = (size_t)b * P.cap + nb;
               P.tokens[o] = k;
-              P.frames[o] = t_fs;
+              P.frames[o] = t;
               P.scores[o] = v;
-              P.durs[o] = 0;
+              P.durs[o] = d;
               P.counts[b] = nb + 1;
             }
             sm.cnt[b] = nb + 1;
             sm.label[b] = k;
             f |= 2;
+            u += 1;
+            if (d > 0) {
+              t += d;
+              u = 0;
+            } else if (u == P.ms) {
+              t += 1;
+              u = 0;
+            }
           }
+          sm.tb[b] = t;
+          sm.ub[b] = u;
+          if (!(t < len)) f |= 1;
         }
-        live = !(f & 1);
-      } else if (!(f & 1)) {
-        const int len = __ldg(&P.out_len[b]);
-        int t = sm.tb[b], u = sm.ub[b];
-        if (k == blank) {
-          const int d = tdt ? dd : 1;
-          t += d > 1 ? d : 1;
-          u = 0;
-        } else {
-          const int d = tdt ? dd : 0;
-          const int nb = sm.cnt[b];
-          if (emitter && nb < P.cap) {
-            const size_t o = (size_t)b * P.cap + nb;
-            P.tokens[o] = k;
-            P.frames[o] = t;
-            P.scores[o] = v;
-            P.durs[o] = d;
-            P.counts[b] = nb + 1;
-          }
-          sm.cnt[b] = nb + 1;
-          sm.label[b] = k;
-          f |= 2;
-          u += 1;
-          if (d > 0) {
-            t += d;
-            u = 0;
-          } else if (u == P.ms) {
-            t += 1;
-            u = 0;
-          }
-        }
-        sm.tb[b] = t;
-        sm.ub[b] = u;
-        if (!(t < len)) f |= 1;
-        live = !(f & 1);
       }
-      acc = (f >> 1) & 1;
+      const bool acc_b = valid && ((f >> 1) & 1), live_b = valid && !(f & 1);
+      const bool accany = __ballot_sync(0xffffffffu, acc_b) != 0;
+      const bool liveany = __ballot_sync(0xffffffffu, live_b) != 0;
+      bool fin = false, frame_end = false;
+      if (fs) {
+        int sym = sm.misc[3] + 1;
+        int t = t_fs;
+        if (!liveany || sym >= P.ms) {  // frame ends (decoders.cpp:297-313)
+          frame_end = true;
+          t += 1;
+          sym = 0;
+          if (t >= maxlen) fin = true;
+          if (valid) f = (f & 2) | (t >= __ldg(&P.out_len[b]) ? 1 : 0);
+        }
+        __syncwarp();
+        if (b == 0) {
+          sm.misc[3] = sym;
+          sm.misc[2] = t;
+        }
+      } else {
+        fin = !liveany;
+      }
+      if (joint_evals + 1 > P.max_iters) fin = true;
       sm.flag[b] = f;
-    }
-    if (role == ROLE_R && layer == 0) mark(24);
-    acc_any = epi_or(acc);
-    const int live_any = epi_or(live);
-    finish = false;
-    if (fs) {
-      int sym = sm.misc[3] + 1;
-      int t = t_fs;
-      if (!live_any || sym >= P.ms) {  // frame ends (decoders.cpp:297-313)
-        t += 1;
-        sym = 0;
-        ++outer_iters;
-        if (t >= maxlen) finish = true;
-        if (et < B) sm.flag[et] = (sm.flag[et] & 2) | (t >= __ldg(&P.out_len[et]) ? 1 : 0);
-      }
-      epi_sync();
-      if (et == 0) {
-        sm.misc[3] = sym;
-        sm.misc[2] = t;
-      }
-    } else {
-      finish = !live_any;
-    }
-    ++joint_evals;
-    if (joint_evals > P.max_iters) {
-      err = ERR_RUNAWAY;
-      finish = true;
+      if (b == 0) sm.misc[5] = (accany ? 1 : 0) | (fin ? 2 : 0) | (frame_end ? 4 : 0);
+      if (role == ROLE_R && layer == 0) mark(24);
     }
     epi_sync();
-    if (et == 0) red_release_add(cnt + (size_t)cidx_ack() * CSTRIDE, 1);
-    mark(role == ROLE_J ? 3 : role == ROLE_R ? (layer == 0 ? 4 : 10) : role == ROLE_I ? 6 : 8);
+    const int o = sm.misc[5];
+    acc_any = o & 1;
+    finish = (o >> 1) & 1;
+    if (o & 4) ++outer_iters;
+    ++joint_evals;
+    if (joint_evals > P.max_iters) err = ERR_RUNAWAY;
+    if (role == ROLE_R && layer == 0 && acc_any && !finish) {
+      // the layer-0 cell needs table0[label]: gather now (lands during read_acc)
+      const int unit = lstm ? 32 * tile + (m >> 2) : 128 * tile + m, gate = lstm ? (m & 3) : 0;
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        const int r = r0 + i;
+        ih[i] = r < B ? __ldg(&P.table0[(size_t)sm.kdec[r] * P.GH + unit * P.Gg + gate]) : 0.0f;
+      }
+    }
+    mark(role == ROLE_J ? 3 : role == ROLE_R ? (layer == 0 ? 4 : 10) : role == ROLE_I ? 6 : role == ROLE_E ? 15 : 8);
   }
 
   // ---- the decode skeleton: pred(te) after each accepting decision, idle(te) otherwise
@@ -652,41 +706,46 @@ struct Epi {
       } else {
         idle(s + 1);
       }
+      // this CTA is done with step s's words: ack (slot reuse, joint_round)
+      if (et == 0) red_release_add(cnt + (size_t)cidx_ack() * CSTRIDE, 1);
       ++s;
       if (et < 32) sm.flag[et] &= ~2;
       epi_sync();
     }
   }
 
-  // ---- layer cells: pre-activations (gate row m, 32 rows) -> committed h of the tile's units
-  // LSTM: gate-major rows (g = m/32, unit 32*tile + m%32); thread (unit et%32, rows et/32 + 4j)
+  // ---- layer cells: pre-activations (gate row m, rows r0..r0+15) -> committed h.
+  // LSTM tiles are unit-major (m = 4*unit + gate): a lane quad holds one unit's
+  // i,f,g,o, so the gates meet through a per-warp smem transpose (__syncwarp,
+  // no CTA barrier).  Lane (quad qd, slot g') then runs the cell for rows
+  // r0 + 4j + g', j < 4.
   __device__ __forceinline__ void cell_lstm(const float (&pre)[NR], int l, int pe, float (&c)[4], float (&h)[4]) {
-    const int g = m >> 5, ul = m & 31;
-    float* xg = sm.xs + g * 1024;  // [g][r][ul]
-    if (g == 2) {
+    const int lane = et & 31, g = lane & 3, qd = lane >> 2;
+    float* xw = sm.xs + (et >> 5) * (NR * 33);  // this warp's [16 rows][33]
+    // i, f, o: sigmoid; g: tanh(x) = 2 sigmoid(2x) - 1 (absolute error ~1e-7,
+    // what the cell update c' = f c + i g needs; one code path per lane quad)
+    const float sc = g == 2 ? 2.0f : 1.0f;
 #pragma unroll
-      for (int i = 0; i < NR; ++i) xg[(r0 + i) * 32 + ul] = tanh_fast(pre[i]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < NR; ++i) xg[(r0 + i) * 32 + ul] = sigm(pre[i]);
+    for (int i = 0; i < NR; ++i) {
+      const float a = sigm(sc * pre[i]);
+      xw[i * 33 + lane] = g == 2 ? 2.0f * a - 1.0f : a;
     }
-    epi_sync();
-    if (role == ROLE_R) mark(20);
-    const int ulc = et & 31, rb = et >> 5;  // unit, rows rb + 8j
-    const int u = 32 * tile + ulc;
+    __syncwarp();
+    const int u = 32 * tile + 8 * (m >> 5) + qd;
     unsigned char* ch = P.act[l] + ((size_t)(pe & 1) * P.act_kc[l] + (u >> 6)) * CHUNK;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int r = rb + 8 * j;
+      const int i = 4 * j + g, r = r0 + i;
+      const float i_ = xw[i * 33 + 4 * qd], f_ = xw[i * 33 + 4 * qd + 1];
+      const float g_ = xw[i * 33 + 4 * qd + 2], o_ = xw[i * 33 + 4 * qd + 3];
       const bool commit = r < B && (sm.flag[r] & 2);
-      const float i_ = sm.xs[r * 32 + ulc], f_ = sm.xs[1024 + r * 32 + ulc];
-      const float g_ = sm.xs[2048 + r * 32 + ulc], o_ = sm.xs[3072 + r * 32 + ulc];
       const float cn = f_ * c[j] + i_ * g_;
       const float hn = u < P.H ? o_ * tanh_fast(cn) : 0.0f;
       c[j] = commit ? cn : c[j];
       h[j] = commit ? hn : h[j];
       store_split(ch, r, u & 63, h[j]);
     }
+    __syncwarp();
     if (role == ROLE_R) mark(21);
     bump(cidx_act(l, (32 * tile) >> 6));
   }
@@ -711,9 +770,9 @@ struct Epi {
 };
 
 __device__ __forceinline__ void Epi::run_role() {
-  const int unit = lstm ? 32 * tile + (m & 31) : 128 * tile + m;
-  const int gate = lstm ? (m >> 5) : 0;
-  if (role == ROLE_J) {
+  const int unit = lstm ? 32 * tile + (m >> 2) : 128 * tile + m;  // LSTM tiles: m = 4*unit + gate
+  const int gate = lstm ? (m & 3) : 0;
+  if (role == ROLE_J || role == ROLE_E) {
     run([&](long long) {}, [&](long long) {});
   } else if (role == ROLE_P) {
     float gp[NR], fpv[NR];
@@ -790,13 +849,13 @@ __device__ __forceinline__ void Epi::run_role() {
           if (isr0) {
             // gates0 = (table0[label] + hh0) + b   (App. B order); hh0 was
             // accumulated after the previous step (TMEM), zero for P0
+            if (p == 0) {  // P0: label blank for every row
 #pragma unroll
-            for (int i = 0; i < NR; ++i) {
-              const int r = r0 + i;
-              x[i] = (r < B && (sm.flag[r] & 2))
-                         ? __ldg(&P.table0[(size_t)sm.label[r] * P.GH + unit * P.Gg + gate])
-                         : 0.0f;
+              for (int i = 0; i < NR; ++i)
+                ih[i] = r0 + i < B ? __ldg(&P.table0[(size_t)blank * P.GH + unit * P.Gg + gate]) : 0.0f;
             }
+#pragma unroll
+            for (int i = 0; i < NR; ++i) x[i] = (sm.flag[r0 + i] & 2) ? ih[i] : 0.0f;
             if (p > 0) {
               read_acc(round - 1, v);
             } else {
@@ -855,8 +914,8 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
   const int4 rl = P.roles[blockIdx.x];
   const int role = rl.x, layer = rl.y, tile = rl.z;
   const float wsc = __int_as_float(rl.w);
-  const int in_buf = role == ROLE_J ? TRUNK : role == ROLE_P ? P.L - 1 : role == ROLE_R ? layer : layer - 1;
-  const int KC = P.act_kc[in_buf];
+  const int in_buf = (role == ROLE_J || role == ROLE_E) ? TRUNK : role == ROLE_P ? P.L - 1 : role == ROLE_R ? layer : layer - 1;
+  const int KC = role == ROLE_E ? 0 : P.act_kc[in_buf];
   Smem sm = carve(smem_raw, KC);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int B = P.B;
@@ -871,7 +930,7 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.accf[i], 1);
-      mbar_init(&sm.acce[i], 1);
+      mbar_init(&sm.acce[i], NEPI / 32);
     }
     mbar_init(sm.cmd, 1);
     mbar_init(sm.wbar, 1);

@@ -102,7 +102,7 @@ struct rnntg_decoder {
   ptc::TParams tp{};
   size_t tsmem = 0;
   unsigned* tcnt = nullptr;
-  size_t tcnt_bytes = 0;
+  size_t tcnt_bytes = 0, tpw_bytes = 0;
 };
 
 namespace {
@@ -516,6 +516,7 @@ rnntg_status setup_tc(rnntg_decoder* d) {
     if (l > 0)
       for (int t = 0; t < NG; ++t) roles.push_back(make_int4(ptc::ROLE_I, l, t, 0));
   }
+  roles.push_back(make_int4(ptc::ROLE_E, 0, 0, 0));
   const int G = (int)roles.size();
   int nsm = 0, optin = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
@@ -536,6 +537,11 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   std::vector<float> row(ptc::MAXKP);
   for (int c = 0; c < G; ++c) {
     const int role = roles[c].x, l = roles[c].y, t = roles[c].z;
+    if (role == ptc::ROLE_E) {
+      const float one = 1.0f;
+      std::memcpy(&roles[c].w, &one, 4);
+      continue;
+    }
     const int K = role == ptc::ROLE_J ? J : H;
     const int Kp = role == ptc::ROLE_J ? Jp : Hp;
     // weight element (tile row mm, k); 0 outside the model
@@ -551,8 +557,8 @@ rnntg_status setup_tc(rnntg_decoder* d) {
         const int j = 128 * t + mm;
         return j < J ? w[bse + 1][(size_t)k * J + j] : 0.0f;
       }
-      const int u = lstm ? 32 * t + (mm & 31) : 128 * t + mm;
-      const int g = lstm ? (mm >> 5) : 0;
+      const int u = lstm ? 32 * t + (mm >> 2) : 128 * t + mm;  // unit-major: row = 4*unit + gate
+      const int g = lstm ? (mm & 3) : 0;
       if (u >= H) return 0.0f;
       const std::vector<float>& W = role == ptc::ROLE_R ? w[2 + 3 * l] : w[1 + 3 * l];
       return W[(size_t)k * (lstm ? 4 * H : H) + g * H + u];
@@ -643,8 +649,9 @@ rnntg_status setup_tc(rnntg_decoder* d) {
     }
   }
   for (int l = 1; l < L; ++l) CK(d->mem.alloc(&tp.hh[l], (size_t)2 * 64 * 32 * 128));
-  CK(d->mem.alloc(&tp.part, (size_t)ptc::NSLOT * NJ * 32));
-  CK(d->mem.alloc(&tp.partd, (size_t)ptc::NSLOT * NJ * 32));
+  d->tpw_bytes = (size_t)ptc::NSLOT * 2 * NJ * 32 * sizeof(unsigned long long);
+  CK(d->mem.alloc(&tp.pw, (size_t)ptc::NSLOT * 2 * NJ * 32));
+  CK(d->mem.alloc(&tp.ps, (size_t)ptc::NSLOT * NJ * 32));
   d->tcnt_bytes = (size_t)ptc::NCOUNTERS * ptc::CSTRIDE * sizeof(unsigned);
   CK(d->mem.alloc(&d->tcnt, (size_t)ptc::NCOUNTERS * ptc::CSTRIDE));
   tp.cnt = d->tcnt;
@@ -654,7 +661,7 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   tp.durs = d->st.durs;
   tp.counts = d->st.counts;
   tp.ctrl = d->st.ctrl;
-  for (int r = 0; r < 4; ++r) tp.prof_first[r] = -1;
+  for (int r = 0; r < ptc::NROLES; ++r) tp.prof_first[r] = -1;
   for (int c = G - 1; c >= 0; --c) tp.prof_first[roles[c].x] = c;
   if (env_flag("RNNTG_PROF", false)) CK(d->mem.alloc(&tp.prof, (size_t)(ptc::NEV + G) * ptc::PROF_WIN));
   return RNNTG_OK;
@@ -663,6 +670,9 @@ rnntg_status setup_tc(rnntg_decoder* d) {
 cudaError_t launch_tc(rnntg_decoder* d, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(d->tcnt, 0, d->tcnt_bytes, st);
   if (e != cudaSuccess) return e;
+  // tagged argmax words carry step tags: clear them so a stale word from the
+  // previous decode can never validate
+  if ((e = cudaMemsetAsync(d->tp.pw, 0, d->tpw_bytes, st)) != cudaSuccess) return e;
   void* args[1] = {&d->tp};
   return cudaLaunchCooperativeKernel((const void*)ptc::ptc_kernel, dim3(d->tp.G), dim3(ptc::NTH), args,
                                      d->tsmem, st);

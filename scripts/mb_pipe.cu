@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(128, 1) k_pipe(const unsigned char* act, int r
   const uint32_t tmem = *tslot;
   long long t0 = clock64();
   if (warp == 0 && lane == 0) {
-    if (V != 2) {
+    if (V != 2 && V != 5 && V != 6) {
       long long issued = 0;
       for (int r = 0; r < rounds; ++r)
         for (int kc = 0; kc < KC; ++kc) {
@@ -102,6 +102,25 @@ __global__ void __launch_bounds__(128, 1) k_pipe(const unsigned char* act, int r
     constexpr uint32_t ID64 = idesc_f16(128, 64), ID32 = idesc_f16(128, 32);
     const uint32_t whi0 = su(whi), ring0 = su(ring);
     long long used = 0;
+    if (V == 5 || V == 6) {
+      // resident chunks: pure issue-rate test; V5 = 2 MMAs per k step, V6 = SS N64 only
+      const long long w0 = clock64();
+      for (int r = 0; r < rounds; ++r) {
+        const uint32_t d1 = tmem + (r & 1) * 96, d2 = d1 + 64;
+        for (int kc = 0; kc < KC; ++kc) {
+          const uint64_t ad = sdesc(whi0 + kc * 16384), bd = sdesc(ring0 + (kc & 3) * CHUNK);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            mma_ss(d1, ad + 2 * k, bd + 2 * k, ID64, 1);
+            if (V == 5) mma_ts(d2, tmem + 192 + kc * 32 + k * 8, bd + 2 * k, ID32, 1);
+          }
+        }
+      }
+      commit(&accb[0]);
+      mwait(&accb[0], 0);
+      const long long w1 = clock64();
+      if (lane == 0) out[blockIdx.x] = w1 - w0;
+    } else
     for (int r = 0; r < rounds; ++r) {
       const uint32_t d1 = tmem + (r & 1) * 96, d2 = d1 + 64;
       for (int kc = 0; kc < KC; ++kc) {
@@ -121,12 +140,14 @@ __global__ void __launch_bounds__(128, 1) k_pipe(const unsigned char* act, int r
         ++used;
       }
     }
-    commit(&accb[0]);
-    mwait(&accb[0], 0);
+    if (V != 5 && V != 6) {
+      commit(&accb[0]);
+      mwait(&accb[0], 0);
+    }
   }
   __syncthreads();
   long long t1 = clock64();
-  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  if (threadIdx.x == 0 && V != 5 && V != 6) out[blockIdx.x] = t1 - t0;
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
@@ -157,7 +178,8 @@ int main() {
   for (int grid : {1, 74}) {
     run<0, 4>("v0 kernel loop (fence after full wait)", act, dout, grid);
     run<1, 4>("v1 no tcgen05 fence", act, dout, grid);
-    run<2, 4>("v2 resident chunks (MMA issue only)", act, dout, grid);
+    run<5, 4>("v5 resident, 2 MMAs/k, no waits", act, dout, grid);
+    run<6, 4>("v6 resident, SS N64 only", act, dout, grid);
     run<0, 2>("v3 2-stage ring", act, dout, grid);
     run<0, 6>("v0 6-stage ring", act, dout, grid);
   }

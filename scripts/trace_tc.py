@@ -23,7 +23,7 @@ D.replay_decode(cap, x, lens)
 D.replay_decode(cap, x, lens)
 st = cap.stats()
 print("us/step", 1000 * st["gpu_ms"] / st["joint_evals"])
-G = 74
+G = 75
 buf = (C.c_uint64 * ((32 + G) * 64))()
 assert lib().rnntg_debug_trace(cap._h, buf, (32 + G) * 64) == 0, lib().rnntg_last_error()
 allev = np.array(buf, dtype=np.int64).reshape(32 + G, 64)
@@ -45,7 +45,7 @@ print("step period (J post -> next J post):", np.median(step) / 1000, "us")
 cyc = np.median((ev[26] - ev[25]).astype(np.float64)); ns = np.median((ev[3] - ev[0]).astype(np.float64))
 print("SM clock during decode: %.0f MHz" % (1000 * cyc / ns))
 pub = allev[32:].astype(np.float64) - ev[0][None, :].astype(np.float64)
-roles = ["J"] * 9 + ["P"] * 5 + ["R0"] * 20 + ["R1"] * 20 + ["I1"] * 20
+roles = ["J"] * 9 + ["P"] * 5 + ["R0"] * 20 + ["R1"] * 20 + ["I1"] * 20 + ["E"]
 for name in ["J", "R0", "I1", "R1", "P"]:
     idx = [i for i, r in enumerate(roles) if r == name]
     med = [np.median(pub[i]) / 1000 for i in idx]

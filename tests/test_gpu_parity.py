@@ -38,7 +38,7 @@ def golden():
         return json.load(fh)
 
 
-EXECS = [D.Exec.Graph, D.Exec.Persistent]
+EXECS = [D.Exec.Graph, D.Exec.Persistent, D.Exec.Tensor]
 
 
 def run_case(seed, tdt, algo, report, exec=D.Exec.Graph):
@@ -122,6 +122,8 @@ def test_lstm_golden(golden, idx, exec):
             "graph_tdt": DecodeAlgo.TdtLabelLoop}[rec["algo"]]
     if exec == D.Exec.Persistent and rec["layers"] > 2:
         pytest.skip("persistent executor supports <= 2 layers")
+    if exec == D.Exec.Tensor and rec["B"] > 32:
+        pytest.skip("tensor executor supports batch <= 32 per decoder")
     m = Model(to_model_dims(d), p)
     got = D.replay_decode(D.build_decode_graph(m, algo, rec["B"], rec["T"], rec["ms"], exec), x,
                           lens)
@@ -209,9 +211,12 @@ def test_full_size_properties(exec):
     m.close()
 
 
-def test_executors_agree_full_size():
-    """Graph and persistent executors on C2 shapes: identical token/frame
-    sequences (different FMA orders; any near-tie would show up here)."""
+@pytest.mark.parametrize("other", [D.Exec.Persistent, D.Exec.Tensor], ids=lambda e: e.name)
+@pytest.mark.parametrize("algo", [DecodeAlgo.FrameSync, DecodeAlgo.LabelLoop], ids=lambda a: a.name)
+def test_executors_agree_full_size(other, algo):
+    """Graph vs persistent / tensor-core executors on C2 shapes: identical
+    token/frame sequences (different summation orders and, for the tensor
+    executor, fp16 hi/lo tensor-core products; a near-tie would show here)."""
     _need_gpu()
     dims = ModelDims(1024, 640, 640, 640, 1024, (), "lstm", 2)
     m = Model.from_seed(dims, 1)
@@ -219,8 +224,9 @@ def test_executors_agree_full_size():
     B, T = 32, 250
     x = synth.encoder_outputs(2, B, T, 1024)
     lens = np.full(B, T, np.int32)
-    g = D.greedy_decode_sync_free(m, x, lens, 5, D.Exec.Graph)
-    p = D.greedy_decode_sync_free(m, x, lens, 5, D.Exec.Persistent)
+    run = D.greedy_decode_sync_free if algo == DecodeAlgo.FrameSync else D.label_looping_decode
+    g = run(m, x, lens, 5, D.Exec.Graph)
+    p = run(m, x, lens, 5, other)
     same = sum(a.tokens == b.tokens and a.frames == b.frames for a, b in zip(g, p))
     print(f"\nexecutors agree on {same}/{B} utterances")
     assert same == B
