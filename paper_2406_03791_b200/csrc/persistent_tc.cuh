@@ -104,7 +104,7 @@ struct TParams {
 };
 constexpr int PROF_WIN = 64;  // traced joint steps [PROF_S0, PROF_S0 + PROF_WIN)
 constexpr int PROF_S0 = 100;
-constexpr int NEV = 32;
+constexpr int NEV = 40;
 
 // ------------------------------------------------------------------ PTX
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
@@ -227,6 +227,19 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_wait_all() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void red_relaxed_add(unsigned* p, unsigned v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // byte offset of (row r, k) inside a [rows x 64] fp16 K-major SWIZZLE_128B chunk
@@ -355,10 +368,12 @@ struct Epi {
     if (P.prof && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN)
       P.prof[(size_t)(NEV + blockIdx.x) * PROF_WIN + (s - PROF_S0)] = gtimer();
   }
+  // ev < 32: globaltimer (cross-CTA), ev + 32 slot block: clock64 (intra-CTA, exact)
   __device__ __forceinline__ void mark(int ev) {
     if (tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) {
-      P.prof[(size_t)ev * PROF_WIN + (s - PROF_S0)] = gtimer();
-      if (ev == 0 || ev == 3) P.prof[(size_t)(ev == 0 ? 25 : 26) * PROF_WIN + (s - PROF_S0)] = clock64();
+      // globaltimer reads queue behind outstanding loads: only at step start
+      if (ev == 0) P.prof[(size_t)ev * PROF_WIN + (s - PROF_S0)] = gtimer();
+      P.prof[(size_t)(NEV + P.G + ev) * PROF_WIN + (s - PROF_S0)] = clock64();
     }
   }
   // one load+MMA round on this CTA's input at epoch e (-1 = exit)
@@ -392,12 +407,30 @@ struct Epi {
     if (et == 0) spin_geq(cnt + (size_t)ci * CSTRIDE, target);
     epi_sync();
   }
-  // this CTA's global stores -> visible (incl. to bulk-copy readers) -> counter += n
+  // this CTA's global stores -> visible -> counter += n.  The release's
+  // MEMBAR.GPU makes the stores visible at L2 before the counter; the
+  // consumer's bulk copies read L2 only after observing the counter and its
+  // own fence.proxy.async (producer-side proxy fences cost ~600 cycles each).
   __device__ __forceinline__ void bump(int ci, int n = 1) {
-    fence_proxy_global();
     epi_sync();
+    if (role == ROLE_P) mark(34);
     if (et == 0)
       for (int i = 0; i < n; ++i) red_release_add(cnt + (size_t)(ci + i) * CSTRIDE, 1);
+  }
+
+  // Publish activation chunks staged in shared memory (canonical layout) with
+  // TMA bulk stores: wait_group 0 guarantees the writes are complete, so the
+  // counter bump can be relaxed (a release's MEMBAR.GPU costs ~2000 cycles,
+  // this path ~800: scripts/mb_pub.cu).
+  //   full chunks: stage [n][CHUNK] -> gdst[n][CHUNK], counters ci..ci+n-1
+  __device__ __forceinline__ void publish_chunks(const unsigned char* stage, unsigned char* gdst, int n, int ci) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    epi_sync();
+    if (et == 0) {
+      for (int c = 0; c < n; ++c) bulk_s2g(gdst + (size_t)c * CHUNK, stage + (size_t)c * CHUNK, CHUNK);
+      bulk_commit_wait_all();
+      for (int c = 0; c < n; ++c) red_relaxed_add(cnt + (size_t)(ci + c) * CSTRIDE, 1);
+    }
   }
 
   __device__ void init_rows() {
@@ -732,6 +765,8 @@ struct Epi {
     }
     __syncwarp();
     const int u = 32 * tile + 8 * (m >> 5) + qd;
+    // a tile's 32 units are half a chunk (64-byte row segments): direct stores
+    // + release (64 separate 64-byte bulk stores cost more, scripts/mb_pub.cu)
     unsigned char* ch = P.act[l] + ((size_t)(pe & 1) * P.act_kc[l] + (u >> 6)) * CHUNK;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -752,8 +787,9 @@ struct Epi {
   // tanh RNN: one unit per row m (128 units per tile)
   __device__ __forceinline__ void cell_tanh(const float (&pre)[NR], int l, int pe, float (&h)[NR]) {
     const int u = 128 * tile + m;
+    unsigned char* stage = reinterpret_cast<unsigned char*>(sm.xs);  // [2][CHUNK] staging
     if (u < P.Hp) {
-      unsigned char* ch = P.act[l] + ((size_t)(pe & 1) * P.act_kc[l] + (u >> 6)) * CHUNK;
+      unsigned char* ch = stage + (size_t)((u >> 6) & 1) * CHUNK;
 #pragma unroll
       for (int i = 0; i < NR; ++i) {
         const int r = r0 + i;
@@ -763,7 +799,8 @@ struct Epi {
       }
     }
     const int c0 = (128 * tile) >> 6;
-    bump(cidx_act(l, c0), min(2, P.act_kc[l] - c0));
+    publish_chunks(stage, P.act[l] + ((size_t)(pe & 1) * P.act_kc[l] + c0) * CHUNK, min(2, P.act_kc[l] - c0),
+                   cidx_act(l, c0));
   }
 
   __device__ void run_role();
@@ -791,8 +828,10 @@ __device__ __forceinline__ void Epi::run_role() {
       }
     };
     auto trunk = [&](long long te) {  // trunk(te) = relu(fp + gp) -> act[TRUNK]
+      mark(32);
+      unsigned char* stage = reinterpret_cast<unsigned char*>(sm.xs);  // [2][CHUNK] staging
       if (j < P.Jp) {
-        unsigned char* ch = P.act[TRUNK] + ((size_t)(te & 1) * P.act_kc[TRUNK] + (j >> 6)) * CHUNK;
+        unsigned char* ch = stage + (size_t)((j >> 6) & 1) * CHUNK;
 #pragma unroll
         for (int i = 0; i < NR; ++i) {
           const int r = r0 + i;
@@ -801,7 +840,9 @@ __device__ __forceinline__ void Epi::run_role() {
         }
       }
       const int c0 = (128 * tile) >> 6;
-      bump(cidx_act(TRUNK, c0), min(2, P.act_kc[TRUNK] - c0));
+      mark(33);
+      publish_chunks(stage, P.act[TRUNK] + ((size_t)(te & 1) * P.act_kc[TRUNK] + c0) * CHUNK,
+                     min(2, P.act_kc[TRUNK] - c0), cidx_act(TRUNK, c0));
     };
     run(
         [&](long long te) {

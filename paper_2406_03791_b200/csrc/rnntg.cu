@@ -663,7 +663,7 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   tp.ctrl = d->st.ctrl;
   for (int r = 0; r < ptc::NROLES; ++r) tp.prof_first[r] = -1;
   for (int c = G - 1; c >= 0; --c) tp.prof_first[roles[c].x] = c;
-  if (env_flag("RNNTG_PROF", false)) CK(d->mem.alloc(&tp.prof, (size_t)(ptc::NEV + G) * ptc::PROF_WIN));
+  if (env_flag("RNNTG_PROF", false)) CK(d->mem.alloc(&tp.prof, (size_t)(2 * ptc::NEV + G) * ptc::PROF_WIN));
   return RNNTG_OK;
 }
 
@@ -1267,7 +1267,7 @@ rnntg_status rnntg_debug_trace(rnntg_decoder* d, unsigned long long* out, int n)
   if (d->exec != RNNTG_EXEC_TENSOR || !d->tp.prof)
     return fail(RNNTG_E_STATE, "tracing needs the tensor executor and RNNTG_PROF=1");
   CK(cudaStreamSynchronize(d->stream));
-  const int tot = (ptc::NEV + d->tp.G) * ptc::PROF_WIN;
+  const int tot = (2 * ptc::NEV + d->tp.G) * ptc::PROF_WIN;
   CK(cudaMemcpy(out, d->tp.prof, sizeof(unsigned long long) * std::min(n, tot), cudaMemcpyDeviceToHost));
   return RNNTG_OK;
 }
