@@ -62,7 +62,10 @@ typedef enum {
 typedef enum {
   RNNTG_EXEC_GRAPH = 0,       /* CUDA graph, nested conditional WHILE nodes */
   RNNTG_EXEC_PERSISTENT = 1,  /* one cooperative persistent kernel, in-kernel loops (FFMA) */
-  RNNTG_EXEC_TENSOR = 2       /* persistent kernel on tcgen05 tensor cores, role-specialised CTAs */
+  RNNTG_EXEC_TENSOR = 2,      /* persistent kernel on tcgen05 tensor cores, role-specialised CTAs */
+  RNNTG_EXEC_HOSTLOOP = 3     /* sync-requiring baseline (greedy_decode_baseline, decoders.cpp:546-563):
+                                 the graph's kernels driven by a host loop with a device->host flag
+                                 read + synchronise per step; rnntg_launch blocks until done */
 } rnntg_exec;
 
 /* RnntDims (model.hpp:31-40) + the prediction-network cell.

@@ -41,7 +41,9 @@ class CudaWeightSource {
   virtual std::vector<const float*> cuda_weights() const = 0;
 };
 
-/// Executor used by the functions below (default: persistent kernel).
+/// Executor used by the functions below (default: the tensor-core persistent
+/// kernel; shapes it does not take fall back to the FFMA persistent kernel,
+/// then to the CUDA graph).
 void set_executor(rnntg_exec exec);
 rnntg_exec executor();
 

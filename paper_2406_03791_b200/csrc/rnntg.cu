@@ -103,6 +103,8 @@ struct rnntg_decoder {
   size_t tsmem = 0;
   unsigned* tcnt = nullptr;
   size_t tcnt_bytes = 0, tpw_bytes = 0;
+  // sync-requiring host-loop baseline: pinned mirror of the control block
+  Ctrl* hctrl = nullptr;
 };
 
 namespace {
@@ -678,6 +680,67 @@ cudaError_t launch_tc(rnntg_decoder* d, cudaStream_t st) {
                                      d->tsmem, st);
 }
 
+// ---------------------------------------------------------------- host loop
+// The sync-requiring baseline (greedy_decode_baseline, decoders.cpp:546-563;
+// Algorithm 1 of the paper): the SAME kernels as the graph executor, launched
+// one by one from a host loop that copies the loop flags back and
+// synchronises after every joint step (and every frame / outer round), i.e.
+// the host round trips the conditional WHILE nodes remove.  The contrast row
+// for the GPU idle fraction; rnntg_launch returns when the decode is done.
+rnntg_status run_hostloop(rnntg_decoder* d) {
+  const DevModel& M = d->m->dm;
+  DevState s = d->st;
+  s.use_cond = 0;
+  cudaStream_t st = d->stream;
+  const int nrb = s.nrb;
+  Ctrl* hc = d->hctrl;
+  auto pred = [&]() -> cudaError_t {
+    for (int l = 0; l < M.L; ++l) {
+      if (M.cell == RNNTG_CELL_LSTM)
+        pred_layer_kernel<1><<<dim3(M.GH / CT, nrb), NT, layer_smem(M, l), st>>>(M, s, l);
+      else
+        pred_layer_kernel<0><<<dim3(M.GH / CT, nrb), NT, layer_smem(M, l), st>>>(M, s, l);
+    }
+    pred_proj_kernel<<<dim3(M.Jp / CT, nrb), NT, pp_smem(M), st>>>(M, s);
+    return cudaGetLastError();
+  };
+  auto joint = [&]() -> cudaError_t {
+    joint_kernel<<<dim3(M.NCHT, nrb), NT, joint_smem(M), st>>>(M, s);
+    return cudaGetLastError();
+  };
+  auto flags = [&]() -> cudaError_t {  // the per-step device -> host sync
+    cudaError_t e = cudaMemcpyAsync(hc, s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(st);
+  };
+  CK(encproj_launch(d->enc, st));
+  prologue_kernel<<<148, 256, 0, st>>>(M, s);
+  CK(cudaGetLastError());
+  CK(pred());  // P0 = pred(blank, 0)
+  CK(flags());
+  if (d->algo == RNNTG_ALGO_FRAME_SYNC) {
+    while (hc->t < hc->max_len && !hc->abort) {
+      do {  // inner: joint + prediction, until every row blanked or sym == ms
+        CK(joint());
+        CK(pred());
+        CK(flags());
+      } while (hc->any && !hc->abort);
+      frame_tail_kernel<<<1, 256, 0, st>>>(M, s);
+      CK(cudaGetLastError());
+      CK(flags());
+    }
+  } else {
+    while (hc->any && !hc->abort) {  // outer: any row active
+      do {  // inner: joint-only blank skipping while a row needs a decision
+        CK(joint());
+        CK(flags());
+      } while (hc->any && !hc->abort);
+      CK(pred());  // acceptors' prediction step + round tail (sets `any`)
+      CK(flags());
+    }
+  }
+  return RNNTG_OK;
+}
+
 cudaError_t build_graph(rnntg_decoder* d) {
   const bool pdl = env_flag("RNNTG_PDL", true);
   cudaError_t e;
@@ -918,7 +981,7 @@ rnntg_status rnntg_decoder_create(rnntg_model* m, int algo, int exec, int batch,
   if (algo < 0 || algo > 2) return fail(RNNTG_E_VALUE, "unknown algo");
   if (algo == RNNTG_ALGO_TDT_LABEL_LOOP && m->dm.D == 0)
     return fail(RNNTG_E_STATE, "duration-head decoding needs a model with a duration head");
-  if (exec != RNNTG_EXEC_GRAPH && exec != RNNTG_EXEC_PERSISTENT && exec != RNNTG_EXEC_TENSOR)
+  if (exec < RNNTG_EXEC_GRAPH || exec > RNNTG_EXEC_HOSTLOOP)
     return fail(RNNTG_E_VALUE, "unknown exec mode");
   CK(cudaSetDevice(m->device));
   auto* d = new rnntg_decoder;
@@ -942,6 +1005,7 @@ rnntg_status rnntg_decoder_create(rnntg_model* m, int algo, int exec, int batch,
         st = fail(RNNTG_E_CUDA, "cannot encode TMA tensor maps for the encoder projection");
       else if (exec == RNNTG_EXEC_GRAPH) e = build_graph(d);
       else if (exec == RNNTG_EXEC_TENSOR) st = setup_tc(d);
+      else if (exec == RNNTG_EXEC_HOSTLOOP) e = cudaMallocHost(&d->hctrl, sizeof(Ctrl));
       else st = setup_persistent(d);
     }
   }
@@ -963,6 +1027,7 @@ rnntg_status rnntg_decoder_destroy(rnntg_decoder* d) {
   if (d->ev0) cudaEventDestroy(d->ev0);
   if (d->ev1) cudaEventDestroy(d->ev1);
   if (d->stream) cudaStreamDestroy(d->stream);
+  if (d->hctrl) cudaFreeHost(d->hctrl);
   d->mem.release();
   delete d;
   return RNNTG_OK;
@@ -1025,6 +1090,9 @@ rnntg_status rnntg_launch(rnntg_decoder* d) {
   } else if (d->exec == RNNTG_EXEC_TENSOR) {
     CK(encproj_launch(d->enc, d->stream));
     CK(launch_tc(d, d->stream));
+  } else if (d->exec == RNNTG_EXEC_HOSTLOOP) {
+    const rnntg_status st = run_hostloop(d);
+    if (st) return st;
   } else {
     CK(cudaGraphLaunch(d->gexec, d->stream));
   }

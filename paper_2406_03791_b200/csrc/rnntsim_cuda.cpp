@@ -16,7 +16,7 @@ namespace rnntsim {
 namespace cuda {
 namespace {
 
-rnntg_exec g_exec = RNNTG_EXEC_PERSISTENT;
+rnntg_exec g_exec = RNNTG_EXEC_TENSOR;
 std::mutex g_mu;
 // Device copies keyed by model object; an entry is reused only while the
 // object at that address still exports the same weights (a new model may be
@@ -182,7 +182,12 @@ CapturedDecoder build_decode_graph(Engine& engine, const DecoderModel& model, De
   const int a = algo == DecodeAlgo::FrameSync ? RNNTG_ALGO_FRAME_SYNC
                 : algo == DecodeAlgo::LabelLoop ? RNNTG_ALGO_LABEL_LOOP
                                                 : RNNTG_ALGO_TDT_LABEL_LOOP;
-  check(rnntg_decoder_create(m, a, g_exec, batch, max_frames, max_symbols, &h->d));
+  rnntg_status st = rnntg_decoder_create(m, a, g_exec, batch, max_frames, max_symbols, &h->d);
+  if (st == RNNTG_E_VALUE && g_exec == RNNTG_EXEC_TENSOR)  // shape outside the tensor executor
+    st = rnntg_decoder_create(m, a, RNNTG_EXEC_PERSISTENT, batch, max_frames, max_symbols, &h->d);
+  if (st == RNNTG_E_VALUE && g_exec != RNNTG_EXEC_GRAPH)  // outside both persistent kernels
+    st = rnntg_decoder_create(m, a, RNNTG_EXEC_GRAPH, batch, max_frames, max_symbols, &h->d);
+  check(st);
   CapturedDecoder cap;
   cap.engine = &engine;
   cap.algo = algo;

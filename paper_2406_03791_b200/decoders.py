@@ -38,6 +38,7 @@ class Exec(enum.IntEnum):
     Graph = 0        # CUDA graph with nested conditional WHILE nodes
     Persistent = 1   # persistent kernel alternative (FFMA, shared-memory weights)
     Tensor = 2       # persistent kernel on tcgen05 tensor cores, role-specialised CTAs
+    HostLoop = 3     # sync-requiring baseline: same kernels, host loop with a flag sync per step
 
 
 @dataclass

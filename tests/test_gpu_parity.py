@@ -38,7 +38,7 @@ def golden():
         return json.load(fh)
 
 
-EXECS = [D.Exec.Graph, D.Exec.Persistent, D.Exec.Tensor]
+EXECS = [D.Exec.Graph, D.Exec.Persistent, D.Exec.Tensor, D.Exec.HostLoop]
 
 
 def run_case(seed, tdt, algo, report, exec=D.Exec.Graph):
@@ -211,7 +211,7 @@ def test_full_size_properties(exec):
     m.close()
 
 
-@pytest.mark.parametrize("other", [D.Exec.Persistent, D.Exec.Tensor], ids=lambda e: e.name)
+@pytest.mark.parametrize("other", [D.Exec.Persistent, D.Exec.Tensor, D.Exec.HostLoop], ids=lambda e: e.name)
 @pytest.mark.parametrize("algo", [DecodeAlgo.FrameSync, DecodeAlgo.LabelLoop], ids=lambda a: a.name)
 def test_executors_agree_full_size(other, algo):
     """Graph vs persistent / tensor-core executors on C2 shapes: identical
