@@ -275,6 +275,14 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent):
     t_roof = max(step_bytes / (hbm_peak * 1e3), t_flops)
     kname = {"persistent": "ptc_kernel" if tensor else "persistent_kernel"}.get(dom, dom)
     extra = {}
+    traffic = None
+    try:  # dram read+write bytes per launch from the committed ncu --set full capture
+        for e in json.load(open(os.path.join(ROOT, "profiles", "r1_ncu_tensor_summary.json"))):
+            if tensor and kname in e.get("kernel", "") and Bl == 32 and T == 250:
+                mb = lambda k: float(e[k].split()[0]) * {"Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9}[e[k].split()[1]]
+                traffic = mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")
+    except Exception:
+        traffic = None
     if tensor and dom == "persistent":
         tc_ach = 3 * flops_per[dom] / (kern[dom] / 1000.0) / 1e12
         extra["tensor"] = {"achieved_tflops": tc_ach, "peak_tflops": tc_peak, "frac": tc_ach / tc_peak,
@@ -282,7 +290,8 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent):
                                    "MEASURED_PEAKS bf16_tflops_sustained; weights resident in "
                                    "smem/TMEM, so the hbm line is the equivalent streaming rate"}
     return {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": hbm_peak, "unit": "GB/s", **extra,
-            "frac": ach / hbm_peak, "traffic": None,
+            "frac": ach / hbm_peak, "traffic": traffic,
+            "traffic_source": "profiles/r1_ncu_tensor_summary.json (ncu --set full, C2)" if traffic else None,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)",
             "algorithmic_bytes_per_launch": bytes_per[dom],
             "avg_launch_us": kern[dom] * 1000.0,
