@@ -10,7 +10,8 @@ import os
 from . import errors
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librnntg.so")
+# RNNTG_LIB selects an alternative in-tree build (A/B experiments); default the product library
+LIB_PATH = os.path.join(HERE, os.environ.get("RNNTG_LIB", "librnntg.so"))
 
 MAX_DUR = 16
 

@@ -49,7 +49,10 @@ namespace ptc {
 constexpr int NEPI = 256;        // 8 epilogue warps: two per TMEM lane quadrant, 16 rows each
 constexpr int NTH = 64 + NEPI;
 constexpr int NR = 16;           // batch rows per epilogue thread
-constexpr int NSTAGE = 4;
+#ifndef NSTAGE_CFG
+#define NSTAGE_CFG 4
+#endif
+constexpr int NSTAGE = NSTAGE_CFG;
 constexpr int MAXNJ = 16;       // joint tiles (V+1+D <= 2048)
 constexpr int CHUNK = 8192;      // [64 rows][64 k] fp16, SWIZZLE_128B
 constexpr int MAXB = 32;         // rows per decoder on this executor
@@ -64,13 +67,27 @@ constexpr int CSTRIDE = 32;      // u32 words between counters (one 128-byte lin
 
 enum Role { ROLE_J = 0, ROLE_P = 1, ROLE_R = 2, ROLE_I = 3, ROLE_E = 4 };  // E: emitter (no weights)
 constexpr int NROLES = 5;
+#ifndef WORDS_DIRECT
+#define WORDS_DIRECT 1  // A/B: direct tagged words 20.17 us/step vs bulk + counter 20.65
+#endif
+#ifndef POLL_NS
+#define POLL_NS 0
+#endif
+#ifndef LAZY_NS
+#define LAZY_NS 0  // A/B: 500 ns backoff for non-critical pollers cost 0.09 us/step
+#endif
+#ifndef SLEEP_HINT
+#define SLEEP_HINT 0  // A/B: try_wait suspend hints cost 0.10 us/step
+#endif
+constexpr int PW_STRIDE = 1;   // u64 words per argmax word slot (16 = one line per word: measured no gain)
 
 // counter word indices (times CSTRIDE)
 __host__ __device__ inline int cidx_act(int buf, int kc) { return buf * MAXKC + kc; }
 __host__ __device__ inline int cidx_hh(int l, int t) { return MAXBUF * MAXKC + l * 64 + t; }
 __host__ __device__ inline int cidx_part() { return MAXBUF * MAXKC + MAXL * 64; }
 __host__ __device__ inline int cidx_ack() { return cidx_part() + 1; }
-constexpr int NCOUNTERS = MAXBUF * MAXKC + MAXL * 64 + 2;
+__host__ __device__ inline int cidx_words(bool r0) { return cidx_part() + (r0 ? 2 : 3); }
+constexpr int NCOUNTERS = MAXBUF * MAXKC + MAXL * 64 + 4;
 
 struct TParams {
   int G, B, T, ms, cap, algo, L, cell;
@@ -90,7 +107,8 @@ struct TParams {
   int act_kc[MAXBUF];
   int nprod[MAXBUF][MAXKC];   // producers per chunk
   float* hh[MAXL];            // [2 parity][tiles][32 rows][128] (layers >= 1)
-  unsigned long long* pw;     // [NSLOT][2][NJ][32] argmax words {best f32 | idx << 8 | tag}, vocab / duration
+  unsigned long long* pw;     // [NSLOT][2][NJ][32] argmax words {best f32 | idx << 8 | tag}, vocab / duration,
+                              // one word per 128-byte line (PW_STRIDE): every CTA polls them
   float2* ps;                 // [NSLOT][NJ][32] vocab (row max, sumexp) for the emitted score
   unsigned* cnt;              // [NCOUNTERS * CSTRIDE]
   int* tokens;
@@ -104,7 +122,7 @@ struct TParams {
 };
 constexpr int PROF_WIN = 64;  // traced joint steps [PROF_S0, PROF_S0 + PROF_WIN)
 constexpr int PROF_S0 = 100;
-constexpr int NEV = 40;
+constexpr int NEV = 48;  // 40..47: globaltimer hand-off marks
 
 // ------------------------------------------------------------------ PTX
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
@@ -193,6 +211,22 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+// mbarrier wait with a suspend-time hint: the waiting warp is parked until the
+// phase completes (or the hint expires) instead of re-issuing try_wait, so idle
+// producer / MMA warps do not take issue slots from the epilogue warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+  if (!SLEEP_HINT) {
+    mbar_wait(bar, phase);
+    return;
+  }
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase), "r"(1000000u)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -222,6 +256,14 @@ __device__ __forceinline__ unsigned long long pack_arg(float v, int idx, unsigne
 }
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+#ifndef POLL_LD
+#define POLL_LD "ld.relaxed.gpu.global.u64"
+#endif
+__device__ __forceinline__ unsigned long long ld_poll_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile(POLL_LD " %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -280,7 +322,7 @@ struct Smem {
 };
 
 constexpr int XS_FLOATS = 128 * 33;   // epilogue exchange: [128 cols][33] / [4 gates][32][32]
-constexpr int RED_F4 = 512;           // column-group merge scratch: [2][8][32] float4
+constexpr int RED_F4 = 256;           // argmax merge / word staging / sumexp group scratch (4 KB)
 __host__ __device__ inline size_t smem_bytes(int KC) {
   return 1024 /*align slack*/ + (size_t)KC * 16384 + (size_t)NSTAGE * CHUNK + XS_FLOATS * 4 +
          RED_F4 * 16 + 12 * 32 * 4 + 16 * 4 + 16 * 8 + 64;
@@ -368,6 +410,17 @@ struct Epi {
     if (P.prof && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN)
       P.prof[(size_t)(NEV + blockIdx.x) * PROF_WIN + (s - PROF_S0)] = gtimer();
   }
+  // hand-off marks (globaltimer, cross-CTA): 40 P trunk published, 42 J words
+  // stored, 43 R0 words seen, 44 R0 h0 published, 46 I1 h1 published
+  __device__ __forceinline__ void gmark(int ev) {
+    if (tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN)
+      P.prof[(size_t)ev * PROF_WIN + (s - PROF_S0)] = gtimer();
+  }
+  // clock64 mark by thread et == 32 (second epilogue warp)
+  __device__ __forceinline__ void mark2(int ev) {
+    if (tracer && et == 32 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN)
+      P.prof[(size_t)(NEV + P.G + ev) * PROF_WIN + (s - PROF_S0)] = clock64();
+  }
   // ev < 32: globaltimer (cross-CTA), ev + 32 slot block: clock64 (intra-CTA, exact)
   __device__ __forceinline__ void mark(int ev) {
     if (tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) {
@@ -386,7 +439,7 @@ struct Epi {
   }
   // accumulator of round r -> v[i] = (W . A)[m][r0 + i] * 2^-s
   __device__ __forceinline__ void read_acc(int r, float (&v)[NR]) {
-    mbar_wait(&sm.accf[r & 1], (uint32_t)((r >> 1) & 1));
+    mbar_wait_sleep(&sm.accf[r & 1], (uint32_t)((r >> 1) & 1));
     tc_fence_after();
     const uint32_t a = tq + (r & 1) * ACC_COLS + r0;
     {
@@ -459,57 +512,112 @@ struct Epi {
     float v[NR];
     read_acc(round - 1, v);
     mark(1);
-    float* xs = sm.xs;  // [128 cols][33]
-#pragma unroll
-    for (int i = 0; i < NR; ++i) xs[m * 33 + r0 + i] = v[i];
     mark(16);
     // slot reuse: every CTA has finished decide(s - NSLOT); checked once per half window
     if (s >= NSLOT / 2 && s % (NSLOT / 2) == 0)
       wait_counter(cidx_ack(), (unsigned)P.G * (unsigned)(s - NSLOT / 2 + 1));
-    else
-      epi_sync();
-    // thread (row r, column group qq): columns 16qq..16qq+15 of the tile
-    const int r = et & 31, qq = et >> 5;
-    const int c0 = 128 * tile + 16 * qq;
-    float mv = -INFINITY, md = -INFINITY;
-    int iv = 0x7fffffff, id = 0x7fffffff;
-    const int V1 = P.V1, VD = P.V1 + P.D;
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      const float x = xs[(16 * qq + c) * 33 + r];
-      const int col = c0 + c;
-      const bool gv = col < V1 && x > mv;
-      mv = gv ? x : mv;
-      iv = gv ? col : iv;
-      const bool gd = col >= V1 && col < VD && x > md;
-      md = gd ? x : md;
-      id = gd ? col - V1 : id;
-    }
-    mark(17);
-    sm.red[qq * 32 + r] = make_float4(mv, 0.0f, 0.0f, __int_as_float(iv));
-    sm.red[256 + qq * 32 + r] = make_float4(md, 0.0f, 0.0f, __int_as_float(id));
-    epi_sync();
     const int slot = (int)(s % NSLOT);
     const unsigned tg = step_tag(s);
-    if (et < 64) {  // merge the 8 column groups in column order: et < 32 vocab, else durations
-      const int rr = et & 31, seg = et >> 5;
-      float bv = -INFINITY;
-      int bi = 0;
+    const int V1 = P.V1, VD = P.V1 + P.D;
+    const int lane = et & 31, q = m >> 5, hf = r0 ? 1 : 0;
+    const int col = 128 * tile + m;
+    // per-row argmax of the tile straight from registers: a warp reduce-scatter
+    // (16 rows over 32 lanes, 16 + 16 shuffles), then the 4 lane-quadrant warps
+    // of the same rows merge through smem in column order.  Ties keep the
+    // lowest column (argmax_last_into, tensor.cpp:283-289).
+    float2* rd = reinterpret_cast<float2*>(sm.red);  // [2 seg][2 half][4 q][16 rows]
+    unsigned long long* wst = reinterpret_cast<unsigned long long*>(sm.red + 128);  // [2 seg][32] word staging (after rd)
+    const bool has_dur = P.D && 128 * tile + 127 >= V1 && 128 * tile < VD;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float4 t = sm.red[seg * 256 + k * 32 + rr];
-        if (t.x > bv) {  // strict: the lowest column wins ties (argmax_last_into)
-          bv = t.x;
-          bi = __float_as_int(t.w);
+    for (int seg = 0; seg < 2; ++seg) {
+      if (seg == 1 && !has_dur) break;
+      const bool valid = seg == 0 ? col < V1 : (col >= V1 && col < VD);
+      const int cid = seg == 0 ? col : col - V1;
+      float a[NR];
+      int ai[NR];
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        a[i] = valid ? v[i] : -INFINITY;
+        ai[i] = cid;
+      }
+#pragma unroll
+      for (int st = 0; st < 4; ++st) {
+        const int o = 16 >> st, n = 8 >> st;
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          float keep = up ? a[n + i] : a[i];
+          int keepi = up ? ai[n + i] : ai[i];
+          const float send = up ? a[i] : a[n + i];
+          const int sendi = up ? ai[i] : ai[n + i];
+          const float got = __shfl_xor_sync(0xffffffffu, send, o);
+          const int goti = __shfl_xor_sync(0xffffffffu, sendi, o);
+          const bool b = got > keep || (got == keep && goti < keepi);
+          a[i] = b ? got : keep;
+          ai[i] = b ? goti : keepi;
         }
       }
-      if (seg == 0 || P.D)
-        st_relaxed_u64(&P.pw[(((size_t)slot * 2 + seg) * P.NJ + tile) * 32 + rr], pack_arg(bv, bi, tg));
-      if (seg == 0) sm.vdec[rr] = bv;  // this tile's row max, for the sumexp pass
+      {
+        const float got = __shfl_xor_sync(0xffffffffu, a[0], 1);
+        const int goti = __shfl_xor_sync(0xffffffffu, ai[0], 1);
+        const bool b = got > a[0] || (got == a[0] && goti < ai[0]);
+        a[0] = b ? got : a[0];
+        ai[0] = b ? goti : ai[0];
+      }
+      if (!(lane & 1)) {
+        const int row = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+        rd[((seg * 2 + hf) * 4 + q) * 16 + row] = make_float2(a[0], __int_as_float(ai[0]));
+      }
     }
-    mark(18);
-    mark_pub();
+    mark(17);
     epi_sync();
+    if (et < 64) {  // et < 32: vocab rows, 32..63: duration rows
+      const int seg = et >> 5, rr = et & 31, h2 = rr >> 4, row = rr & 15;
+      if (seg == 0 || has_dur) {
+        float bv = -INFINITY;
+        int bi = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 t = rd[((seg * 2 + h2) * 4 + k) * 16 + row];
+          if (t.x > bv) {  // quadrants in column order: strict > keeps the lowest column
+            bv = t.x;
+            bi = __float_as_int(t.y);
+          }
+        }
+        wst[seg * 32 + rr] = pack_arg(bv, bi, tg);
+        if (seg == 0) sm.vdec[rr] = bv;  // this tile's row max, for the sumexp pass
+
+      } else if (P.D) {  // tile without duration columns: an empty duration partial
+        wst[32 + rr] = pack_arg(-INFINITY, 0, tg);
+      }
+    }
+#if WORDS_DIRECT
+    epi_sync();
+    if (et < 64 && (et < 32 || P.D))
+      st_relaxed_u64(P.pw + (((size_t)slot * 2 + (et >> 5)) * P.NJ + tile) * 32 + (et & 31), wst[et]);
+#else
+    // publish the words like activation chunks (bulk store, wait_group, relaxed
+    // counter)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    epi_sync();
+    if (et == 0) {
+      unsigned long long* dst = P.pw + (((size_t)slot * 2) * P.NJ + tile) * 32;
+      bulk_s2g(dst, wst, 256);
+      if (P.D) bulk_s2g(dst + (size_t)P.NJ * 32, wst + 32, 256);
+      bulk_commit_wait_all();
+      red_relaxed_add(cnt + (size_t)cidx_words(true) * CSTRIDE, 1);  // polled by R_0 only
+      red_relaxed_add(cnt + (size_t)cidx_words(false) * CSTRIDE, 1);
+    }
+#endif
+    mark(18);
+    gmark(42);
+    mark_pub();
+    float* xs = sm.xs;  // [128 cols][33]
+#pragma unroll
+    for (int i = 0; i < NR; ++i) xs[m * 33 + r0 + i] = v[i];
+    epi_sync();
+    const int r = et & 31, qq = et >> 5;
+    const int c0 = 128 * tile + 16 * qq;
     // sumexp over the vocab columns relative to the tile's row max
     {
       const float M = sm.vdec[r];
@@ -533,11 +641,23 @@ struct Epi {
     mark(2);
   }
 
+  // table0[label] rows of this thread's gate row for the next layer-0 cell
+  // (issued early; consumed only in the cell, so the loads stay in flight)
+  __device__ __forceinline__ void gather_table0() {
+    const int unit = lstm ? 32 * tile + (m >> 2) : 128 * tile + m, gate = lstm ? (m & 3) : 0;
+    // unconditional loads (rows >= B carry the blank label, a valid row): a
+    // predicated load compiles to load + select and the warp stalls on it
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+      ih[i] = __ldg(&P.table0[(size_t)sm.kdec[r0 + i] * P.GH + unit * P.Gg + gate]);
+  }
+
   // ---- replicated decision of step s.  The first epilogue warp (lane = row)
   // spins on the J tiles' tagged argmax words, applies the rules and reduces
   // the row flags with ballots; ONE barrier then publishes the outcome.
   // The emitter also merges the (max, sumexp) partials for the score.
   __device__ void decide() {
+    if (role == ROLE_R && layer == 0) gmark(41);
     if (et < 32) {
       const int b = et;
       const bool valid = b < B;
@@ -547,28 +667,35 @@ struct Epi {
       int kk = blank, dd = 0;
       float best = 0.0f;
       if (valid) {
-        const unsigned long long* wv = P.pw + ((size_t)slot * 2 * P.NJ) * 32 + b;
-        const unsigned long long* wd = wv + (size_t)P.NJ * 32;
+        const unsigned long long* wv = P.pw + (((size_t)slot * 2 * P.NJ) * 32 + b) * PW_STRIDE;
+        const unsigned long long* wd = wv + (size_t)P.NJ * 32 * PW_STRIDE;
         unsigned long long a[MAXNJ], d[MAXNJ];
 #pragma unroll
         for (int t = 0; t < MAXNJ; ++t) a[t] = d[t] = 0ull;
         // every tile's word in flight at once; only R_0 consumes the decision
         // on the critical path, the other roles back off
         const bool lazy = !(role == ROLE_R && layer == 0);
+        if (!WORDS_DIRECT && b == 0) {
+          const unsigned* wc = cnt + (size_t)cidx_words(!lazy) * CSTRIDE;
+          const unsigned target = (unsigned)P.NJ * (unsigned)(s + 1);
+          while (ld_relaxed(wc) < target)
+            if (lazy) __nanosleep(500);
+        }
+        __syncwarp(0xffffffffu >> (32 - B));
         bool ok;
         do {
           ok = true;
 #pragma unroll
           for (int t = 0; t < MAXNJ; ++t)
             if (t < P.NJ) {
-              if ((unsigned)(a[t] >> 32 & 0xffu) != tg) a[t] = ld_relaxed_u64(wv + t * 32);
-              if (P.D && (unsigned)(d[t] >> 32 & 0xffu) != tg) d[t] = ld_relaxed_u64(wd + t * 32);
+              if ((unsigned)(a[t] >> 32 & 0xffu) != tg) a[t] = ld_poll_u64(wv + t * 32 * PW_STRIDE);
+              if (P.D && (unsigned)(d[t] >> 32 & 0xffu) != tg) d[t] = ld_poll_u64(wd + t * 32 * PW_STRIDE);
             }
 #pragma unroll
           for (int t = 0; t < MAXNJ; ++t)
             if (t < P.NJ)
               ok = ok && (unsigned)(a[t] >> 32 & 0xffu) == tg && (!P.D || (unsigned)(d[t] >> 32 & 0xffu) == tg);
-          if (!ok && lazy) __nanosleep(500);
+          if (!ok && lazy && LAZY_NS) __nanosleep(LAZY_NS);
         } while (!ok);
         best = -INFINITY;
         float bd = -INFINITY;
@@ -592,7 +719,14 @@ struct Epi {
         dd = P.D ? P.durations[di] : 0;
       }
       sm.kdec[b] = kk;
-      if (role == ROLE_R && layer == 0) mark(22);
+      if (role == ROLE_R && layer == 0) {
+        // hand the labels to the other 7 epilogue warps now: their table0
+        // gathers for the layer-0 cell overlap the rules below
+        __syncwarp();
+        asm volatile("barrier.cta.arrive.aligned 2, 256;" ::: "memory");
+        mark(22);
+        gmark(43);
+      }
       float v = 0.0f;
       if (emitter) {
         if (b == 0) spin_geq(cnt + (size_t)cidx_part() * CSTRIDE, (unsigned)P.NJ * (unsigned)(s + 1));
@@ -695,23 +829,21 @@ struct Epi {
       sm.flag[b] = f;
       if (b == 0) sm.misc[5] = (accany ? 1 : 0) | (fin ? 2 : 0) | (frame_end ? 4 : 0);
       if (role == ROLE_R && layer == 0) mark(24);
+    } else if (role == ROLE_R && layer == 0) {
+      asm volatile("barrier.cta.sync.aligned 2, 256;" ::: "memory");
+      mark2(35);
+      gather_table0();
+      mark2(36);
     }
     epi_sync();
+    if (role == ROLE_R && layer == 0) mark2(37);
+    if (role == ROLE_R && layer == 0 && et < 32) gather_table0();
     const int o = sm.misc[5];
     acc_any = o & 1;
     finish = (o >> 1) & 1;
     if (o & 4) ++outer_iters;
     ++joint_evals;
     if (joint_evals > P.max_iters) err = ERR_RUNAWAY;
-    if (role == ROLE_R && layer == 0 && acc_any && !finish) {
-      // the layer-0 cell needs table0[label]: gather now (lands during read_acc)
-      const int unit = lstm ? 32 * tile + (m >> 2) : 128 * tile + m, gate = lstm ? (m & 3) : 0;
-#pragma unroll
-      for (int i = 0; i < NR; ++i) {
-        const int r = r0 + i;
-        ih[i] = r < B ? __ldg(&P.table0[(size_t)sm.kdec[r] * P.GH + unit * P.Gg + gate]) : 0.0f;
-      }
-    }
     mark(role == ROLE_J ? 3 : role == ROLE_R ? (layer == 0 ? 4 : 10) : role == ROLE_I ? 6 : role == ROLE_E ? 15 : 8);
   }
 
@@ -821,10 +953,12 @@ __device__ __forceinline__ void Epi::run_role() {
       const int tfs = sm.misc[2];
 #pragma unroll
       for (int i = 0; i < NR; ++i) {
-        const int r = r0 + i;
+        // unconditional (clamped) loads so the warp does not stall here; rows
+        // >= B / columns >= J are masked where the values are used
+        const int r = min(r0 + i, B - 1);
         int t = fs ? tfs : sm.tb[r];
         t = t < 0 ? 0 : (t > P.T - 1 ? P.T - 1 : t);
-        fpv[i] = (r < B && j < P.J) ? __ldg(&P.fp[((size_t)r * P.T + t) * P.Jp + j]) : 0.0f;
+        fpv[i] = __ldg(&P.fp[((size_t)r * P.T + t) * P.Jp + min(j, P.Jp - 1)]);
       }
     };
     auto trunk = [&](long long te) {  // trunk(te) = relu(fp + gp) -> act[TRUNK]
@@ -843,6 +977,7 @@ __device__ __forceinline__ void Epi::run_role() {
       mark(33);
       publish_chunks(stage, P.act[TRUNK] + ((size_t)(te & 1) * P.act_kc[TRUNK] + c0) * CHUNK,
                      min(2, P.act_kc[TRUNK] - c0), cidx_act(TRUNK, c0));
+      gmark(40);
     };
     run(
         [&](long long te) {
@@ -925,6 +1060,7 @@ __device__ __forceinline__ void Epi::run_role() {
           if (lstm) cell_lstm(v, layer, p, c4, h4);
           else cell_tanh(v, layer, p, hr);
           mark_pub();
+          gmark(isr0 ? 44 : 46);
           if (isr0) {
             mark(5);
             post(p);  // hh0(p+1) = h0(p) @ W_hh0 into the other accumulator
@@ -1015,10 +1151,12 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
   if (warp == 0) {
     // ================= producer: stream input chunks into the ring =================
     if (lane == 0) {
-      long long issued = 0;
+      // ring stage, the empty-barrier parity of its previous use (a stage's k-th
+      // reuse waits for parity (k - 1) & 1), stages filled once
+      int ps = 0, pph = 1, pfill = 0;
       const unsigned* cb = P.cnt + (size_t)cidx_act(in_buf, 0) * CSTRIDE;
       for (int r = 0;; ++r) {
-        mbar_wait(sm.cmd, r & 1);
+        mbar_wait_sleep(sm.cmd, r & 1);
         const int e = ((volatile int*)sm.misc)[r & 1];
         if (e < 0) break;
         const unsigned char* src = P.act[in_buf] + (size_t)(e & 1) * KC * CHUNK;
@@ -1035,15 +1173,25 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
 #pragma unroll
           for (int kc = 0; kc < MAXKC; ++kc)
             if (kc == ready && kc < KC && v[kc] >= (unsigned)P.nprod[in_buf][kc] * (unsigned)(e + 1)) ++ready;
-          if (ready == next) continue;
+          if (ready == next) {
+            if (POLL_NS) __nanosleep(POLL_NS);
+            continue;
+          }
           fence_proxy_global();
           for (int kc = next; kc < ready; ++kc) {
             if (tr && (kc == 0 || kc == KC - 1)) P.prof[(size_t)(kc ? 13 : 12) * PROF_WIN + (e - PROF_S0)] = gtimer();
-            const int s = (int)(issued % NSTAGE);
-            if (issued >= NSTAGE) mbar_wait(&sm.empty[s], (uint32_t)(((issued / NSTAGE) - 1) & 1));
+            if (kc == 0 && P.prof && (role == ROLE_I || role == ROLE_P) && (int)blockIdx.x == P.prof_first[role] &&
+                e >= 1 && e < 1 + 4 * PROF_WIN)
+              P.prof[(size_t)(role == ROLE_I ? 45 : 47) * PROF_WIN + ((e - 1) % PROF_WIN)] = gtimer();
+            const int s = ps;
+            if (pfill >= NSTAGE) mbar_wait_sleep(&sm.empty[s], (uint32_t)pph);
             mbar_arrive_expect_tx(&sm.full[s], CHUNK);
             bulk_g2s(sm.ring + s * CHUNK, src + (size_t)kc * CHUNK, CHUNK, &sm.full[s]);
-            ++issued;
+            if (pfill < NSTAGE) ++pfill;
+            if (++ps == NSTAGE) {
+              ps = 0;
+              pph ^= 1;
+            }
           }
           next = ready;
         }
@@ -1051,22 +1199,22 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
     }
   } else if (warp == 1) {
     // ================= MMA issuer (converged warp) =================
-    long long used = 0;
+    int cs = 0, cph = 0;  // ring stage consumed next, its full-barrier phase
     constexpr uint32_t ID64 = idesc_f16(128, 64), ID32 = idesc_f16(128, 32);
     const uint32_t whi0 = smem_u32(sm.whi), ring0 = smem_u32(sm.ring);
     for (int r = 0;; ++r) {
-      mbar_wait(sm.cmd, r & 1);
+      mbar_wait_sleep(sm.cmd, r & 1);
       const int e = ((volatile int*)sm.misc)[r & 1];
       if (e < 0) break;
       const int set = r & 1;
-      if (r >= 2) mbar_wait(&sm.acce[set], (uint32_t)(((r >> 1) - 1) & 1));
+      if (r >= 2) mbar_wait_sleep(&sm.acce[set], (uint32_t)(((r >> 1) - 1) & 1));
       tc_fence_after();
       const uint32_t d1 = tmem + set * ACC_COLS, d2 = d1 + 64;
       const bool tr = P.prof && role == ROLE_J && (int)blockIdx.x == P.prof_first[role] && e >= PROF_S0 &&
                       e < PROF_S0 + PROF_WIN && lane == 0;
       for (int kc = 0; kc < KC; ++kc) {
-        const int s = (int)(used % NSTAGE);
-        mbar_wait(&sm.full[s], (uint32_t)((used / NSTAGE) & 1));
+        const int s = cs;
+        mbar_wait_sleep(&sm.full[s], (uint32_t)cph);
         if (tr && (kc == 0 || kc == KC - 1)) P.prof[(size_t)(kc ? 28 : 27) * PROF_WIN + (e - PROF_S0)] = gtimer();
         tc_fence_after();
         const uint64_t ad = sdesc_sw128(whi0 + kc * 16384), bd = sdesc_sw128(ring0 + s * CHUNK);
@@ -1077,7 +1225,10 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
           mma_ts(d2, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID32, acc);
         }
         mma_commit(&sm.empty[s]);
-        ++used;
+        if (++cs == NSTAGE) {
+          cs = 0;
+          cph ^= 1;
+        }
       }
       mma_commit(&sm.accf[set]);
       if (tr) P.prof[(size_t)29 * PROF_WIN + (e - PROF_S0)] = gtimer();

@@ -651,8 +651,8 @@ rnntg_status setup_tc(rnntg_decoder* d) {
     }
   }
   for (int l = 1; l < L; ++l) CK(d->mem.alloc(&tp.hh[l], (size_t)2 * 64 * 32 * 128));
-  d->tpw_bytes = (size_t)ptc::NSLOT * 2 * NJ * 32 * sizeof(unsigned long long);
-  CK(d->mem.alloc(&tp.pw, (size_t)ptc::NSLOT * 2 * NJ * 32));
+  d->tpw_bytes = (size_t)ptc::NSLOT * 2 * NJ * 32 * ptc::PW_STRIDE * sizeof(unsigned long long);
+  CK(d->mem.alloc(&tp.pw, (size_t)ptc::NSLOT * 2 * NJ * 32 * ptc::PW_STRIDE));
   CK(d->mem.alloc(&tp.ps, (size_t)ptc::NSLOT * NJ * 32));
   d->tcnt_bytes = (size_t)ptc::NCOUNTERS * ptc::CSTRIDE * sizeof(unsigned);
   CK(d->mem.alloc(&d->tcnt, (size_t)ptc::NCOUNTERS * ptc::CSTRIDE));

@@ -24,11 +24,11 @@ D.replay_decode(cap, x, lens)
 st = cap.stats()
 print("us/step", 1000 * st["gpu_ms"] / st["joint_evals"])
 G = 75
-buf = (C.c_uint64 * ((80 + G) * 64))()
-assert lib().rnntg_debug_trace(cap._h, buf, (80 + G) * 64) == 0, lib().rnntg_last_error()
-allev = np.array(buf, dtype=np.int64).reshape(80 + G, 64)
-cyca = allev[40 + G:]
-ev = allev[:40]
+buf = (C.c_uint64 * ((96 + G) * 64))()
+assert lib().rnntg_debug_trace(cap._h, buf, (96 + G) * 64) == 0, lib().rnntg_last_error()
+allev = np.array(buf, dtype=np.int64).reshape(96 + G, 64)
+cyca = allev[48 + G:]
+ev = allev[:48]
 names = {0: "J post", 12: "J chunk0 ready", 13: "J chunk9 ready", 1: "J acc ready", 2: "J part pub",
          3: "J decide done", 4: "R0 decide done", 5: "R0 h0 pub", 6: "I1 decide done", 7: "I1 acc ready",
          11: "I1 h1 pub", 10: "R1 decide done", 8: "P decide done", 9: "P acc ready", 14: "P trunk pub",
@@ -45,7 +45,7 @@ step = np.diff(ev[0].astype(np.float64))
 print("step period (J post -> next J post):", np.median(step) / 1000, "us")
 cyc = np.median((ev[26] - ev[25]).astype(np.float64)); ns = np.median((ev[3] - ev[0]).astype(np.float64))
 print("SM clock during decode: %.0f MHz" % (1000 * cyc / ns))
-pub = allev[40:40 + G].astype(np.float64) - ev[0][None, :].astype(np.float64)
+pub = allev[48:48 + G].astype(np.float64) - ev[0][None, :].astype(np.float64)
 roles = ["J"] * 9 + ["P"] * 5 + ["R0"] * 20 + ["R1"] * 20 + ["I1"] * 20 + ["E"]
 for name in ["J", "R0", "I1", "R1", "P"]:
     idx = [i for i, r in enumerate(roles) if r == name]
@@ -57,9 +57,15 @@ def iv(a, b, name):
     d = (cyca[b] - cyca[a]).astype(np.float64)
     ok = (cyca[a] > 0) & (cyca[b] > 0)
     if ok.any(): print(f"  {name:34s} {np.median(d[ok]):8.0f} cyc")
-iv(1, 16, "J acc -> xs written"); iv(16, 17, "J xs -> scan done"); iv(17, 18, "J scan -> words stored")
+iv(1, 16, "J acc -> xs written"); iv(16, 17, "J acc -> shuffle argmax done"); iv(17, 18, "J merge -> words stored")
 iv(18, 2, "J words -> sumexp published"); iv(2, 3, "J sumexp pub -> decide done")
 iv(22, 24, "R0 words seen -> rules done"); iv(24, 4, "R0 rules -> decide done"); iv(4, 19, "R0 decide -> pre ready")
 iv(19, 21, "R0 pre -> h stored"); iv(21, 5, "R0 h stored -> h0 published")
 iv(23, 24, "R0 (unused)"); iv(6, 7, "I1 decide -> acc ready"); iv(7, 11, "I1 acc -> h1 published"); iv(8, 9, "P decide -> acc ready"); iv(9, 14, "P acc -> trunk published")
 iv(9, 32, "P acc -> trunk start"); iv(32, 33, "P trunk compute+stores"); iv(33, 34, "P bump epi_sync"); iv(34, 14, "P release + mark")
+
+print("hand-offs (globaltimer medians relative to J post of the step, us):")
+for e, nm in [(40, "P trunk published (prev step)"), (12, "J chunk0 seen"), (41, "R0 decide entered"), (42, "J words stored"), (43, "R0 words seen"), (44, "R0 h0 published"), (46, "I1 h1 published")]:
+    d = (ev[e] - ev[0]).astype(np.float64); ok = ev[e] > 0
+    if ok.any(): print(f"  {nm:32s} {np.median(d[ok]) / 1000:8.2f}")
+iv(22, 35, "R0 words seen(w0) -> w1 released"); iv(35, 36, "R0 w1 gather issue"); iv(36, 37, "R0 w1 gather -> epi_sync out"); iv(24, 37, "R0 w0 rules done -> epi_sync out (w1)")
