@@ -73,6 +73,12 @@ constexpr int NROLES = 5;
 #ifndef POLL_NS
 #define POLL_NS 0
 #endif
+#ifndef TMA_ACT
+#define TMA_ACT 1  // activations via 2-D tensor maps (plain row-major in global, swizzled by TMA)
+#endif
+#ifndef ARGMAX_REDUX
+#define ARGMAX_REDUX 0
+#endif
 #ifndef LAZY_NS
 #define LAZY_NS 0  // A/B: 500 ns backoff for non-critical pollers cost 0.09 us/step
 #endif
@@ -90,6 +96,12 @@ __host__ __device__ inline int cidx_words(bool r0) { return cidx_part() + (r0 ? 
 constexpr int NCOUNTERS = MAXBUF * MAXKC + MAXL * 64 + 4;
 
 struct TParams {
+  // TMA_ACT: activation buffer b is a 2-D fp16 tensor [2 parity x 64 rows][Kp]
+  // (row-major); ldmap: box 64 x 64, SWIZZLE_128B (lands in UMMA canonical
+  // layout); stmap: the producers' box (32 x 64 plain for LSTM tiles, 64 x 64
+  // SWIZZLE_128B from canonical staging otherwise)
+  CUtensorMap ldmap[MAXBUF];
+  CUtensorMap stmap[MAXBUF];
   int G, B, T, ms, cap, algo, L, cell;
   int H, Hp, J, Jp, V1, D;
   int NJ;                     // joint tiles
@@ -274,6 +286,18 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 __device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
                "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_ld2(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_st2(const CUtensorMap* map, int x, int y, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(x),
+               "r"(y), "r"(smem_u32(src))
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit_wait_all() {
@@ -476,11 +500,17 @@ struct Epi {
   // counter bump can be relaxed (a release's MEMBAR.GPU costs ~2000 cycles,
   // this path ~800: scripts/mb_pub.cu).
   //   full chunks: stage [n][CHUNK] -> gdst[n][CHUNK], counters ci..ci+n-1
-  __device__ __forceinline__ void publish_chunks(const unsigned char* stage, unsigned char* gdst, int n, int ci) {
+  __device__ __forceinline__ void publish_chunks(const unsigned char* stage, unsigned char* gdst, int n, int ci,
+                                                 int buf, int kc0, int par) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     epi_sync();
     if (et == 0) {
+#if TMA_ACT
+      for (int c = 0; c < n; ++c) tma_st2(&P.stmap[buf], 64 * (kc0 + c), 64 * par, stage + (size_t)c * CHUNK);
+      (void)gdst;
+#else
       for (int c = 0; c < n; ++c) bulk_s2g(gdst + (size_t)c * CHUNK, stage + (size_t)c * CHUNK, CHUNK);
+#endif
       bulk_commit_wait_all();
       for (int c = 0; c < n; ++c) red_relaxed_add(cnt + (size_t)(ci + c) * CSTRIDE, 1);
     }
@@ -533,6 +563,24 @@ struct Epi {
       if (seg == 1 && !has_dur) break;
       const bool valid = seg == 0 ? col < V1 : (col >= V1 && col < VD);
       const int cid = seg == 0 ? col : col - V1;
+#if ARGMAX_REDUX
+      // per row: warp max of an order-preserving key of the value, then the
+      // lowest column among the lanes holding it (two redux.sync per row)
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        unsigned u = __float_as_uint(valid ? v[i] : -INFINITY);
+        u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+        unsigned mk, mi;
+        asm volatile("redux.sync.max.u32 %0, %1, 0xffffffff;" : "=r"(mk) : "r"(u));
+        const unsigned cand = u == mk ? (unsigned)cid : 0xffffffffu;
+        asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(mi) : "r"(cand));
+        if (lane == i) {
+          const unsigned fb = (mk & 0x80000000u) ? (mk & 0x7fffffffu) : ~mk;
+          rd[((seg * 2 + hf) * 4 + q) * 16 + i] = make_float2(__uint_as_float(fb), __int_as_float((int)mi));
+        }
+      }
+    }
+#else
       float a[NR];
       int ai[NR];
 #pragma unroll
@@ -569,6 +617,7 @@ struct Epi {
         rd[((seg * 2 + hf) * 4 + q) * 16 + row] = make_float2(a[0], __int_as_float(ai[0]));
       }
     }
+#endif
     mark(17);
     epi_sync();
     if (et < 64) {  // et < 32: vocab rows, 32..63: duration rows
@@ -897,9 +946,15 @@ struct Epi {
     }
     __syncwarp();
     const int u = 32 * tile + 8 * (m >> 5) + qd;
+#if TMA_ACT
+    // a tile's 32 units: one 32 x 64 box, staged plain [64 rows][32] fp16
+    __half* st16 = reinterpret_cast<__half*>(sm.red);
+    const int ul = u - 32 * tile;
+#else
     // a tile's 32 units are half a chunk (64-byte row segments): direct stores
     // + release (64 separate 64-byte bulk stores cost more, scripts/mb_pub.cu)
     unsigned char* ch = P.act[l] + ((size_t)(pe & 1) * P.act_kc[l] + (u >> 6)) * CHUNK;
+#endif
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int i = 4 * j + g, r = r0 + i;
@@ -910,11 +965,27 @@ struct Epi {
       const float hn = u < P.H ? o_ * tanh_fast(cn) : 0.0f;
       c[j] = commit ? cn : c[j];
       h[j] = commit ? hn : h[j];
+#if TMA_ACT
+      const __half hh = __float2half_rn(h[j]);
+      st16[r * 32 + ul] = hh;
+      st16[(32 + r) * 32 + ul] = __float2half_rn(h[j] - __half2float(hh));
+#else
       store_split(ch, r, u & 63, h[j]);
+#endif
     }
     __syncwarp();
     if (role == ROLE_R) mark(21);
+#if TMA_ACT
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    epi_sync();
+    if (et == 0) {
+      tma_st2(&P.stmap[l], 32 * tile, 64 * (pe & 1), st16);
+      bulk_commit_wait_all();
+      red_relaxed_add(cnt + (size_t)cidx_act(l, (32 * tile) >> 6) * CSTRIDE, 1);
+    }
+#else
     bump(cidx_act(l, (32 * tile) >> 6));
+#endif
   }
   // tanh RNN: one unit per row m (128 units per tile)
   __device__ __forceinline__ void cell_tanh(const float (&pre)[NR], int l, int pe, float (&h)[NR]) {
@@ -932,7 +1003,7 @@ struct Epi {
     }
     const int c0 = (128 * tile) >> 6;
     publish_chunks(stage, P.act[l] + ((size_t)(pe & 1) * P.act_kc[l] + c0) * CHUNK, min(2, P.act_kc[l] - c0),
-                   cidx_act(l, c0));
+                   cidx_act(l, c0), l, c0, pe & 1);
   }
 
   __device__ void run_role();
@@ -976,7 +1047,7 @@ __device__ __forceinline__ void Epi::run_role() {
       const int c0 = (128 * tile) >> 6;
       mark(33);
       publish_chunks(stage, P.act[TRUNK] + ((size_t)(te & 1) * P.act_kc[TRUNK] + c0) * CHUNK,
-                     min(2, P.act_kc[TRUNK] - c0), cidx_act(TRUNK, c0));
+                     min(2, P.act_kc[TRUNK] - c0), cidx_act(TRUNK, c0), TRUNK, c0, (int)(te & 1));
       gmark(40);
     };
     run(
@@ -1186,7 +1257,12 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
             const int s = ps;
             if (pfill >= NSTAGE) mbar_wait_sleep(&sm.empty[s], (uint32_t)pph);
             mbar_arrive_expect_tx(&sm.full[s], CHUNK);
+#if TMA_ACT
+            tma_ld2(sm.ring + s * CHUNK, &P.ldmap[in_buf], 64 * kc, 64 * (e & 1), &sm.full[s]);
+            (void)src;
+#else
             bulk_g2s(sm.ring + s * CHUNK, src + (size_t)kc * CHUNK, CHUNK, &sm.full[s]);
+#endif
             if (pfill < NSTAGE) ++pfill;
             if (++ps == NSTAGE) {
               ps = 0;

@@ -650,6 +650,29 @@ rnntg_status setup_tc(rnntg_decoder* d) {
       }
     }
   }
+  // activation tensor maps: [2 parity x 64 rows][Kp] fp16, row-major
+  {
+    PFN_encodeTiled enc = get_encode_tiled();
+    if (!enc) return fail(RNNTG_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    for (int b = 0; b <= ptc::TRUNK; ++b) {
+      if (!(b < L || b == ptc::TRUNK)) continue;
+      const int Kp = tp.act_kc[b] * 64;
+      const cuuint64_t dims[2] = {(cuuint64_t)Kp, 128};
+      const cuuint64_t strides[1] = {(cuuint64_t)Kp * 2};
+      const cuuint32_t estr[2] = {1, 1};
+      const cuuint32_t lbox[2] = {64, 64};
+      if (enc(&tp.ldmap[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, tp.act[b], dims, strides, lbox, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return fail(RNNTG_E_CUDA, "activation load tensor map");
+      const bool half_tiles = lstm && b < L;  // LSTM tiles publish 32-unit boxes
+      const cuuint32_t sbox[2] = {half_tiles ? 32u : 64u, 64};
+      if (enc(&tp.stmap[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, tp.act[b], dims, strides, sbox, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, half_tiles ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return fail(RNNTG_E_CUDA, "activation store tensor map");
+    }
+  }
   for (int l = 1; l < L; ++l) CK(d->mem.alloc(&tp.hh[l], (size_t)2 * 64 * 32 * 128));
   d->tpw_bytes = (size_t)ptc::NSLOT * 2 * NJ * 32 * ptc::PW_STRIDE * sizeof(unsigned long long);
   CK(d->mem.alloc(&tp.pw, (size_t)ptc::NSLOT * 2 * NJ * 32 * ptc::PW_STRIDE));
