@@ -60,7 +60,10 @@ constexpr int MAXKP = 640;       // K <= 640: W_lo (K/2 TMEM columns) + 2 x 96 a
 constexpr int MAXKC = MAXKP / 64;
 constexpr int TRUNK = MAXL;      // activation buffer ids: h_0..h_{L-1}, trunk
 constexpr int MAXBUF = MAXL + 1;
-constexpr int NSLOT = 32;        // joint-partial ring depth (ack checked every NSLOT/2 steps)
+#ifndef NSLOT_CFG
+#define NSLOT_CFG 8  // A/B: 8 vs 32 slots -0.03 us/step
+#endif
+constexpr int NSLOT = NSLOT_CFG;  // joint-partial ring depth (ack checked every NSLOT/2 steps)
 constexpr int ACC_COLS = 96;
 constexpr int WLO_COL = 2 * ACC_COLS;
 constexpr int CSTRIDE = 32;      // u32 words between counters (one 128-byte line each)
@@ -72,6 +75,21 @@ constexpr int NROLES = 5;
 #endif
 #ifndef POLL_NS
 #define POLL_NS 0
+#endif
+#ifndef ECHO_GATE
+#define ECHO_GATE 0  // A/B: gating 55 pollers behind an R_0 echo cost 0.3 us/step
+#endif
+#ifndef WORD_READBACK
+#define WORD_READBACK 0  // A/B: no gain
+#endif
+#ifndef WORDS_ONE_LANE
+#define WORDS_ONE_LANE 0
+#endif
+#ifndef ACK_RELAXED
+#define ACK_RELAXED 1
+#endif
+#ifndef SPIN_ONE
+#define SPIN_ONE 0
 #endif
 #ifndef TMA_ACT
 #define TMA_ACT 1  // activations via 2-D tensor maps (plain row-major in global, swizzled by TMA)
@@ -93,7 +111,7 @@ __host__ __device__ inline int cidx_hh(int l, int t) { return MAXBUF * MAXKC + l
 __host__ __device__ inline int cidx_part() { return MAXBUF * MAXKC + MAXL * 64; }
 __host__ __device__ inline int cidx_ack() { return cidx_part() + 1; }
 __host__ __device__ inline int cidx_words(bool r0) { return cidx_part() + (r0 ? 2 : 3); }
-constexpr int NCOUNTERS = MAXBUF * MAXKC + MAXL * 64 + 4;
+constexpr int NCOUNTERS = MAXBUF * MAXKC + MAXL * 64 + 5;  // last: ECHO_GATE decided word
 
 struct TParams {
   // TMA_ACT: activation buffer b is a 2-D fp16 tensor [2 parity x 64 rows][Kp]
@@ -130,6 +148,8 @@ struct TParams {
   int* counts;
   Ctrl* ctrl;
   unsigned long long* prof;   // optional event trace [NEV][PROF_WIN] (first CTA of each role)
+  unsigned long long* echo;   // optional: R_0 tile 0 echoes the step it decided (round-trip probe)
+  unsigned* decided;          // ECHO_GATE: steps R_0 tile 0 has seen the J words of
   int prof_first[NROLES];     // first CTA index per role (tracing CTAs)
 };
 constexpr int PROF_WIN = 64;  // traced joint steps [PROF_S0, PROF_S0 + PROF_WIN)
@@ -642,8 +662,32 @@ struct Epi {
     }
 #if WORDS_DIRECT
     epi_sync();
-    if (et < 64 && (et < 32 || P.D))
-      st_relaxed_u64(P.pw + (((size_t)slot * 2 + (et >> 5)) * P.NJ + tile) * 32 + (et & 31), wst[et]);
+#if WORDS_ONE_LANE
+    if (et == 0)
+      for (int i = 0; i < (P.D ? 64 : 32); ++i)
+        st_relaxed_u64(P.pw + (((size_t)slot * 2 + (i >> 5)) * P.NJ + tile) * 32 + (i & 31), wst[i]);
+    if (false) {
+#else
+    if (et < 64 && (et < 32 || P.D)) {
+#endif
+      unsigned long long* wp = P.pw + (((size_t)slot * 2 + (et >> 5)) * P.NJ + tile) * 32 + (et & 31);
+      st_relaxed_u64(wp, wst[et]);
+#if WORD_READBACK
+      // read the word back: measured to push the line out (a warp-wide strong
+      // store with no memory traffic after it took ~2 us to become visible)
+      volatile unsigned long long rb = ld_poll_u64(wp);
+      (void)rb;
+#endif
+    }
+    if (P.echo && tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) {
+      // exact J -> R_0 -> J round trip on this SM's clock: J bumps a probe word,
+      // R_0 tile 0 (spinning on it) echoes the step
+      const long long c0 = clock64();
+      st_relaxed_u64(P.echo + 8, (unsigned long long)(s + 1));
+      while (ld_poll_u64(P.echo) != (unsigned long long)(s + 1)) {
+      }
+      P.prof[(size_t)37 * PROF_WIN + (s - PROF_S0)] = clock64() - c0;
+    }
 #else
     // publish the words like activation chunks (bulk store, wait_group, relaxed
     // counter)
@@ -707,13 +751,19 @@ struct Epi {
   // The emitter also merges the (max, sumexp) partials for the score.
   __device__ void decide() {
     if (role == ROLE_R && layer == 0) gmark(41);
+    if (P.echo && role == ROLE_R && layer == 0 && tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) {
+      while (ld_poll_u64(P.echo + 8) != (unsigned long long)(s + 1)) {
+      }
+      st_relaxed_u64(P.echo, (unsigned long long)(s + 1));
+    }
     if (et < 32) {
       const int b = et;
       const bool valid = b < B;
       const int slot = (int)(s % NSLOT);
       const unsigned tg = step_tag(s);
       const bool emitter = role == ROLE_E;
-      int kk = blank, dd = 0;
+      int kk = blank, dd = 0, npoll_out = 0;
+      long long lat1_out = 0;
       float best = 0.0f;
       if (valid) {
         const unsigned long long* wv = P.pw + (((size_t)slot * 2 * P.NJ) * 32 + b) * PW_STRIDE;
@@ -724,6 +774,18 @@ struct Epi {
         // every tile's word in flight at once; only R_0 consumes the decision
         // on the critical path, the other roles back off
         const bool lazy = !(role == ROLE_R && layer == 0);
+#if ECHO_GATE
+        // only R_0 (the critical consumer) polls the J words; the other roles
+        // wait for R_0 tile 0's echo of the step (a word that 55 CTAs poll),
+        // then read the words once: 75 CTAs polling the word lines for ~15 us
+        // before they are written delayed the writes by ~2 us
+        if (lazy) {
+          if (b == 0)
+            while (ld_relaxed(P.decided) < (unsigned)(s + 1)) {
+            }
+          __syncwarp(0xffffffffu >> (32 - B));
+        }
+#endif
         if (!WORDS_DIRECT && b == 0) {
           const unsigned* wc = cnt + (size_t)cidx_words(!lazy) * CSTRIDE;
           const unsigned target = (unsigned)P.NJ * (unsigned)(s + 1);
@@ -732,20 +794,47 @@ struct Epi {
         }
         __syncwarp(0xffffffffu >> (32 - B));
         bool ok;
+        const int nj = P.NJ;
+        int npoll = 0;
+        long long lat1 = 0;
+        if (tracer && role == ROLE_R && layer == 0 && b == 0) {  // one strong load, timed
+          const long long c0 = clock64();
+          const unsigned long long w0 = ld_poll_u64(wv);
+          long long c1 = 0;
+          if (w0 != 0x123456789abcdefull) c1 = clock64();  // the branch waits for the load
+          lat1 = c1 - c0;
+        }
+#if SPIN_ONE
+        // spin on one word (tile NJ-1, written last in column order by no one in
+        // particular) with a single load in flight, then read the rest once
+        while ((unsigned)(ld_poll_u64(wv + (nj - 1) * 32 * PW_STRIDE) >> 32 & 0xffu) != tg) ++npoll;
+#endif
         do {
+          ++npoll;
           ok = true;
+          // branch-free: every slot loads (clamped to a valid tile), so all
+          // loads are in flight together; a branch per load serialised them
+          // (one ~300-cycle round trip each, ~2000 cycles per poll)
 #pragma unroll
-          for (int t = 0; t < MAXNJ; ++t)
-            if (t < P.NJ) {
-              if ((unsigned)(a[t] >> 32 & 0xffu) != tg) a[t] = ld_poll_u64(wv + t * 32 * PW_STRIDE);
-              if (P.D && (unsigned)(d[t] >> 32 & 0xffu) != tg) d[t] = ld_poll_u64(wd + t * 32 * PW_STRIDE);
+          for (int t = 0; t < MAXNJ; ++t) {
+            const int tt = t < nj ? t : nj - 1;
+            a[t] = ld_poll_u64(wv + tt * 32 * PW_STRIDE);
+          }
+          if (P.D) {
+#pragma unroll
+            for (int t = 0; t < MAXNJ; ++t) {
+              const int tt = t < nj ? t : nj - 1;
+              d[t] = ld_poll_u64(wd + tt * 32 * PW_STRIDE);
             }
+          }
 #pragma unroll
           for (int t = 0; t < MAXNJ; ++t)
             if (t < P.NJ)
               ok = ok && (unsigned)(a[t] >> 32 & 0xffu) == tg && (!P.D || (unsigned)(d[t] >> 32 & 0xffu) == tg);
           if (!ok && lazy && LAZY_NS) __nanosleep(LAZY_NS);
         } while (!ok);
+        npoll_out = npoll;
+        lat1_out = lat1;
         best = -INFINITY;
         float bd = -INFINITY;
         int di = 0;
@@ -768,6 +857,14 @@ struct Epi {
         dd = P.D ? P.durations[di] : 0;
       }
       sm.kdec[b] = kk;
+#if ECHO_GATE
+      if (role == ROLE_R && layer == 0 && tile == 0 && b == 0)
+        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(P.decided), "r"((unsigned)(s + 1)) : "memory");
+#endif
+
+      if (role == ROLE_R && layer == 0 && tracer && b == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN)
+        P.prof[(size_t)39 * PROF_WIN + (s - PROF_S0)] = (unsigned long long)npoll_out,
+        P.prof[(size_t)38 * PROF_WIN + (s - PROF_S0)] = (unsigned long long)lat1_out;
       if (role == ROLE_R && layer == 0) {
         // hand the labels to the other 7 epilogue warps now: their table0
         // gathers for the layer-0 cell overlap the rules below
@@ -920,8 +1017,14 @@ struct Epi {
       } else {
         idle(s + 1);
       }
-      // this CTA is done with step s's words: ack (slot reuse, joint_round)
+      // this CTA is done with step s's words: ack (slot reuse, joint_round).
+      // The ack follows reads only (their values are consumed), so it needs
+      // no release; ~75 MEMBAR.GPU per step slowed every hand-off.
+#if ACK_RELAXED
+      if (et == 0) red_relaxed_add(cnt + (size_t)cidx_ack() * CSTRIDE, 1);
+#else
       if (et == 0) red_release_add(cnt + (size_t)cidx_ack() * CSTRIDE, 1);
+#endif
       ++s;
       if (et < 32) sm.flag[et] &= ~2;
       epi_sync();

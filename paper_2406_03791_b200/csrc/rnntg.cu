@@ -680,6 +680,7 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   d->tcnt_bytes = (size_t)ptc::NCOUNTERS * ptc::CSTRIDE * sizeof(unsigned);
   CK(d->mem.alloc(&d->tcnt, (size_t)ptc::NCOUNTERS * ptc::CSTRIDE));
   tp.cnt = d->tcnt;
+  tp.decided = d->tcnt + (size_t)(ptc::NCOUNTERS - 1) * ptc::CSTRIDE;  // zeroed with the counters
   tp.tokens = d->st.tokens;
   tp.frames = d->st.frames;
   tp.scores = d->st.scores;
@@ -688,7 +689,10 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   tp.ctrl = d->st.ctrl;
   for (int r = 0; r < ptc::NROLES; ++r) tp.prof_first[r] = -1;
   for (int c = G - 1; c >= 0; --c) tp.prof_first[roles[c].x] = c;
-  if (env_flag("RNNTG_PROF", false)) CK(d->mem.alloc(&tp.prof, (size_t)(2 * ptc::NEV + G) * ptc::PROF_WIN));
+  if (env_flag("RNNTG_PROF", false)) {
+    CK(d->mem.alloc(&tp.prof, (size_t)(2 * ptc::NEV + G) * ptc::PROF_WIN));
+    if (env_flag("RNNTG_ECHO", false)) CK(d->mem.alloc(&tp.echo, 16));
+  }
   return RNNTG_OK;
 }
 

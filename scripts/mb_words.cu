@@ -12,6 +12,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <algorithm>
 
 #define CK(x)                                                                         \
   do {                                                                                \
@@ -35,21 +36,29 @@ constexpr int NW = 9;
 
 template <int V>
 __global__ void __launch_bounds__(64, 1) k_words(unsigned long long* words, unsigned long long* ack, int nr,
-                                                 int iters, long long* out) {
+                                                 int iters, long long* out, long long delay) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int me = blockIdx.x;
   const long long t0 = clock64();
   if (me < NW) {  // writer
     for (int it = 1; it <= iters; ++it) {
+      if (delay) {  // readers spin this long before the words are written
+        const long long d0 = clock64();
+        while (clock64() - d0 < delay) {
+        }
+      }
+      const long long tw = clock64();
       if (warp == 0) {
         const unsigned long long w = ((unsigned long long)it << 32) | (unsigned)(me * 32 + lane);
         if (V == 2) atomicExch(&words[me * 32 + lane], w);
         else str(&words[me * 32 + lane], w);
       }
       // wait for the ack of this iteration
-      if (threadIdx.x == 0)
+      if (threadIdx.x == 0) {
         while ((ldr(ack) >> 32) != (unsigned long long)it) {
         }
+        if (me == 0) out[64 + (it & 63)] = clock64() - tw;
+      }
       __syncthreads();
     }
   } else if (me < NW + nr) {  // reader
@@ -58,7 +67,7 @@ __global__ void __launch_bounds__(64, 1) k_words(unsigned long long* words, unsi
         unsigned long long a[NW];
         if (V == 3) {
           for (int t = 0; t < NW; ++t)
-            do a[t] = ldr(&words[t * 32 + lane]); while ((a[t] >> 32) != (unsigned long long)it);
+            do a[t] = ldr(&words[t * 32 + lane]); while ((a[t] >> 32) < (unsigned long long)it);
         } else {
           for (int t = 0; t < NW; ++t) a[t] = 0;
           bool ok;
@@ -66,9 +75,9 @@ __global__ void __launch_bounds__(64, 1) k_words(unsigned long long* words, unsi
             ok = true;
 #pragma unroll
             for (int t = 0; t < NW; ++t)
-              if ((a[t] >> 32) != (unsigned long long)it) a[t] = ldr(&words[t * 32 + lane]);
+              a[t] = ldr(&words[t * 32 + lane]);
 #pragma unroll
-            for (int t = 0; t < NW; ++t) ok = ok && (a[t] >> 32) == (unsigned long long)it;
+            for (int t = 0; t < NW; ++t) ok = ok && (a[t] >> 32) >= (unsigned long long)it;
           } while (!ok);
         }
         __syncwarp();
@@ -82,15 +91,17 @@ __global__ void __launch_bounds__(64, 1) k_words(unsigned long long* words, unsi
 }
 
 template <int V>
-void run(const char* name, int nr, unsigned long long* words, unsigned long long* ack, long long* dout) {
+void run(const char* name, int nr, unsigned long long* words, unsigned long long* ack, long long* dout,
+         long long delay = 0) {
   const int iters = 200;
   CK(cudaMemset(words, 0, NW * 32 * 8));
   CK(cudaMemset(ack, 0, 8));
-  k_words<V><<<NW + nr, 64>>>(words, ack, nr, iters, dout);
+  k_words<V><<<NW + nr, 64>>>(words, ack, nr, iters, dout, delay);
   CK(cudaDeviceSynchronize());
-  long long h[64];
-  CK(cudaMemcpy(h, dout, (NW + nr) * 8, cudaMemcpyDeviceToHost));
-  printf("%-48s round trip %6.0f cycles (words hop + ack hop)\n", name, (double)h[0] / iters);
+  long long h[128];
+  CK(cudaMemcpy(h, dout, 128 * 8, cudaMemcpyDeviceToHost));
+  std::sort(h + 64, h + 128);
+  printf("%-48s delay %6lld: write->ack round trip median %6lld cycles\n", name, delay, h[96]);
 }
 
 int main() {
@@ -99,11 +110,11 @@ int main() {
   long long* dout;
   CK(cudaMalloc(&words, NW * 32 * 8));
   CK(cudaMalloc(&ack, 8));
-  CK(cudaMalloc(&dout, 64 * 8));
-  run<0>("w0 relaxed words, 20 readers, batched poll", 20, words, ack, dout);
-  run<1>("w1 relaxed words, 1 reader", 1, words, ack, dout);
-  run<2>("w2 atom.exch words, 20 readers", 20, words, ack, dout);
-  run<3>("w3 relaxed words, 20 readers, tile-by-tile poll", 20, words, ack, dout);
-  run<0>("w0 relaxed words, 55 readers, batched poll", 55, words, ack, dout);
+  CK(cudaMalloc(&dout, 128 * 8));
+  for (long long d : {0LL, 2000LL, 10000LL, 30000LL}) {
+    run<0>("w0 relaxed words, 20 readers", 20, words, ack, dout, d);
+    run<0>("w0 relaxed words, 55 readers", 55, words, ack, dout, d);
+    run<1>("w1 relaxed words, 1 reader", 1, words, ack, dout, d);
+  }
   return 0;
 }

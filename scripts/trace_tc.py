@@ -69,3 +69,10 @@ for e, nm in [(40, "P trunk published (prev step)"), (12, "J chunk0 seen"), (41,
     d = (ev[e] - ev[0]).astype(np.float64); ok = ev[e] > 0
     if ok.any(): print(f"  {nm:32s} {np.median(d[ok]) / 1000:8.2f}")
 iv(22, 35, "R0 words seen(w0) -> w1 released"); iv(35, 36, "R0 w1 gather issue"); iv(36, 37, "R0 w1 gather -> epi_sync out"); iv(24, 37, "R0 w0 rules done -> epi_sync out (w1)")
+np_ = allev[39].astype(np.float64)
+print("R0 decide poll iterations per step: median", np.median(np_[np_ > 0]), "min", np_[np_ > 0].min(), "max", np_.max())
+l1 = allev[38].astype(np.float64)
+print("R0 single strong load latency (cycles): median", np.median(l1[l1 > 0]), "min", l1[l1 > 0].min(), "max", l1.max())
+rt = allev[37].astype(np.float64)
+if (rt > 0).any() and os.environ.get("RNNTG_ECHO"):
+    print("J->R0->J round trip (J clock, cycles): median", np.median(rt[rt > 0]), "min", rt[rt > 0].min())
