@@ -584,11 +584,14 @@ rnntg_status setup_tc(rnntg_decoder* d) {
     for (int mm = 0; mm < 128; ++mm) {
       for (int k = 0; k < Kp; ++k) row[k] = wel(mm, k) * scale;
       for (int k = 0; k < Kp; k += 2) {
+        // smem image <- W_hi and TMEM pairs <- W_lo (ptc::SWAP_HILO: the reverse)
         uint16_t lb[2];
         for (int j = 0; j < 2; ++j) {
           const float v = row[k + j];
-          const uint16_t hb = f2h_bits(v);
-          lb[j] = f2h_bits(v - h2f(hb));
+          uint16_t hb = f2h_bits(v);
+          uint16_t l = f2h_bits(v - h2f(hb));
+          if (ptc::SWAP_HILO) std::swap(hb, l);
+          lb[j] = l;
           std::memcpy(hi + (size_t)((k + j) / 64) * 16384 + ptc::swz(mm, (k + j) % 64), &hb, 2);
         }
         lo[(size_t)(k / 2) * 128 + mm] = (uint32_t)lb[0] | ((uint32_t)lb[1] << 16);
