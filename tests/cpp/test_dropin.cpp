@@ -14,6 +14,7 @@
 #include "rnntsim/decoders.hpp"
 #include "rnntsim/errors.hpp"
 #include "rnntsim_cuda.hpp"
+#include "cuda_lstm.hpp"
 
 using namespace rnntsim;
 
@@ -43,39 +44,6 @@ bool same(const Hypotheses& a, const Hypotheses& b, double* max_rel) {
   return true;
 }
 
-class CudaLstm : public oracle::LstmModel, public cuda::CudaWeightSource {
- public:
-  CudaLstm(const orc_dims& d, std::vector<std::vector<float>> w)
-      : oracle::LstmModel(d, ptrs(w).data()), d_(d), w_(std::move(w)) {}
-  rnntg_dims cuda_dims() const override {
-    rnntg_dims r{};
-    r.vocab = d_.vocab;
-    r.embed = d_.embed;
-    r.hidden = d_.hidden;
-    r.layers = d_.layers;
-    r.cell = RNNTG_CELL_LSTM;
-    r.joint = d_.joint;
-    r.feature = d_.feature;
-    r.num_durations = d_.num_durations;
-    for (int i = 0; i < d_.num_durations; ++i) r.durations[i] = d_.durations[i];
-    return r;
-  }
-  std::vector<const float*> cuda_weights() const override {
-    std::vector<const float*> p;
-    for (const auto& v : w_) p.push_back(v.data());
-    return p;
-  }
-
- private:
-  static std::vector<const float*> ptrs(const std::vector<std::vector<float>>& w) {
-    std::vector<const float*> p;
-    for (const auto& v : w) p.push_back(v.data());
-    return p;
-  }
-  orc_dims d_;
-  std::vector<std::vector<float>> w_;
-};
-
 }  // namespace
 
 int main() {
@@ -83,9 +51,10 @@ int main() {
     std::printf("no CUDA device\n");
     return 1;
   }
-  for (rnntg_exec ex : {RNNTG_EXEC_GRAPH, RNNTG_EXEC_PERSISTENT}) {
+  for (rnntg_exec ex : {RNNTG_EXEC_GRAPH, RNNTG_EXEC_PERSISTENT, RNNTG_EXEC_TENSOR, RNNTG_EXEC_HOSTLOOP}) {
     cuda::set_executor(ex);
-    const char* en = ex == RNNTG_EXEC_GRAPH ? "graph" : "persistent";
+    const char* en = ex == RNNTG_EXEC_GRAPH ? "graph" : ex == RNNTG_EXEC_PERSISTENT ? "persistent"
+                     : ex == RNNTG_EXEC_TENSOR ? "tensor" : "hostloop";
     // criterion 1 analogue: 200 random configs x 4 drop-in decoders
     int mism = 0;
     double rel = 0.0;
