@@ -93,7 +93,7 @@ constexpr bool SWAP_HILO = SWAP_HILO_CFG;
 #define ACK_RELAXED 1
 #endif
 #ifndef SPIN_ONE
-#define SPIN_ONE 0
+#define SPIN_ONE 1
 #endif
 #ifndef TMA_ACT
 #define TMA_ACT 1  // activations via 2-D tensor maps (plain row-major in global, swizzled by TMA)
@@ -811,6 +811,8 @@ struct Epi {
 #if SPIN_ONE
         // spin on one word (tile NJ-1, written last in column order by no one in
         // particular) with a single load in flight, then read the rest once
+        // (warp-wide strong loads are serviced ~100 cycles apart: a 9-16 load
+        // batch per poll made each poll ~1 us; one load per poll is ~360 cycles)
         while ((unsigned)(ld_poll_u64(wv + (nj - 1) * 32 * PW_STRIDE) >> 32 & 0xffu) != tg) ++npoll;
 #endif
         do {
@@ -820,16 +822,12 @@ struct Epi {
           // loads are in flight together; a branch per load serialised them
           // (one ~300-cycle round trip each, ~2000 cycles per poll)
 #pragma unroll
-          for (int t = 0; t < MAXNJ; ++t) {
-            const int tt = t < nj ? t : nj - 1;
-            a[t] = ld_poll_u64(wv + tt * 32 * PW_STRIDE);
-          }
+          for (int t = 0; t < MAXNJ; ++t)
+            if (t < nj) a[t] = ld_poll_u64(wv + t * 32 * PW_STRIDE);
           if (P.D) {
 #pragma unroll
-            for (int t = 0; t < MAXNJ; ++t) {
-              const int tt = t < nj ? t : nj - 1;
-              d[t] = ld_poll_u64(wd + tt * 32 * PW_STRIDE);
-            }
+            for (int t = 0; t < MAXNJ; ++t)
+              if (t < nj) d[t] = ld_poll_u64(wd + t * 32 * PW_STRIDE);
           }
 #pragma unroll
           for (int t = 0; t < MAXNJ; ++t)
