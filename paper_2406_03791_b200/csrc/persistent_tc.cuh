@@ -82,6 +82,15 @@ constexpr int NROLES = 5;
 #ifndef WORD_READBACK
 #define WORD_READBACK 0  // A/B: no gain
 #endif
+#ifndef PRODUCER_V2
+// converged producer warp: lane-parallel counter poll + ballot, fully unrolled
+// issue with the ring reset every round (stage = chunk % NSTAGE, a constant);
+// the single-lane loop cost ~350 cycles of serial issue per 8 KB chunk
+#define PRODUCER_V2 1
+#endif
+#ifndef LAZY_BATCH_NS
+#define LAZY_BATCH_NS 0
+#endif
 #ifndef SWAP_HILO_CFG
 #define SWAP_HILO_CFG 1  // A/B: W_hi in TMEM (TS, N=64) + W_lo in smem (SS, N=32): -0.3 us/step
 #endif
@@ -158,7 +167,8 @@ struct TParams {
 };
 constexpr int PROF_WIN = 64;  // traced joint steps [PROF_S0, PROF_S0 + PROF_WIN)
 constexpr int PROF_S0 = 100;
-constexpr int NEV = 48;  // 40..47: globaltimer hand-off marks
+constexpr int NEV = 112;  // 40..47: globaltimer hand-off marks; 48..53: I1/P load + MMA marks;
+                          // 56..80 J / 82..106 I1 per-chunk clock64 (load issue, full, issued, acc)
 
 // ------------------------------------------------------------------ PTX
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
@@ -319,6 +329,18 @@ __device__ __forceinline__ void tma_ld2(void* dst, const CUtensorMap* map, int x
       "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_ld2_u(uint32_t dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}" : "=r"(p));
+  return p != 0;
+}
 __device__ __forceinline__ void tma_st2(const CUtensorMap* map, int x, int y, const void* src) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(x),
                "r"(y), "r"(smem_u32(src))
@@ -367,13 +389,14 @@ struct Smem {
   uint64_t* cmd;        // [1]
   uint64_t* wbar;       // [1]
   uint32_t* tslot;
+  unsigned long long* dbg;  // [32] per-chunk trace stamps (RNNTG_PROF)
 };
 
 constexpr int XS_FLOATS = 128 * 33;   // epilogue exchange: [128 cols][33] / [4 gates][32][32]
 constexpr int RED_F4 = 256;           // argmax merge / word staging / sumexp group scratch (4 KB)
 __host__ __device__ inline size_t smem_bytes(int KC) {
   return 1024 /*align slack*/ + (size_t)KC * 16384 + (size_t)NSTAGE * CHUNK + XS_FLOATS * 4 +
-         RED_F4 * 16 + 12 * 32 * 4 + 16 * 4 + 16 * 8 + 64;
+         RED_F4 * 16 + 12 * 32 * 4 + 16 * 4 + 16 * 8 + 64 + 256;
 }
 
 __device__ inline Smem carve(unsigned char* raw, int KC) {
@@ -403,6 +426,7 @@ __device__ inline Smem carve(unsigned char* raw, int KC) {
   s.cmd = s.acce + 2;
   s.wbar = s.cmd + 1;
   s.tslot = reinterpret_cast<uint32_t*>(s.wbar + 1);
+  s.dbg = reinterpret_cast<unsigned long long*>(s.wbar + 2);
   return s;
 }
 
@@ -475,6 +499,31 @@ struct Epi {
       // globaltimer reads queue behind outstanding loads: only at step start
       if (ev == 0) P.prof[(size_t)ev * PROF_WIN + (s - PROF_S0)] = gtimer();
       P.prof[(size_t)(NEV + P.G + ev) * PROF_WIN + (s - PROF_S0)] = clock64();
+    }
+  }
+  // I1 / P: producer chunk-0 / last-chunk issue and MMA-issued times of this
+  // round (stamped in misc[8..13] by warps 0/1) -> events ev0 .. ev0+2
+  __device__ __forceinline__ void log_ld(int ev0) {
+    if (tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) {
+      const volatile unsigned long long* t = reinterpret_cast<const volatile unsigned long long*>(sm.misc + 8);
+      for (int k = 0; k < 3; ++k) P.prof[(size_t)(ev0 + k) * PROF_WIN + (s - PROF_S0)] = t[k];
+    }
+  }
+  // J / I1: per-chunk load-issue and full times, MMA-issued and acc-ready
+  // (clock64, this SM) -> events ev0 + [0, 10) issue, + [10, 20) full, +20, +21
+  __device__ __forceinline__ void log_chunks(int ev0, long long tacc) {
+    if (tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) {
+      const volatile unsigned long long* t = sm.dbg;
+      const int KC = P.act_kc[role == ROLE_J ? TRUNK : layer - 1];
+      for (int k = 0; k < KC && k < 10; ++k) {
+        P.prof[(size_t)(ev0 + k) * PROF_WIN + (s - PROF_S0)] = t[k];
+        P.prof[(size_t)(ev0 + 10 + k) * PROF_WIN + (s - PROF_S0)] = t[16 + k];
+      }
+      P.prof[(size_t)(ev0 + 20) * PROF_WIN + (s - PROF_S0)] = t[31];
+      P.prof[(size_t)(ev0 + 21) * PROF_WIN + (s - PROF_S0)] = (unsigned long long)tacc;
+      P.prof[(size_t)(ev0 + 22) * PROF_WIN + (s - PROF_S0)] = t[11] - t[10];  // polls after chunk 0
+      P.prof[(size_t)(ev0 + 23) * PROF_WIN + (s - PROF_S0)] = t[12];  // chunk 2: before empty wait
+      P.prof[(size_t)(ev0 + 24) * PROF_WIN + (s - PROF_S0)] = t[13];  // chunk 2: after TMA issue
     }
   }
   // one load+MMA round on this CTA's input at epoch e (-1 = exit)
@@ -567,6 +616,7 @@ struct Epi {
     read_acc(round - 1, v);
     mark(1);
     mark(16);
+    if (P.prof) log_chunks(56, clock64());
     // slot reuse: every CTA has finished decide(s - NSLOT); checked once per half window
     if (s >= NSLOT / 2 && s % (NSLOT / 2) == 0)
       wait_counter(cidx_ack(), (unsigned)P.G * (unsigned)(s - NSLOT / 2 + 1));
@@ -799,6 +849,7 @@ struct Epi {
         __syncwarp(0xffffffffu >> (32 - B));
         bool ok;
         const int nj = P.NJ;
+        const bool hasd = P.D != 0;
         int npoll = 0;
         long long lat1 = 0;
         if (tracer && role == ROLE_R && layer == 0 && b == 0) {  // one strong load, timed
@@ -814,6 +865,16 @@ struct Epi {
         // (warp-wide strong loads are serviced ~100 cycles apart: a 9-16 load
         // batch per poll made each poll ~1 us; one load per poll is ~360 cycles)
         while ((unsigned)(ld_poll_u64(wv + (nj - 1) * 32 * PW_STRIDE) >> 32 & 0xffu) != tg) ++npoll;
+        if (role == ROLE_R && layer == 0 && b == 0) {
+          mark(30);
+          gmark(54);  // last tile's word seen
+        }
+#endif
+        const int nspin = npoll;
+#if LAZY_BATCH_NS
+        // the CTAs off the critical path read the tile words after R_0 did:
+        // 75 CTAs reading the same 18 lines at once made R_0's read ~3x slower
+        if (lazy) __nanosleep(LAZY_BATCH_NS);
 #endif
         do {
           ++npoll;
@@ -824,39 +885,45 @@ struct Epi {
 #pragma unroll
           for (int t = 0; t < MAXNJ; ++t)
             if (t < nj) a[t] = ld_poll_u64(wv + t * 32 * PW_STRIDE);
-          if (P.D) {
+          if (hasd) {
 #pragma unroll
             for (int t = 0; t < MAXNJ; ++t)
               if (t < nj) d[t] = ld_poll_u64(wd + t * 32 * PW_STRIDE);
           }
+          // branch-free tag check: a short-circuit && compiled to one branch +
+          // reconvergence block per tile (~1000 cycles for 16 tiles)
+          unsigned bad = 0u;
 #pragma unroll
-          for (int t = 0; t < MAXNJ; ++t)
-            if (t < P.NJ)
-              ok = ok && (unsigned)(a[t] >> 32 & 0xffu) == tg && (!P.D || (unsigned)(d[t] >> 32 & 0xffu) == tg);
+          for (int t = 0; t < MAXNJ; ++t) {
+            const unsigned ta = (unsigned)(a[t] >> 32) & 0xffu, td = (unsigned)(d[t] >> 32) & 0xffu;
+            bad |= (unsigned)(t < nj) & ((unsigned)(ta != tg) | ((unsigned)hasd & (unsigned)(td != tg)));
+          }
+          ok = bad == 0u;
           if (!ok && lazy && LAZY_NS) __nanosleep(LAZY_NS);
         } while (!ok);
+        if (role == ROLE_R && layer == 0 && b == 0) {
+          mark(31);
+          gmark(55);  // every tile's word seen
+          if (tracer && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) P.prof[(size_t)15 * PROF_WIN + (s - PROF_S0)] = npoll - nspin;
+        }
         npoll_out = npoll;
         lat1_out = lat1;
         best = -INFINITY;
         float bd = -INFINITY;
         int di = 0;
+        // selects, no branches; tiles in column order: strict > keeps the lowest index
 #pragma unroll
-        for (int t = 0; t < MAXNJ; ++t)
-          if (t < P.NJ) {
-            const float x = __uint_as_float((unsigned)a[t]);
-            if (x > best) {  // tiles in column order: strict > keeps the lowest index
-              best = x;
-              kk = (int)((unsigned)(a[t] >> 32) >> 8);
-            }
-            if (P.D) {
-              const float y = __uint_as_float((unsigned)d[t]);
-              if (y > bd) {
-                bd = y;
-                di = (int)((unsigned)(d[t] >> 32) >> 8);
-              }
-            }
-          }
-        dd = P.D ? P.durations[di] : 0;
+        for (int t = 0; t < MAXNJ; ++t) {
+          const float x = __uint_as_float((unsigned)a[t]);
+          const bool tx = (t < nj) & (x > best);
+          best = tx ? x : best;
+          kk = tx ? (int)((unsigned)(a[t] >> 32) >> 8) : kk;
+          const float y = __uint_as_float((unsigned)d[t]);
+          const bool ty = hasd & (t < nj) & (y > bd);
+          bd = ty ? y : bd;
+          di = ty ? (int)((unsigned)(d[t] >> 32) >> 8) : di;
+        }
+        dd = hasd ? P.durations[di] : 0;
       }
       sm.kdec[b] = kk;
 #if ECHO_GATE
@@ -1162,6 +1229,7 @@ __device__ __forceinline__ void Epi::run_role() {
           float v[NR];
           read_acc(round - 1, v);
           mark(9);
+          log_ld(51);
 #pragma unroll
           for (int i = 0; i < NR; ++i) gp[i] = v[i];
           trunk(te);
@@ -1230,6 +1298,8 @@ __device__ __forceinline__ void Epi::run_role() {
             }
             read_acc(round - 1, v);
             mark(7);
+            if (layer == 1) log_ld(48);
+            if (P.prof && layer == 1) log_chunks(82, clock64());
 #pragma unroll
             for (int i = 0; i < NR; ++i) v[i] = (v[i] + x[i]) + bias_m;
           }
@@ -1324,6 +1394,109 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
   __syncthreads();
   tc_fence_after();
 
+#if PRODUCER_V2
+  if (warp == 0) {
+    // ================= producer (converged warp): stream input chunks into the ring =================
+    // Stage of chunk kc is kc % NSTAGE every round: a round is posted only after
+    // the epilogue read the previous round's accumulator, so every earlier MMA
+    // (and its smem read) has completed and the first NSTAGE chunks need no
+    // empty-barrier wait.  eb bit s = uses of stage s so far (mod 2).
+    const unsigned* mycnt = P.cnt + (size_t)(cidx_act(in_buf, 0) + (lane < KC ? lane : 0)) * CSTRIDE;
+    const unsigned my_np = lane < KC ? (unsigned)P.nprod[in_buf][lane] : 0u;
+    const CUtensorMap* lmap = &P.ldmap[in_buf];
+    const bool stamp_ip = P.prof && (role == ROLE_I || role == ROLE_P) && (int)blockIdx.x == P.prof_first[role];
+    const bool ctr = P.prof && (role == ROLE_J || role == ROLE_I) && (int)blockIdx.x == P.prof_first[role] && lane == 0;
+    const bool trj = P.prof && role == ROLE_J && (int)blockIdx.x == P.prof_first[role] && lane == 0;
+    unsigned long long* const prof = P.prof;
+    const uint32_t ring0 = smem_u32(sm.ring);
+    uint32_t eb = 0;
+    for (int r = 0;; ++r) {
+      mbar_wait(sm.cmd, r & 1);
+      const int e = ((volatile int*)sm.misc)[r & 1];
+      if (e < 0) break;
+      const bool tr = trj && e >= PROF_S0 && e < PROF_S0 + PROF_WIN;
+      const unsigned target = my_np * (unsigned)(e + 1);
+      int next = 0, npoll = 0;
+      while (next < KC) {
+        // one counter per lane, all in flight in one instruction
+        const bool need = lane >= next && lane < KC;
+        unsigned v = 0u;
+        if (need) v = ld_relaxed(mycnt);
+        const unsigned ok = __ballot_sync(0xffffffffu, lane < next || (need && v >= target));
+        const int ready = __ffs(~ok) - 1;  // chunks [0, ready) are published
+        if (ctr) ++npoll;
+        if (ready == next) continue;
+        if (ctr && next == 0) sm.dbg[10] = npoll;
+        fence_proxy_global();
+#pragma unroll
+        for (int kc = 0; kc < MAXKC; ++kc) {
+          if (kc >= next && kc < ready) {
+            const int st = kc % NSTAGE;
+            if (kc >= NSTAGE) mbar_wait(&sm.empty[st], ((eb >> st) & 1u) ^ 1u);
+            eb ^= 1u << st;
+            if (tr && (kc == 0 || kc == KC - 1)) prof[(size_t)(kc ? 13 : 12) * PROF_WIN + (e - PROF_S0)] = gtimer();
+            if ((kc == 0 || kc == KC - 1) && stamp_ip && lane == 0)
+              reinterpret_cast<volatile unsigned long long*>(sm.misc + 8)[kc ? 1 : 0] = gtimer();
+            if (ctr) sm.dbg[kc] = clock64();
+            if (elect_one()) {
+              mbar_arrive_expect_tx(&sm.full[st], CHUNK);
+              tma_ld2_u(ring0 + st * CHUNK, lmap, 64 * kc, 64 * (e & 1), &sm.full[st]);
+            }
+            __syncwarp();
+          }
+        }
+        next = ready;
+      }
+      if (ctr) sm.dbg[11] = npoll;
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer (converged warp) =================
+    constexpr uint32_t ID64 = idesc_f16(128, 64), ID32 = idesc_f16(128, 32);
+    const uint32_t whi0 = smem_u32(sm.whi), ring0 = smem_u32(sm.ring);
+    const bool ctr = P.prof && (role == ROLE_J || role == ROLE_I) && (int)blockIdx.x == P.prof_first[role] && lane == 0;
+    const bool trj = P.prof && role == ROLE_J && (int)blockIdx.x == P.prof_first[role] && lane == 0;
+    const bool stamp_ip = P.prof && (role == ROLE_I || role == ROLE_P) && (int)blockIdx.x == P.prof_first[role] && lane == 0;
+    uint32_t fb = 0;  // bit s = fills of stage s consumed so far (mod 2)
+    for (int r = 0;; ++r) {
+      mbar_wait(sm.cmd, r & 1);
+      const int e = ((volatile int*)sm.misc)[r & 1];
+      if (e < 0) break;
+      const int set = r & 1;
+      if (r >= 2) mbar_wait(&sm.acce[set], (uint32_t)(((r >> 1) - 1) & 1));
+      tc_fence_after();
+      const uint32_t d1 = tmem + set * ACC_COLS, d2 = d1 + 64;
+      const bool tr = trj && e >= PROF_S0 && e < PROF_S0 + PROF_WIN;
+#pragma unroll
+      for (int kc = 0; kc < MAXKC; ++kc) {
+        if (kc < KC) {
+          const int st = kc % NSTAGE;
+          mbar_wait(&sm.full[st], (fb >> st) & 1u);
+          fb ^= 1u << st;
+          if (ctr) sm.dbg[16 + kc] = clock64();
+          if (tr && (kc == 0 || kc == KC - 1)) P.prof[(size_t)(kc ? 28 : 27) * PROF_WIN + (e - PROF_S0)] = gtimer();
+          tc_fence_after();
+          const uint64_t ad = sdesc_sw128(whi0 + kc * 16384), bd = sdesc_sw128(ring0 + st * CHUNK);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t acc = (kc | k) != 0;
+            if (SWAP_HILO) {  // W_hi from TMEM (N = 64), W_lo from smem (N = 32)
+              mma_ts(d1, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID64, acc);
+              mma_ss(d2, ad + 2 * k, bd + 2 * k, ID32, acc);
+            } else {
+              mma_ss(d1, ad + 2 * k, bd + 2 * k, ID64, acc);
+              mma_ts(d2, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID32, acc);
+            }
+          }
+          mma_commit(&sm.empty[st]);
+        }
+      }
+      mma_commit(&sm.accf[set]);
+      if (ctr) sm.dbg[31] = clock64();
+      if (tr) P.prof[(size_t)29 * PROF_WIN + (e - PROF_S0)] = gtimer();
+      if (stamp_ip) reinterpret_cast<volatile unsigned long long*>(sm.misc + 8)[2] = gtimer();
+    }
+  } else {
+#else
   if (warp == 0) {
     // ================= producer: stream input chunks into the ring =================
     if (lane == 0) {
@@ -1331,15 +1504,24 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
       // reuse waits for parity (k - 1) & 1), stages filled once
       int ps = 0, pph = 1, pfill = 0;
       const unsigned* cb = P.cnt + (size_t)cidx_act(in_buf, 0) * CSTRIDE;
+      // every parameter the loop needs, read once: kernel-parameter (constant
+      // bank) reads inside the loop cost ~100+ cycles each here
+      unsigned np[MAXKC];
+#pragma unroll
+      for (int kc = 0; kc < MAXKC; ++kc) np[kc] = kc < KC ? (unsigned)P.nprod[in_buf][kc] : 0u;
+      const CUtensorMap* lmap = &P.ldmap[in_buf];
+      const bool stamp_ip = P.prof && (role == ROLE_I || role == ROLE_P) && (int)blockIdx.x == P.prof_first[role];
+      const bool ctr = P.prof && (role == ROLE_J || role == ROLE_I) && (int)blockIdx.x == P.prof_first[role];
+      const bool trj = P.prof && role == ROLE_J && (int)blockIdx.x == P.prof_first[role];
+      unsigned long long* const prof = P.prof;
       for (int r = 0;; ++r) {
         mbar_wait_sleep(sm.cmd, r & 1);
         const int e = ((volatile int*)sm.misc)[r & 1];
         if (e < 0) break;
-        const unsigned char* src = P.act[in_buf] + (size_t)(e & 1) * KC * CHUNK;
-        const bool tr = P.prof && role == ROLE_J && (int)blockIdx.x == P.prof_first[role] && e >= PROF_S0 && e < PROF_S0 + PROF_WIN;
+        const bool tr = trj && e >= PROF_S0 && e < PROF_S0 + PROF_WIN;
         // poll every outstanding chunk counter at once (one L2 round trip per
         // poll, not one per chunk), then stream all ready chunks in order
-        int next = 0;
+        int next = 0, npoll = 0;
         while (next < KC) {
           unsigned v[MAXKC];
 #pragma unroll
@@ -1348,26 +1530,29 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
           int ready = next;
 #pragma unroll
           for (int kc = 0; kc < MAXKC; ++kc)
-            if (kc == ready && kc < KC && v[kc] >= (unsigned)P.nprod[in_buf][kc] * (unsigned)(e + 1)) ++ready;
+            if (kc == ready && kc < KC && v[kc] >= np[kc] * (unsigned)(e + 1)) ++ready;
+          if (ctr) ++npoll;
           if (ready == next) {
             if (POLL_NS) __nanosleep(POLL_NS);
             continue;
           }
+          if (ctr && next == 0) sm.dbg[10] = npoll;  // polls until chunk 0 was ready
           fence_proxy_global();
           for (int kc = next; kc < ready; ++kc) {
-            if (tr && (kc == 0 || kc == KC - 1)) P.prof[(size_t)(kc ? 13 : 12) * PROF_WIN + (e - PROF_S0)] = gtimer();
-            if (kc == 0 && P.prof && (role == ROLE_I || role == ROLE_P) && (int)blockIdx.x == P.prof_first[role] &&
-                e >= 1 && e < 1 + 4 * PROF_WIN)
-              P.prof[(size_t)(role == ROLE_I ? 45 : 47) * PROF_WIN + ((e - 1) % PROF_WIN)] = gtimer();
+            if (tr && (kc == 0 || kc == KC - 1)) prof[(size_t)(kc ? 13 : 12) * PROF_WIN + (e - PROF_S0)] = gtimer();
+            if ((kc == 0 || kc == KC - 1) && stamp_ip)  // stamped per round, logged by the epilogue
+              reinterpret_cast<volatile unsigned long long*>(sm.misc + 8)[kc ? 1 : 0] = gtimer();
             const int s = ps;
+            if (ctr && kc == 2) sm.dbg[12] = clock64();
             if (pfill >= NSTAGE) mbar_wait_sleep(&sm.empty[s], (uint32_t)pph);
+            if (ctr) sm.dbg[kc] = clock64();
             mbar_arrive_expect_tx(&sm.full[s], CHUNK);
 #if TMA_ACT
-            tma_ld2(sm.ring + s * CHUNK, &P.ldmap[in_buf], 64 * kc, 64 * (e & 1), &sm.full[s]);
-            (void)src;
+            tma_ld2(sm.ring + s * CHUNK, lmap, 64 * kc, 64 * (e & 1), &sm.full[s]);
 #else
-            bulk_g2s(sm.ring + s * CHUNK, src + (size_t)kc * CHUNK, CHUNK, &sm.full[s]);
+            bulk_g2s(sm.ring + s * CHUNK, P.act[in_buf] + ((size_t)(e & 1) * KC + kc) * CHUNK, CHUNK, &sm.full[s]);
 #endif
+            if (ctr && kc == 2) sm.dbg[13] = clock64();
             if (pfill < NSTAGE) ++pfill;
             if (++ps == NSTAGE) {
               ps = 0;
@@ -1376,6 +1561,7 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
           }
           next = ready;
         }
+        if (ctr) sm.dbg[11] = npoll;
       }
     }
   } else if (warp == 1) {
@@ -1391,11 +1577,13 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
       if (r >= 2) mbar_wait_sleep(&sm.acce[set], (uint32_t)(((r >> 1) - 1) & 1));
       tc_fence_after();
       const uint32_t d1 = tmem + set * ACC_COLS, d2 = d1 + 64;
+      const bool ctr = P.prof && (role == ROLE_J || role == ROLE_I) && (int)blockIdx.x == P.prof_first[role];
       const bool tr = P.prof && role == ROLE_J && (int)blockIdx.x == P.prof_first[role] && e >= PROF_S0 &&
                       e < PROF_S0 + PROF_WIN && lane == 0;
       for (int kc = 0; kc < KC; ++kc) {
         const int s = cs;
         mbar_wait_sleep(&sm.full[s], (uint32_t)cph);
+        if (ctr && lane == 0) sm.dbg[16 + kc] = clock64();
         if (tr && (kc == 0 || kc == KC - 1)) P.prof[(size_t)(kc ? 28 : 27) * PROF_WIN + (e - PROF_S0)] = gtimer();
         tc_fence_after();
         const uint64_t ad = sdesc_sw128(whi0 + kc * 16384), bd = sdesc_sw128(ring0 + s * CHUNK);
@@ -1417,9 +1605,13 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
         }
       }
       mma_commit(&sm.accf[set]);
+      if (ctr && lane == 0) sm.dbg[31] = clock64();
       if (tr) P.prof[(size_t)29 * PROF_WIN + (e - PROF_S0)] = gtimer();
+      if (P.prof && (role == ROLE_I || role == ROLE_P) && (int)blockIdx.x == P.prof_first[role] && lane == 0)
+        reinterpret_cast<volatile unsigned long long*>(sm.misc + 8)[2] = gtimer();
     }
   } else {
+#endif
     // ================= epilogue + replicated control (128 threads) =================
     Epi e(P, sm, tmem, tid - 64, warp & 3, role, layer, tile, wsc);
     e.run_role();
