@@ -64,8 +64,6 @@ constexpr int MAXBUF = MAXL + 1;
 #define NSLOT_CFG 8  // A/B: 8 vs 32 slots -0.03 us/step
 #endif
 constexpr int NSLOT = NSLOT_CFG;  // joint-partial ring depth (ack checked every NSLOT/2 steps)
-constexpr int ACC_COLS = 96;
-constexpr int WLO_COL = 2 * ACC_COLS;
 constexpr int CSTRIDE = 32;      // u32 words between counters (one 128-byte line each)
 
 enum Role { ROLE_J = 0, ROLE_P = 1, ROLE_R = 2, ROLE_I = 3, ROLE_E = 4 };  // E: emitter (no weights)
@@ -82,12 +80,6 @@ constexpr int NROLES = 5;
 #ifndef WORD_READBACK
 #define WORD_READBACK 0  // A/B: no gain
 #endif
-#ifndef PRODUCER_V2
-// converged producer warp: lane-parallel counter poll + ballot, fully unrolled
-// issue with the ring reset every round (stage = chunk % NSTAGE, a constant);
-// the single-lane loop cost ~350 cycles of serial issue per 8 KB chunk
-#define PRODUCER_V2 1
-#endif
 #ifndef LAZY_BATCH_NS
 #define LAZY_BATCH_NS 0
 #endif
@@ -95,6 +87,35 @@ constexpr int NROLES = 5;
 #define SWAP_HILO_CFG 1  // A/B: W_hi in TMEM (TS, N=64) + W_lo in smem (SS, N=32): -0.3 us/step
 #endif
 constexpr bool SWAP_HILO = SWAP_HILO_CFG;
+#ifndef LO_TMEM_CFG
+// W_lo of the first chunks in TMEM too: two TS MMAs per k-step pipeline (52
+// cycles resident, 72.6 in the load+MMA pipeline of scripts/mb_pipe2.cu) where
+// TS + SS serialise (63 / 78.2).  TMEM room comes from one 64-column
+// accumulator: W_lo.x_hi accumulates into the W_hi.x_hi columns (same 2^s
+// scale).  Off: inside the executor every LO_TMEM build measured ~2.3 us/step
+// SLOWER (A/B, 18.2 vs 15.9 us), for reasons not pinned down (the slowdown
+// also shows in epilogue sections that do not touch the tensor pipe).
+#define LO_TMEM_CFG 0
+#endif
+constexpr bool LO_TMEM = LO_TMEM_CFG && SWAP_HILO_CFG;
+#ifndef CHUNK_ASM
+#define CHUNK_ASM 1  // one elect.sync per chunk of 8 MMAs (see mma_chunk_tt)
+#endif
+constexpr int ACC_COLS = LO_TMEM ? 64 : 96;  // [x_hi | x_lo | lo.x_hi] (LO_TMEM: [x_hi + lo.x_hi | x_lo])
+#ifndef NACC_CFG
+#define NACC_CFG 1
+#endif
+#ifndef NLO_MAX
+#define NLO_MAX 16
+#endif
+constexpr int NACC = LO_TMEM ? NACC_CFG : 2;  // accumulator sets
+constexpr int WLO_COL = NACC * ACC_COLS;     // first TMEM weight column (TMEM-resident W_hi pairs)
+// chunks whose W_lo is TMEM-resident too (after the KC chunks of W_hi pairs)
+__host__ __device__ constexpr int nlo_chunks(int KC) {
+  return LO_TMEM ? ((512 - WLO_COL) / 32 - KC < KC ? ((512 - WLO_COL) / 32 - KC < NLO_MAX ? (512 - WLO_COL) / 32 - KC : NLO_MAX)
+                                                   : (KC < NLO_MAX ? KC : NLO_MAX))
+                 : 0;
+}
 #ifndef WORDS_ONE_LANE
 #define WORDS_ONE_LANE 0
 #endif
@@ -142,6 +163,7 @@ struct TParams {
   const int4* roles;          // [G] {role, layer, tile, float bits of 2^-s}
   const unsigned char* wimg;  // [G][wstride]: W_hi smem image, then W_lo packed [Kp/2][128] u32
   size_t wstride;
+  size_t wtoff;               // byte offset of the TMEM column-pair image in a CTA's weight image
   const float* bias[MAXL];    // reference layout [G*H]
   const float* table0;        // [V1][GH] gate-interleaved (col = u*Gg + g)
   const float* fp;            // [B*T][Jp] encoder projection (K1)
@@ -196,6 +218,54 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint3
       "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
       "r"(a), "l"(b), "r"(id), "r"(acc));
+}
+// One 64-deep chunk (4 k-steps) under ONE elect.sync, then the stage commit:
+// D[0:64) += A_hi x B (TMEM A, N = 64) and D[0:32) += A_lo x B[:, 0:32) with A_lo
+// from TMEM (tt) or a smem descriptor (ts).  A per-MMA elect block cost ~10
+// instructions of ELECT/VOTE/R2UR each; the MMA warp issued a chunk every ~470
+// cycles against ~230 of tensor-pipe work.  first: the chunk starts the tile
+// (its first MMA overwrites D).
+__device__ __forceinline__ void mma_chunk_tt(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t b, uint32_t first,
+                                             uint32_t id64, uint32_t id32, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\t.reg .b32 h1, h2, h3, l1, l2, l3;\n\t.reg .b64 b1, b2, b3;\n\t"
+      "setp.eq.b32 p, %4, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+      "add.u32 h1, %1, 8;\n\tadd.u32 h2, %1, 16;\n\tadd.u32 h3, %1, 24;\n\t"
+      "add.u32 l1, %2, 8;\n\tadd.u32 l2, %2, 16;\n\tadd.u32 l3, %2, 24;\n\t"
+      "add.u64 b1, %3, 2;\n\tadd.u64 b2, %3, 4;\n\tadd.u64 b3, %3, 6;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h1], b1, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l1], b1, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h2], b2, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l2], b2, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h3], b3, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l3], b3, %6, t;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}" ::"r"(d),
+      "r"(ahi), "r"(alo), "l"(b), "r"(first), "r"(id64), "r"(id32), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mma_chunk_ts(uint32_t d, uint32_t ahi, uint64_t alo, uint64_t b, uint32_t first,
+                                             uint32_t id64, uint32_t id32, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\t.reg .b32 h1, h2, h3;\n\t.reg .b64 l1, l2, l3, b1, b2, b3;\n\t"
+      "setp.eq.b32 p, %4, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+      "add.u32 h1, %1, 8;\n\tadd.u32 h2, %1, 16;\n\tadd.u32 h3, %1, 24;\n\t"
+      "add.u64 l1, %2, 2;\n\tadd.u64 l2, %2, 4;\n\tadd.u64 l3, %2, 6;\n\t"
+      "add.u64 b1, %3, 2;\n\tadd.u64 b2, %3, 4;\n\tadd.u64 b3, %3, 6;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h1], b1, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l1, b1, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h2], b2, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l2, b2, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h3], b3, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l3, b3, %6, t;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}" ::"r"(d),
+      "r"(ahi), "l"(alo), "l"(b), "r"(first), "r"(id64), "r"(id32), "r"(smem_u32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
@@ -536,10 +606,18 @@ struct Epi {
   }
   // accumulator of round r -> v[i] = (W . A)[m][r0 + i] * 2^-s
   __device__ __forceinline__ void read_acc(int r, float (&v)[NR]) {
-    mbar_wait_sleep(&sm.accf[r & 1], (uint32_t)((r >> 1) & 1));
+    const int set = NACC == 1 ? 0 : (r & 1);
+    mbar_wait_sleep(&sm.accf[set], (uint32_t)(NACC == 1 ? (r & 1) : ((r >> 1) & 1)));
     tc_fence_after();
-    const uint32_t a = tq + (r & 1) * ACC_COLS + r0;
-    {
+    const uint32_t a = tq + set * ACC_COLS + r0;
+    if (LO_TMEM) {  // [W_hi.x_hi + W_lo.x_hi | W_hi.x_lo]
+      uint32_t x0[16], x1[16];
+      tmem_ld16(a, x0);
+      tmem_ld16(a + 32, x1);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < NR; ++i) v[i] = (__uint_as_float(x0[i]) + __uint_as_float(x1[i])) * wsc;
+    } else {
       uint32_t x0[16], x1[16], x2[16];
       tmem_ld16(a, x0);
       tmem_ld16(a + 32, x1);
@@ -551,7 +629,7 @@ struct Epi {
     }
     tc_fence_before();
     __syncwarp();
-    if ((et & 31) == 0) mbar_arrive(&sm.acce[r & 1]);  // one arrival per epilogue warp
+    if ((et & 31) == 0) mbar_arrive(&sm.acce[set]);  // one arrival per epilogue warp
   }
   __device__ __forceinline__ void wait_counter(int ci, unsigned target) {
     if (et == 0) spin_geq(cnt + (size_t)ci * CSTRIDE, target);
@@ -1379,9 +1457,10 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
   }
   if (warp >= 2) {
     const int q = warp & 3, half = warp >= 6;
-    const uint32_t* lo = reinterpret_cast<const uint32_t*>(wimg + (size_t)KC * 16384);
+    const uint32_t* lo = reinterpret_cast<const uint32_t*>(wimg + P.wtoff);
     const int m = 32 * q + lane;
-    for (int c0 = half * KC * 16; c0 < (half + 1) * KC * 16; c0 += 8) {
+    const int ncol = (KC + nlo_chunks(KC)) * 32;  // W_hi pairs, then the TMEM-resident W_lo pairs
+    for (int c0 = half * (ncol / 2); c0 < (half + 1) * (ncol / 2); c0 += 8) {
       uint32_t r[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) r[j] = __ldg(lo + (size_t)(c0 + j) * 128 + m);
@@ -1394,7 +1473,6 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
   __syncthreads();
   tc_fence_after();
 
-#if PRODUCER_V2
   if (warp == 0) {
     // ================= producer (converged warp): stream input chunks into the ring =================
     // Stage of chunk kc is kc % NSTAGE every round: a round is posted only after
@@ -1457,14 +1535,16 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
     const bool trj = P.prof && role == ROLE_J && (int)blockIdx.x == P.prof_first[role] && lane == 0;
     const bool stamp_ip = P.prof && (role == ROLE_I || role == ROLE_P) && (int)blockIdx.x == P.prof_first[role] && lane == 0;
     uint32_t fb = 0;  // bit s = fills of stage s consumed so far (mod 2)
+    const int nlo = nlo_chunks(KC);
     for (int r = 0;; ++r) {
       mbar_wait(sm.cmd, r & 1);
       const int e = ((volatile int*)sm.misc)[r & 1];
       if (e < 0) break;
-      const int set = r & 1;
-      if (r >= 2) mbar_wait(&sm.acce[set], (uint32_t)(((r >> 1) - 1) & 1));
+      const int set = NACC == 1 ? 0 : (r & 1);
+      if (NACC == 1 && r >= 1) mbar_wait(&sm.acce[0], (uint32_t)((r - 1) & 1));
+      if (NACC == 2 && r >= 2) mbar_wait(&sm.acce[set], (uint32_t)(((r >> 1) - 1) & 1));
       tc_fence_after();
-      const uint32_t d1 = tmem + set * ACC_COLS, d2 = d1 + 64;
+      const uint32_t d1 = tmem + set * ACC_COLS, d2 = LO_TMEM ? d1 : d1 + 64;
       const bool tr = trj && e >= PROF_S0 && e < PROF_S0 + PROF_WIN;
 #pragma unroll
       for (int kc = 0; kc < MAXKC; ++kc) {
@@ -1476,18 +1556,32 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
           if (tr && (kc == 0 || kc == KC - 1)) P.prof[(size_t)(kc ? 28 : 27) * PROF_WIN + (e - PROF_S0)] = gtimer();
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(whi0 + kc * 16384), bd = sdesc_sw128(ring0 + st * CHUNK);
+          if (LO_TMEM && CHUNK_ASM) {  // W_lo.x_hi accumulates into the x_hi columns
+            if (kc < nlo)  // both weight halves from TMEM
+              mma_chunk_tt(d1, tmem + WLO_COL + kc * 32, tmem + WLO_COL + (KC + kc) * 32, bd, kc == 0, ID64, ID32,
+                           &sm.empty[st]);
+            else
+              mma_chunk_ts(d1, tmem + WLO_COL + kc * 32, ad, bd, kc == 0, ID64, ID32, &sm.empty[st]);
+          } else if (LO_TMEM && kc < nlo) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint32_t acc = (kc | k) != 0;
-            if (SWAP_HILO) {  // W_hi from TMEM (N = 64), W_lo from smem (N = 32)
-              mma_ts(d1, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID64, acc);
-              mma_ss(d2, ad + 2 * k, bd + 2 * k, ID32, acc);
-            } else {
-              mma_ss(d1, ad + 2 * k, bd + 2 * k, ID64, acc);
-              mma_ts(d2, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID32, acc);
+            for (int k = 0; k < 4; ++k) {
+              mma_ts(d1, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID64, (kc | k) != 0);
+              mma_ts(d2, tmem + WLO_COL + (KC + kc) * 32 + k * 8, bd + 2 * k, ID32, 1u);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t acc = (kc | k) != 0;
+              if (SWAP_HILO) {  // W_hi from TMEM (N = 64), W_lo from smem (N = 32)
+                mma_ts(d1, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID64, acc);
+                mma_ss(d2, ad + 2 * k, bd + 2 * k, ID32, LO_TMEM ? 1u : acc);
+              } else {
+                mma_ss(d1, ad + 2 * k, bd + 2 * k, ID64, acc);
+                mma_ts(d2, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID32, acc);
+              }
             }
           }
-          mma_commit(&sm.empty[st]);
+          if (!(LO_TMEM && CHUNK_ASM)) mma_commit(&sm.empty[st]);
         }
       }
       mma_commit(&sm.accf[set]);
@@ -1496,122 +1590,6 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
       if (stamp_ip) reinterpret_cast<volatile unsigned long long*>(sm.misc + 8)[2] = gtimer();
     }
   } else {
-#else
-  if (warp == 0) {
-    // ================= producer: stream input chunks into the ring =================
-    if (lane == 0) {
-      // ring stage, the empty-barrier parity of its previous use (a stage's k-th
-      // reuse waits for parity (k - 1) & 1), stages filled once
-      int ps = 0, pph = 1, pfill = 0;
-      const unsigned* cb = P.cnt + (size_t)cidx_act(in_buf, 0) * CSTRIDE;
-      // every parameter the loop needs, read once: kernel-parameter (constant
-      // bank) reads inside the loop cost ~100+ cycles each here
-      unsigned np[MAXKC];
-#pragma unroll
-      for (int kc = 0; kc < MAXKC; ++kc) np[kc] = kc < KC ? (unsigned)P.nprod[in_buf][kc] : 0u;
-      const CUtensorMap* lmap = &P.ldmap[in_buf];
-      const bool stamp_ip = P.prof && (role == ROLE_I || role == ROLE_P) && (int)blockIdx.x == P.prof_first[role];
-      const bool ctr = P.prof && (role == ROLE_J || role == ROLE_I) && (int)blockIdx.x == P.prof_first[role];
-      const bool trj = P.prof && role == ROLE_J && (int)blockIdx.x == P.prof_first[role];
-      unsigned long long* const prof = P.prof;
-      for (int r = 0;; ++r) {
-        mbar_wait_sleep(sm.cmd, r & 1);
-        const int e = ((volatile int*)sm.misc)[r & 1];
-        if (e < 0) break;
-        const bool tr = trj && e >= PROF_S0 && e < PROF_S0 + PROF_WIN;
-        // poll every outstanding chunk counter at once (one L2 round trip per
-        // poll, not one per chunk), then stream all ready chunks in order
-        int next = 0, npoll = 0;
-        while (next < KC) {
-          unsigned v[MAXKC];
-#pragma unroll
-          for (int kc = 0; kc < MAXKC; ++kc)
-            v[kc] = (kc >= next && kc < KC) ? ld_relaxed(cb + kc * CSTRIDE) : 0u;
-          int ready = next;
-#pragma unroll
-          for (int kc = 0; kc < MAXKC; ++kc)
-            if (kc == ready && kc < KC && v[kc] >= np[kc] * (unsigned)(e + 1)) ++ready;
-          if (ctr) ++npoll;
-          if (ready == next) {
-            if (POLL_NS) __nanosleep(POLL_NS);
-            continue;
-          }
-          if (ctr && next == 0) sm.dbg[10] = npoll;  // polls until chunk 0 was ready
-          fence_proxy_global();
-          for (int kc = next; kc < ready; ++kc) {
-            if (tr && (kc == 0 || kc == KC - 1)) prof[(size_t)(kc ? 13 : 12) * PROF_WIN + (e - PROF_S0)] = gtimer();
-            if ((kc == 0 || kc == KC - 1) && stamp_ip)  // stamped per round, logged by the epilogue
-              reinterpret_cast<volatile unsigned long long*>(sm.misc + 8)[kc ? 1 : 0] = gtimer();
-            const int s = ps;
-            if (ctr && kc == 2) sm.dbg[12] = clock64();
-            if (pfill >= NSTAGE) mbar_wait_sleep(&sm.empty[s], (uint32_t)pph);
-            if (ctr) sm.dbg[kc] = clock64();
-            mbar_arrive_expect_tx(&sm.full[s], CHUNK);
-#if TMA_ACT
-            tma_ld2(sm.ring + s * CHUNK, lmap, 64 * kc, 64 * (e & 1), &sm.full[s]);
-#else
-            bulk_g2s(sm.ring + s * CHUNK, P.act[in_buf] + ((size_t)(e & 1) * KC + kc) * CHUNK, CHUNK, &sm.full[s]);
-#endif
-            if (ctr && kc == 2) sm.dbg[13] = clock64();
-            if (pfill < NSTAGE) ++pfill;
-            if (++ps == NSTAGE) {
-              ps = 0;
-              pph ^= 1;
-            }
-          }
-          next = ready;
-        }
-        if (ctr) sm.dbg[11] = npoll;
-      }
-    }
-  } else if (warp == 1) {
-    // ================= MMA issuer (converged warp) =================
-    int cs = 0, cph = 0;  // ring stage consumed next, its full-barrier phase
-    constexpr uint32_t ID64 = idesc_f16(128, 64), ID32 = idesc_f16(128, 32);
-    const uint32_t whi0 = smem_u32(sm.whi), ring0 = smem_u32(sm.ring);
-    for (int r = 0;; ++r) {
-      mbar_wait_sleep(sm.cmd, r & 1);
-      const int e = ((volatile int*)sm.misc)[r & 1];
-      if (e < 0) break;
-      const int set = r & 1;
-      if (r >= 2) mbar_wait_sleep(&sm.acce[set], (uint32_t)(((r >> 1) - 1) & 1));
-      tc_fence_after();
-      const uint32_t d1 = tmem + set * ACC_COLS, d2 = d1 + 64;
-      const bool ctr = P.prof && (role == ROLE_J || role == ROLE_I) && (int)blockIdx.x == P.prof_first[role];
-      const bool tr = P.prof && role == ROLE_J && (int)blockIdx.x == P.prof_first[role] && e >= PROF_S0 &&
-                      e < PROF_S0 + PROF_WIN && lane == 0;
-      for (int kc = 0; kc < KC; ++kc) {
-        const int s = cs;
-        mbar_wait_sleep(&sm.full[s], (uint32_t)cph);
-        if (ctr && lane == 0) sm.dbg[16 + kc] = clock64();
-        if (tr && (kc == 0 || kc == KC - 1)) P.prof[(size_t)(kc ? 28 : 27) * PROF_WIN + (e - PROF_S0)] = gtimer();
-        tc_fence_after();
-        const uint64_t ad = sdesc_sw128(whi0 + kc * 16384), bd = sdesc_sw128(ring0 + s * CHUNK);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t acc = (kc | k) != 0;
-          if (SWAP_HILO) {  // W_hi from TMEM (N = 64), W_lo from smem (N = 32)
-            mma_ts(d1, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID64, acc);
-            mma_ss(d2, ad + 2 * k, bd + 2 * k, ID32, acc);
-          } else {
-            mma_ss(d1, ad + 2 * k, bd + 2 * k, ID64, acc);
-            mma_ts(d2, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID32, acc);
-          }
-        }
-        mma_commit(&sm.empty[s]);
-        if (++cs == NSTAGE) {
-          cs = 0;
-          cph ^= 1;
-        }
-      }
-      mma_commit(&sm.accf[set]);
-      if (ctr && lane == 0) sm.dbg[31] = clock64();
-      if (tr) P.prof[(size_t)29 * PROF_WIN + (e - PROF_S0)] = gtimer();
-      if (P.prof && (role == ROLE_I || role == ROLE_P) && (int)blockIdx.x == P.prof_first[role] && lane == 0)
-        reinterpret_cast<volatile unsigned long long*>(sm.misc + 8)[2] = gtimer();
-    }
-  } else {
-#endif
     // ================= epilogue + replicated control (128 threads) =================
     Epi e(P, sm, tmem, tid - 64, warp & 3, role, layer, tile, wsc);
     e.run_role();

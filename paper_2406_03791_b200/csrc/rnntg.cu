@@ -534,7 +534,13 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   // ---- weight images: W_hi [KC][128 x 64] swizzled, then W_lo [K/2][128] packed pairs ----
   const auto& w = m->host_w;
   const int bse = 1 + 3 * L;
-  const size_t wstride = (size_t)KCmax * 16384 + (size_t)KCmax * 32 * 128 * 4;
+  // per CTA: [KCmax][16 KB] smem image, then TMEM column pairs (u32 = 2 fp16
+  // along k) for 128 lanes: the KC chunks' TMEM-resident half, then W_lo of
+  // the first nlo_chunks(KC) chunks (ptc::LO_TMEM)
+  const size_t wtoff = (size_t)KCmax * 16384;
+  int tcols = 0;
+  for (int kc : {Hp / 64, Jp / 64}) tcols = std::max(tcols, (kc + ptc::nlo_chunks(kc)) * 32);
+  const size_t wstride = wtoff + (size_t)tcols * 128 * 4;
   std::vector<unsigned char> img((size_t)G * wstride, 0);
   std::vector<float> row(ptc::MAXKP);
   for (int c = 0; c < G; ++c) {
@@ -580,21 +586,25 @@ rnntg_status setup_tc(rnntg_decoder* d) {
     std::memcpy(&invbits, &inv, 4);
     roles[c].w = invbits;
     unsigned char* hi = img.data() + (size_t)c * wstride;
-    uint32_t* lo = reinterpret_cast<uint32_t*>(hi + (size_t)KCmax * 16384);
+    uint32_t* lo = reinterpret_cast<uint32_t*>(hi + wtoff);
+    const int kcr = Kp / 64, nlo = ptc::nlo_chunks(kcr);
     for (int mm = 0; mm < 128; ++mm) {
       for (int k = 0; k < Kp; ++k) row[k] = wel(mm, k) * scale;
       for (int k = 0; k < Kp; k += 2) {
         // smem image <- W_hi and TMEM pairs <- W_lo (ptc::SWAP_HILO: the reverse)
-        uint16_t lb[2];
+        uint16_t lb[2], sb[2];
         for (int j = 0; j < 2; ++j) {
           const float v = row[k + j];
           uint16_t hb = f2h_bits(v);
           uint16_t l = f2h_bits(v - h2f(hb));
           if (ptc::SWAP_HILO) std::swap(hb, l);
           lb[j] = l;
+          sb[j] = hb;
           std::memcpy(hi + (size_t)((k + j) / 64) * 16384 + ptc::swz(mm, (k + j) % 64), &hb, 2);
         }
         lo[(size_t)(k / 2) * 128 + mm] = (uint32_t)lb[0] | ((uint32_t)lb[1] << 16);
+        if (k / 64 < nlo)  // this chunk's smem-image half is TMEM-resident too
+          lo[(size_t)(kcr * 32 + k / 2) * 128 + mm] = (uint32_t)sb[0] | ((uint32_t)sb[1] << 16);
       }
     }
   }
@@ -626,6 +636,7 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   CK(upload(d->mem, &dimg, img));
   tp.wimg = dimg;
   tp.wstride = wstride;
+  tp.wtoff = wtoff;
   for (int l = 0; l < L; ++l) {
     float* db = nullptr;
     CK(upload(d->mem, &db, w[3 + 3 * l]));

@@ -8,6 +8,13 @@
 //   c6  TS N=96 only        c7  SS N=96 only
 //   c8  TS N=64 + TS N=32   (both A operands in TMEM)
 //   c9  SS N=64 + SS N=32   (both in smem)
+//   c10 TS N=64 M=64        c11 SS N=32 M=64     c12 TS N=64 + SS N=32, M=64
+//   c13 SS N=64 + SS N=32, M=64
+//   c14 TS N=64 + TS N=32 into the SAME accumulator columns 0..31
+//   c15 TS N=64 + SS N=32 into the same columns
+//   c16 executor layout, LO_TMEM: D cols 0..63, W_hi A at 64 + 8 ks, W_lo A at 384 + 8 ks
+//       for ks < 16 (TS + TS), SS W_lo for ks >= 16, all into D
+//   c17 executor layout before: D1 0..63, D2 64..95, W_hi A at 192 + 8 ks (TS), SS W_lo into D2
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o scripts/mb_mma scripts/mb_mma.cu
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -66,7 +73,7 @@ constexpr int KSTEPS = 40;
 template <int C>
 __global__ void __launch_bounds__(128, 1) k_mma(long long* out, int reps) {
   // smem: A (W) [10 chunks][16 KB] at 0, B ring [4][8 KB] at 160 KB, barrier after
-  uint64_t* bar = reinterpret_cast<uint64_t*>(dsm + 160 * 1024 + 32 * 1024);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(dsm + 160 * 1024 + 48 * 1024);  // ring + N=96 overrun room
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
@@ -87,7 +94,7 @@ __global__ void __launch_bounds__(128, 1) k_mma(long long* out, int reps) {
     long long tot = 0;
     for (int r = 0; r < reps; ++r) {
       const long long t0 = clock64();
-#pragma unroll 4
+#pragma unroll
       for (int ks = 0; ks < KSTEPS; ++ks) {
         const int kc = ks >> 2, k = ks & 3, st = kc & 3;
         const uint64_t ad = sdesc(a0 + kc * 16384) + 2 * k, bd = sdesc(b0 + st * 8192) + 2 * k;
@@ -103,6 +110,21 @@ __global__ void __launch_bounds__(128, 1) k_mma(long long* out, int reps) {
         if (C == 7) mma_ss(d1, ad, bd, idesc_f16(128, 96), acc);
         if (C == 8) { mma_ts(d1, at, bd, idesc_f16(128, 64), acc); mma_ts(d2, at, bd, idesc_f16(128, 32), acc); }
         if (C == 9) { mma_ss(d1, ad, bd, idesc_f16(128, 64), acc); mma_ss(d2, ad, bd, idesc_f16(128, 32), acc); }
+        if (C == 10) mma_ts(d1, at, bd, idesc_f16(64, 64), acc);
+        if (C == 11) mma_ss(d2, ad, bd, idesc_f16(64, 32), acc);
+        if (C == 12) { mma_ts(d1, at, bd, idesc_f16(64, 64), acc); mma_ss(d2, ad, bd, idesc_f16(64, 32), acc); }
+        if (C == 16) {
+          mma_ts(tmem, tmem + 64 + ks * 8, bd, idesc_f16(128, 64), acc);
+          if (ks < 16) mma_ts(tmem, tmem + 384 + ks * 8, bd, idesc_f16(128, 32), 1);
+          else mma_ss(tmem, ad, bd, idesc_f16(128, 32), 1);
+        }
+        if (C == 17) {
+          mma_ts(tmem, tmem + 192 + ks * 8, bd, idesc_f16(128, 64), acc);
+          mma_ss(tmem + 64, ad, bd, idesc_f16(128, 32), acc);
+        }
+        if (C == 14) { mma_ts(d1, at, bd, idesc_f16(128, 64), acc); mma_ts(d1, at, bd, idesc_f16(128, 32), 1); }
+        if (C == 15) { mma_ts(d1, at, bd, idesc_f16(128, 64), acc); mma_ss(d1, ad, bd, idesc_f16(128, 32), 1); }
+        if (C == 13) { mma_ss(d1, ad, bd, idesc_f16(64, 64), acc); mma_ss(d2, ad, bd, idesc_f16(64, 32), acc); }
       }
       commit(bar);
       mwait(bar, r & 1);
@@ -121,11 +143,11 @@ __global__ void __launch_bounds__(128, 1) k_mma(long long* out, int reps) {
 
 template <int C>
 void run(const char* name, long long* dout) {
-  const int smem = 160 * 1024 + 32 * 1024 + 64;
+  const int smem = 160 * 1024 + 48 * 1024 + 64;
   CK(cudaFuncSetAttribute(k_mma<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   k_mma<C><<<1, 128, smem>>>(dout, 20);
   CK(cudaDeviceSynchronize());
-  long long h[16];
+  long long h[32];
   CK(cudaMemcpy(h, dout, sizeof(h), cudaMemcpyDeviceToHost));
   printf("%-26s %6lld cycles / 40 k-steps = %5.1f per k-step\n", name, h[C], h[C] / 40.0);
 }
@@ -133,17 +155,25 @@ void run(const char* name, long long* dout) {
 int main() {
   setvbuf(stdout, NULL, _IONBF, 0);
   long long* dout;
-  CK(cudaMalloc(&dout, 16 * 8));
-  CK(cudaMemset(dout, 0, 16 * 8));
+  CK(cudaMalloc(&dout, 32 * 8));
+  CK(cudaMemset(dout, 0, 32 * 8));
   run<0>("c0 TS64 + SS32 (today)", dout);
   run<1>("c1 SS64 + TS32", dout);
   run<2>("c2 TS64", dout);
   run<3>("c3 SS32", dout);
   run<4>("c4 SS64", dout);
   run<5>("c5 TS32", dout);
+  run<16>("c16 executor LO_TMEM layout", dout);
+  run<17>("c17 executor previous layout", dout);
+  run<14>("c14 TS64 + TS32 same D", dout);
+  run<15>("c15 TS64 + SS32 same D", dout);
   run<6>("c6 TS96", dout);
   run<7>("c7 SS96", dout);
-  run<8>("c8 TS64 + TS32", dout);
   run<9>("c9 SS64 + SS32", dout);
+  run<11>("c11 SS32 M64", dout);
+  run<13>("c13 SS64 + SS32 M64", dout);
+  run<10>("c10 TS64 M64", dout);
+  run<12>("c12 TS64 + SS32 M64", dout);
+  run<8>("c8 TS64 + TS32", dout);
   return 0;
 }

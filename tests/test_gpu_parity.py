@@ -137,6 +137,27 @@ def test_lstm_golden(golden, idx, exec):
     assert rep.ok, rep.failures
 
 
+@pytest.mark.parametrize("H,J,tdt", [(96, 200, False), (320, 640, True), (640, 192, False)])
+def test_tensor_mixed_chunk_counts(H, J, tdt):
+    """Tensor executor with hidden and joint widths padding to different chunk
+    counts (the per-CTA weight image is laid out for the larger one; W_lo is
+    TMEM-resident for a width-dependent number of leading chunks)."""
+    _need_gpu()
+    d = O.Dims(300, H, H, J, 40, (0, 1, 2, 3, 4) if tdt else (), O.CELL_LSTM, 2)
+    p = O.init_params(11, d)
+    B, T, ms = 8, 30, 4
+    x = O.fill_uniform(12, -1.0, 1.0, (B, T, d.feature))
+    lens = np.array([T - (3 * i) % 9 for i in range(B)], np.int32)
+    algo = DecodeAlgo.TdtLabelLoop if tdt else DecodeAlgo.FrameSync
+    m = Model(to_model_dims(d), p)
+    got = D.replay_decode(D.build_decode_graph(m, algo, B, T, ms, D.Exec.Tensor), x, lens)
+    ref = O.decode_batch(d, p, x, lens, ms, tdt, record=True)
+    rep = compare_batch(got, ref, d.vocab, tdt, f"mixed H{H} J{J}")
+    print(f"\nmixed H{H} J{J}: {rep.exact}/{rep.utterances} exact, max score rel {rep.max_score_rel:.2e}")
+    assert rep.ok, rep.failures
+    m.close()
+
+
 @pytest.mark.parametrize("cell,layers,tdt", [("tanh", 1, False), ("lstm", 2, True),
                                               ("lstm", 1, False), ("lstm", 3, True)])
 def test_step_joint_and_prediction(cell, layers, tdt):
