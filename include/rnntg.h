@@ -141,6 +141,12 @@ rnntg_status rnntg_read(rnntg_decoder* d, int32_t* counts, int32_t* tokens,
                         int32_t* frames, float* scores, int32_t* durations,
                         int cap);
 rnntg_status rnntg_get_stats(rnntg_decoder* d, rnntg_stats* s);
+/* Host-side work of the last decode, for the reference's TimingReport
+ * (engine.hpp:119-128): device->host synchronisations the host waited on
+ * (rnntg_sync and, for RNNTG_EXEC_HOSTLOOP, one per inner step), host launch
+ * calls (kernels + graph launches) and graph launches.  Counted since the last
+ * rnntg_launch; read after rnntg_read / rnntg_sync. */
+rnntg_status rnntg_host_counts(rnntg_decoder* d, int64_t* syncs, int64_t* launches, int64_t* graph_launches);
 /* The decoder's CUDA stream (cudaStream_t), for callers that overlap work. */
 void* rnntg_decoder_stream(rnntg_decoder* d);
 

@@ -56,6 +56,17 @@ Hypotheses tdt_label_looping_decode(Engine& engine, const DecoderModel& model, c
 CapturedDecoder build_decode_graph(Engine& engine, const DecoderModel& model, DecodeAlgo algo,
                                    int batch, int max_frames, int max_symbols);
 Hypotheses replay_decode(CapturedDecoder& captured, const Tensor& x, const Tensor& out_len);
+/// replay_decode plus the reference's TimingReport (engine.hpp:119-128) of
+/// this decode, measured on the device instead of simulated: CUPTI kernel
+/// activity gives span_us (first kernel start -> last kernel end),
+/// device_busy_us (union of kernel intervals, graph kernel nodes counted
+/// individually), idle_fraction = 1 - busy/span and num_kernels; the host
+/// wall time of the launch call is host_busy_us; num_syncs / num_graph_launches
+/// come from the library's host counters (rnntg_host_counts).  The report feeds
+/// the reference's compare_runs / speedup_table_csv (analysis.cpp:112-154)
+/// unchanged.  Throws StateError for an uninitialized capture.
+Hypotheses replay_decode_timed(CapturedDecoder& captured, const Tensor& x, const Tensor& out_len,
+                               TimingReport* report);
 /// Joint-step evaluations of the last CUDA decode issued with this engine.
 int64_t decode_joint_evals(const Engine& engine);
 

@@ -80,6 +80,9 @@ constexpr int NROLES = 5;
 #ifndef WORD_READBACK
 #define WORD_READBACK 0  // A/B: no gain
 #endif
+#ifndef EARLY_GATHER
+#define EARLY_GATHER 1  // rules warp's table0 loads go out before the rules
+#endif
 #ifndef LAZY_BATCH_NS
 #define LAZY_BATCH_NS 0
 #endif
@@ -943,12 +946,8 @@ struct Epi {
         // (warp-wide strong loads are serviced ~100 cycles apart: a 9-16 load
         // batch per poll made each poll ~1 us; one load per poll is ~360 cycles)
         while ((unsigned)(ld_poll_u64(wv + (nj - 1) * 32 * PW_STRIDE) >> 32 & 0xffu) != tg) ++npoll;
-        if (role == ROLE_R && layer == 0 && b == 0) {
-          mark(30);
-          gmark(54);  // last tile's word seen
-        }
+        if (role == ROLE_R && layer == 0 && b == 0) mark(30);  // last tile's word seen
 #endif
-        const int nspin = npoll;
 #if LAZY_BATCH_NS
         // the CTAs off the critical path read the tile words after R_0 did:
         // 75 CTAs reading the same 18 lines at once made R_0's read ~3x slower
@@ -979,11 +978,7 @@ struct Epi {
           ok = bad == 0u;
           if (!ok && lazy && LAZY_NS) __nanosleep(LAZY_NS);
         } while (!ok);
-        if (role == ROLE_R && layer == 0 && b == 0) {
-          mark(31);
-          gmark(55);  // every tile's word seen
-          if (tracer && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) P.prof[(size_t)15 * PROF_WIN + (s - PROF_S0)] = npoll - nspin;
-        }
+        if (role == ROLE_R && layer == 0 && b == 0) mark(31);  // every tile's word seen
         npoll_out = npoll;
         lat1_out = lat1;
         best = -INFINITY;
@@ -1014,9 +1009,13 @@ struct Epi {
         P.prof[(size_t)38 * PROF_WIN + (s - PROF_S0)] = (unsigned long long)lat1_out;
       if (role == ROLE_R && layer == 0) {
         // hand the labels to the other 7 epilogue warps now: their table0
-        // gathers for the layer-0 cell overlap the rules below
+        // gathers for the layer-0 cell overlap the rules below; this warp's
+        // own gather (rows 0..15, labels of lanes 0..15) goes out first too
         __syncwarp();
         asm volatile("barrier.cta.arrive.aligned 2, 256;" ::: "memory");
+#if EARLY_GATHER
+        gather_table0();
+#endif
         mark(22);
         gmark(43);
       }
@@ -1130,7 +1129,7 @@ struct Epi {
     }
     epi_sync();
     if (role == ROLE_R && layer == 0) mark2(37);
-    if (role == ROLE_R && layer == 0 && et < 32) gather_table0();
+    if (!EARLY_GATHER && role == ROLE_R && layer == 0 && et < 32) gather_table0();
     const int o = sm.misc[5];
     acc_any = o & 1;
     finish = (o >> 1) & 1;

@@ -86,6 +86,12 @@ struct rnntg_decoder {
   cudaStream_t stream = nullptr;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
+  // persistent executors: encoder projection + counter resets + the
+  // cooperative kernel captured once, replayed by one cudaGraphLaunch (the
+  // host otherwise leaves the GPU idle between the projection and the
+  // persistent kernel for the duration of the cooperative-launch call)
+  cudaGraphExec_t lexec = nullptr;
+  bool ltried = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool bound = false, launched = false;
   float* x_dev = nullptr;  // [B*T][Fp] pitched, zero-padded features
@@ -105,6 +111,8 @@ struct rnntg_decoder {
   size_t tcnt_bytes = 0, tpw_bytes = 0;
   // sync-requiring host-loop baseline: pinned mirror of the control block
   Ctrl* hctrl = nullptr;
+  // host-side work of the last decode (TimingReport.num_syncs / launches)
+  int64_t n_syncs = 0, n_launches = 0, n_graph_launches = 0;
 };
 
 namespace {
@@ -736,6 +744,7 @@ rnntg_status run_hostloop(rnntg_decoder* d) {
   const int nrb = s.nrb;
   Ctrl* hc = d->hctrl;
   auto pred = [&]() -> cudaError_t {
+    d->n_launches += M.L + 1;
     for (int l = 0; l < M.L; ++l) {
       if (M.cell == RNNTG_CELL_LSTM)
         pred_layer_kernel<1><<<dim3(M.GH / CT, nrb), NT, layer_smem(M, l), st>>>(M, s, l);
@@ -746,14 +755,17 @@ rnntg_status run_hostloop(rnntg_decoder* d) {
     return cudaGetLastError();
   };
   auto joint = [&]() -> cudaError_t {
+    ++d->n_launches;
     joint_kernel<<<dim3(M.NCHT, nrb), NT, joint_smem(M), st>>>(M, s);
     return cudaGetLastError();
   };
   auto flags = [&]() -> cudaError_t {  // the per-step device -> host sync
+    ++d->n_syncs;
     cudaError_t e = cudaMemcpyAsync(hc, s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st);
     return e != cudaSuccess ? e : cudaStreamSynchronize(st);
   };
   CK(encproj_launch(d->enc, st));
+  d->n_launches += 2;
   prologue_kernel<<<148, 256, 0, st>>>(M, s);
   CK(cudaGetLastError());
   CK(pred());  // P0 = pred(blank, 0)
@@ -765,6 +777,7 @@ rnntg_status run_hostloop(rnntg_decoder* d) {
         CK(pred());
         CK(flags());
       } while (hc->any && !hc->abort);
+      ++d->n_launches;
       frame_tail_kernel<<<1, 256, 0, st>>>(M, s);
       CK(cudaGetLastError());
       CK(flags());
@@ -1064,6 +1077,7 @@ rnntg_status rnntg_decoder_destroy(rnntg_decoder* d) {
   cudaSetDevice(d->m->device);
   if (d->stream) cudaStreamSynchronize(d->stream);
   if (d->gexec) cudaGraphExecDestroy(d->gexec);
+  if (d->lexec) cudaGraphExecDestroy(d->lexec);
   if (d->graph) cudaGraphDestroy(d->graph);
   if (d->ev0) cudaEventDestroy(d->ev0);
   if (d->ev1) cudaEventDestroy(d->ev1);
@@ -1118,19 +1132,51 @@ rnntg_status rnntg_bind_device(rnntg_decoder* d, const float* x_dev, const int32
   return RNNTG_OK;
 }
 
+// issue the persistent executors' launch sequence on st
+cudaError_t issue_persistent(rnntg_decoder* d, cudaStream_t st) {
+  cudaError_t e = encproj_launch(d->enc, st);
+  if (e != cudaSuccess) return e;
+  if (d->exec == RNNTG_EXEC_TENSOR) return launch_tc(d, st);
+  void* args[1] = {&d->pp};
+  return cudaLaunchCooperativeKernel((const void*)pk::persistent_kernel, dim3(d->pp.G), dim3(pk::NTH), args, d->psmem,
+                                     st);
+}
+
+// capture issue_persistent into d->lexec once; on any failure the direct
+// launches stay in use (the capture leaves no error state behind)
+void capture_persistent(rnntg_decoder* d) {
+  d->ltried = true;
+  if (!env_flag("RNNTG_LAUNCH_GRAPH", true)) return;
+  cudaGraph_t g = nullptr;
+  if (cudaStreamBeginCapture(d->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  const cudaError_t e = issue_persistent(d, d->stream);
+  const cudaError_t e2 = cudaStreamEndCapture(d->stream, &g);
+  if (e != cudaSuccess || e2 != cudaSuccess || !g || cudaGraphInstantiate(&d->lexec, g, 0) != cudaSuccess)
+    d->lexec = nullptr;
+  if (g) cudaGraphDestroy(g);
+  cudaGetLastError();
+}
+
 rnntg_status rnntg_launch(rnntg_decoder* d) {
   if (!d) return fail(RNNTG_E_STATE, "decoder is null");
   if (!d->bound) return fail(RNNTG_E_STATE, "captured decoder is not initialized (no inputs bound)");
   CK(cudaSetDevice(d->m->device));
+  if ((d->exec == RNNTG_EXEC_PERSISTENT || d->exec == RNNTG_EXEC_TENSOR) && !d->ltried) capture_persistent(d);
   CK(cudaEventRecord(d->ev0, d->stream));
-  if (d->exec == RNNTG_EXEC_PERSISTENT) {
-    CK(encproj_launch(d->enc, d->stream));
-    void* args[1] = {&d->pp};
-    CK(cudaLaunchCooperativeKernel((const void*)pk::persistent_kernel, dim3(d->pp.G), dim3(pk::NTH),
-                                   args, d->psmem, d->stream));
-  } else if (d->exec == RNNTG_EXEC_TENSOR) {
-    CK(encproj_launch(d->enc, d->stream));
-    CK(launch_tc(d, d->stream));
+  d->n_syncs = d->n_graph_launches = 0;
+  d->n_launches = d->exec == RNNTG_EXEC_PERSISTENT || d->exec == RNNTG_EXEC_TENSOR ? 2 : 0;
+  if (d->exec == RNNTG_EXEC_GRAPH) d->n_launches = d->n_graph_launches = 1;
+  if (d->exec == RNNTG_EXEC_PERSISTENT || d->exec == RNNTG_EXEC_TENSOR) {
+    if (d->lexec) {
+      CK(cudaGraphLaunch(d->lexec, d->stream));
+      d->n_graph_launches = 1;
+      d->n_launches = 1;
+    } else {
+      CK(issue_persistent(d, d->stream));
+    }
   } else if (d->exec == RNNTG_EXEC_HOSTLOOP) {
     const rnntg_status st = run_hostloop(d);
     if (st) return st;
@@ -1146,6 +1192,7 @@ rnntg_status rnntg_sync(rnntg_decoder* d) {
   if (!d) return fail(RNNTG_E_STATE, "decoder is null");
   CK(cudaSetDevice(d->m->device));
   CK(cudaStreamSynchronize(d->stream));
+  if (d->launched) ++d->n_syncs;
   if (d->launched) {
     int err = 0;
     CK(cudaMemcpy(&err, &d->st.ctrl->err, sizeof(int), cudaMemcpyDeviceToHost));
@@ -1173,6 +1220,14 @@ rnntg_status rnntg_read(rnntg_decoder* d, int32_t* counts, int32_t* tokens, int3
   CK(copy2d(frames, d->st.frames, 4));
   CK(copy2d(scores, d->st.scores, 4));
   CK(copy2d(durations, d->st.durs, 4));
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_host_counts(rnntg_decoder* d, int64_t* syncs, int64_t* launches, int64_t* graph_launches) {
+  if (!d || !syncs || !launches || !graph_launches) return fail(RNNTG_E_STATE, "null argument");
+  *syncs = d->n_syncs;
+  *launches = d->n_launches;
+  *graph_launches = d->n_graph_launches;
   return RNNTG_OK;
 }
 

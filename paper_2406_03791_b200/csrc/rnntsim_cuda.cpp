@@ -5,6 +5,7 @@
 #include "rnntsim_cuda.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -130,6 +131,12 @@ struct Handle {
   }
 };
 
+// replay_decode_timed: the decoder whose inputs this thread bound last, and
+// the decode region (CUPTI window + host clock) opened right before its launch
+thread_local Handle* t_bound = nullptr;
+thread_local bool t_timed = false;
+thread_local std::chrono::steady_clock::time_point t_launch0;
+
 Hypotheses read(Handle& h) {
   const int B = h.batch, cap = rnntg_decoder_capacity(h.d);
   std::vector<int32_t> cnt(B), tok((size_t)B * cap), frm((size_t)B * cap);
@@ -201,6 +208,11 @@ CapturedDecoder build_decode_graph(Engine& engine, const DecoderModel& model, De
                                                                  const Tensor& out_len) {
     validate(x, out_len, batch, max_frames, feature, max_symbols);
     check(rnntg_bind(h->d, x.f32().data(), out_len.i32().data()));
+    t_bound = h.get();
+    if (t_timed) {  // the decode region starts at the launch, inputs already on the device
+      check(rnntg_trace_begin());
+      t_launch0 = std::chrono::steady_clock::now();
+    }
     check(rnntg_launch(h->d));
   };
   cap.read_hypotheses = [h]() { return read(*h); };
@@ -212,6 +224,41 @@ Hypotheses replay_decode(CapturedDecoder& captured, const Tensor& x, const Tenso
     throw StateError("captured decoder is not initialized");
   captured.bind_inputs(x, out_len);
   return captured.read_hypotheses();
+}
+
+Hypotheses replay_decode_timed(CapturedDecoder& captured, const Tensor& x, const Tensor& out_len,
+                               TimingReport* report) {
+  if (!captured.engine || !captured.bind_inputs || !captured.read_hypotheses)
+    throw StateError("captured decoder is not initialized");
+  if (!report) throw ValueError("report is null");
+  t_bound = nullptr;
+  t_timed = true;
+  try {
+    captured.bind_inputs(x, out_len);  // validate + H2D, then region start + launch (the whole host loop for HOSTLOOP)
+  } catch (...) {
+    t_timed = false;
+    throw;
+  }
+  t_timed = false;
+  const auto t1 = std::chrono::steady_clock::now();
+  if (!t_bound) throw StateError("captured decoder was not built by rnntsim::cuda");
+  Hypotheses hyps = captured.read_hypotheses();
+  double busy_ms = 0.0, span_ms = 0.0;
+  int64_t kernels = 0;
+  check(rnntg_trace_end(&busy_ms, &span_ms, &kernels));
+  int64_t syncs = 0, launches = 0, graphs = 0;
+  check(rnntg_host_counts(t_bound->d, &syncs, &launches, &graphs));
+  TimingReport r;
+  r.span_us = span_ms * 1e3;
+  r.device_busy_us = busy_ms * 1e3;
+  r.idle_fraction = span_ms > 0.0 ? 1.0 - busy_ms / span_ms : 0.0;
+  r.host_busy_us = std::chrono::duration<double, std::micro>(t1 - t_launch0).count();
+  r.num_kernels = kernels;
+  r.num_syncs = syncs;
+  r.num_permitted_syncs = 0;
+  r.num_graph_launches = graphs;
+  *report = r;
+  return hyps;
 }
 
 Hypotheses greedy_decode_sync_free(Engine& engine, const DecoderModel& model, const Tensor& x,

@@ -66,7 +66,7 @@ iv(23, 24, "R0 (unused)"); iv(6, 7, "I1 decide -> acc ready"); iv(7, 11, "I1 acc
 iv(9, 32, "P acc -> trunk start"); iv(32, 33, "P trunk compute+stores"); iv(33, 34, "P bump epi_sync"); iv(34, 14, "P release + mark")
 
 print("hand-offs (globaltimer medians relative to J post of the step, us):")
-for e, nm in [(40, "P trunk published (prev step)"), (12, "J chunk0 seen"), (41, "R0 decide entered"), (42, "J words stored"), (54, "R0 tile NJ-1 word seen"), (55, "R0 all tile words seen"), (43, "R0 words seen"), (44, "R0 h0 published"), (48, "I1 chunk0 load issued"), (49, "I1 last chunk load issued"),
+for e, nm in [(40, "P trunk published (prev step)"), (12, "J chunk0 seen"), (41, "R0 decide entered"), (42, "J words stored"), (43, "R0 words seen"), (44, "R0 h0 published"), (48, "I1 chunk0 load issued"), (49, "I1 last chunk load issued"),
                 (50, "I1 MMAs issued"), (46, "I1 h1 published"), (51, "P chunk0 load issued"), (52, "P last chunk load issued"),
                 (53, "P MMAs issued")]:
     d = (ev[e] - ev[0]).astype(np.float64); ok = ev[e] > 0
@@ -93,5 +93,3 @@ for base, nm in [(56, "J"), (82, "I1")]:
     print(f"  {nm:3s} data full : {full}")
     print(f"  {nm:3s} MMAs issued {np.median(rel[20]):.0f}, acc read {np.median(rel[21]):.0f}, polls after chunk 0 ready: {np.median(blk[22, ok]):.0f}")
     print(f"  {nm:3s} chunk 2: before empty wait {np.median(rel[23]):.0f}, stamp {np.median(rel[2]):.0f}, after TMA issue {np.median(rel[24]):.0f}")
-bi = allev[15].astype(np.float64)
-print("R0 batch iterations after the spin: median", np.median(bi[bi > 0]), "max", bi.max())

@@ -11,6 +11,7 @@
 
 #include "decode_test_util.hpp"
 #include "lstm_model.hpp"
+#include "rnntsim/analysis.hpp"
 #include "rnntsim/decoders.hpp"
 #include "rnntsim/errors.hpp"
 #include "rnntsim_cuda.hpp"
@@ -141,6 +142,77 @@ int main() {
       report((std::string("dropin errors ") + en).c_str(), ok,
              "ValueError / DimensionError / StateError as in errors.hpp");
     }
+  }
+  // §8(f)3: the reference's TimingReport measured on the device
+  // (cuda::replay_decode_timed, CUPTI) for each executor on a C2-dims batch,
+  // through the reference's own compare_runs / speedup_table_csv
+  // (analysis.cpp:112-154) against the sync-requiring host loop (Alg. 1).
+  {
+    orc_dims d{};
+    d.vocab = 1024;
+    d.embed = d.hidden = 640;
+    d.layers = 2;
+    d.cell = ORC_CELL_LSTM;
+    d.joint = 640;
+    d.feature = 1024;
+    std::vector<std::vector<float>> w(static_cast<size_t>(orc_num_params(&d)));
+    std::vector<float*> wp;
+    for (int i = 0; i < orc_num_params(&d); ++i) {
+      int64_t r, cc;
+      orc_param_size(&d, i, &r, &cc);
+      w[i].resize(static_cast<size_t>(r * cc));
+      wp.push_back(w[i].data());
+    }
+    orc_init_params(1, &d, wp.data());
+    CudaLstm model(d, w);
+    const int B = 32, T = 40, ms = 5;
+    Tensor x(Dtype::Float32, {B, T, 1024});
+    orc_fill_uniform(2, -1.0f, 1.0f, x.f32().data(), x.numel());
+    const Tensor lens = Tensor::from_ints(std::vector<int32_t>(B, T), {B});
+    const double audio_s = B * T * 0.08;  // 80 ms encoder frames (8x subsampled 10 ms features)
+    struct Run {
+      const char* name;
+      rnntg_exec ex;
+      TimingReport rep;
+      Hypotheses hyps;
+    };
+    std::vector<Run> runs = {{"sync-requiring host loop (Alg. 1)", RNNTG_EXEC_HOSTLOOP, {}, {}},
+                             {"conditional-WHILE CUDA graph", RNNTG_EXEC_GRAPH, {}, {}},
+                             {"FFMA persistent kernel", RNNTG_EXEC_PERSISTENT, {}, {}},
+                             {"tcgen05 persistent kernel", RNNTG_EXEC_TENSOR, {}, {}}};
+    bool ok = true;
+    for (Run& r : runs) {
+      cuda::set_executor(r.ex);
+      Engine eng;
+      CapturedDecoder cap = cuda::build_decode_graph(eng, model, DecodeAlgo::FrameSync, B, T, ms);
+      cuda::replay_decode(cap, x, lens);  // warm-up
+      r.hyps = cuda::replay_decode_timed(cap, x, lens, &r.rep);
+      std::printf("timing %-36s %s\n", r.name, timing_report_json(r.rep).c_str());
+      ok = ok && r.rep.span_us > 0.0 && r.rep.num_kernels > 0 && r.rep.device_busy_us <= r.rep.span_us * 1.0001;
+    }
+    const TimingReport& base = runs[0].rep;
+    ok = ok && base.num_syncs > 2 * T;  // a flag readback per inner step
+    // sync-free executors: only the read-back syncs (counts + stats), no per-step ones
+    ok = ok && runs[1].rep.num_graph_launches == 1 && runs[1].rep.num_syncs <= 2;
+    ok = ok && runs[3].rep.num_syncs <= 2 && runs[3].rep.idle_fraction < 0.1;
+    std::vector<SpeedupTableRow> rows;
+    rows.push_back({runs[0].name, rtfx(audio_s, base.span_us * 1e-6), 100.0, 0.0, 1.0, 1.0});
+    for (size_t i = 1; i < runs.size(); ++i) {
+      try {
+        const SpeedupReport s = compare_runs(base, runs[0].hyps, runs[i].rep, runs[i].hyps, 0.0, audio_s);
+        rows.push_back({runs[i].name, s.rtfx_after, 100.0 * s.decoder_fraction_after, s.wer_between,
+                        s.overall_speedup, s.decoder_speedup});
+        ok = ok && s.decoder_speedup > 1.0;
+      } catch (const Error& e) {
+        std::printf("compare_runs(%s): %s\n", runs[i].name, e.what());
+        ok = false;
+      }
+    }
+    std::printf("%s", speedup_table_csv(rows).c_str());
+    report("dropin timing report (f)3", ok,
+           "host-loop idle " + std::to_string(base.idle_fraction) + ", tensor idle " +
+               std::to_string(runs[3].rep.idle_fraction) + ", tensor decoder speed-up " +
+               std::to_string(base.span_us / runs[3].rep.span_us));
   }
   cuda::release_models();
   return g_fail;
