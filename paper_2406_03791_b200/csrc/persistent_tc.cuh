@@ -95,16 +95,21 @@ constexpr bool SWAP_HILO = SWAP_HILO_CFG;
 // cycles resident, 72.6 in the load+MMA pipeline of scripts/mb_pipe2.cu) where
 // TS + SS serialise (63 / 78.2).  TMEM room comes from one 64-column
 // accumulator: W_lo.x_hi accumulates into the W_hi.x_hi columns (same 2^s
-// scale).  Off: inside the executor every LO_TMEM build measured ~2.3 us/step
-// SLOWER (A/B, 18.2 vs 15.9 us), for reasons not pinned down (the slowdown
-// also shows in epilogue sections that do not touch the tensor pipe).
+// scale) or, with LO_SEPD, into its own 32 columns of one 96-column set.
+// Off: inside the executor every LO_TMEM build measured ~2 us/step SLOWER
+// (A/B: same-column 18.2 vs 15.9 us; separate columns 17.4 vs 15.4 us; rolled
+// MMA loops, so not instruction fetch), for reasons not pinned down.
 #define LO_TMEM_CFG 0
 #endif
 constexpr bool LO_TMEM = LO_TMEM_CFG && SWAP_HILO_CFG;
+#ifndef LO_SEPD_CFG
+#define LO_SEPD_CFG 1  // LO_TMEM: W_lo.x_hi into its own 32 columns (no same-column accumulation)
+#endif
+constexpr bool LO_SEPD = LO_TMEM && LO_SEPD_CFG;
 #ifndef CHUNK_ASM
 #define CHUNK_ASM 1  // one elect.sync per chunk of 8 MMAs (see mma_chunk_tt)
 #endif
-constexpr int ACC_COLS = LO_TMEM ? 64 : 96;  // [x_hi | x_lo | lo.x_hi] (LO_TMEM: [x_hi + lo.x_hi | x_lo])
+constexpr int ACC_COLS = LO_TMEM && !LO_SEPD ? 64 : 96;  // [x_hi | x_lo | lo.x_hi] (same-column LO_TMEM: [x_hi + lo.x_hi | x_lo])
 #ifndef NACC_CFG
 #define NACC_CFG 1
 #endif
@@ -192,8 +197,8 @@ struct TParams {
 };
 constexpr int PROF_WIN = 64;  // traced joint steps [PROF_S0, PROF_S0 + PROF_WIN)
 constexpr int PROF_S0 = 100;
-constexpr int NEV = 112;  // 40..47: globaltimer hand-off marks; 48..53: I1/P load + MMA marks;
-                          // 56..80 J / 82..106 I1 per-chunk clock64 (load issue, full, issued, acc)
+constexpr int NEV = 136;  // 40..47: globaltimer hand-off marks; 48..53: I1/P load + MMA marks;
+                          // 56..90 J / 92..126 I1 per-chunk clock64 (load issue, full, issued, acc)
 
 // ------------------------------------------------------------------ PTX
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
@@ -462,14 +467,14 @@ struct Smem {
   uint64_t* cmd;        // [1]
   uint64_t* wbar;       // [1]
   uint32_t* tslot;
-  unsigned long long* dbg;  // [32] per-chunk trace stamps (RNNTG_PROF)
+  unsigned long long* dbg;  // [64] per-chunk trace stamps (RNNTG_PROF)
 };
 
 constexpr int XS_FLOATS = 128 * 33;   // epilogue exchange: [128 cols][33] / [4 gates][32][32]
 constexpr int RED_F4 = 256;           // argmax merge / word staging / sumexp group scratch (4 KB)
 __host__ __device__ inline size_t smem_bytes(int KC) {
   return 1024 /*align slack*/ + (size_t)KC * 16384 + (size_t)NSTAGE * CHUNK + XS_FLOATS * 4 +
-         RED_F4 * 16 + 12 * 32 * 4 + 16 * 4 + 16 * 8 + 64 + 256;
+         RED_F4 * 16 + 12 * 32 * 4 + 16 * 4 + 16 * 8 + 64 + 512;
 }
 
 __device__ inline Smem carve(unsigned char* raw, int KC) {
@@ -597,6 +602,8 @@ struct Epi {
       P.prof[(size_t)(ev0 + 22) * PROF_WIN + (s - PROF_S0)] = t[11] - t[10];  // polls after chunk 0
       P.prof[(size_t)(ev0 + 23) * PROF_WIN + (s - PROF_S0)] = t[12];  // chunk 2: before empty wait
       P.prof[(size_t)(ev0 + 24) * PROF_WIN + (s - PROF_S0)] = t[13];  // chunk 2: after TMA issue
+      for (int k = 0; k < KC && k < 10; ++k)  // chunk landed (observer warp)
+        P.prof[(size_t)(ev0 + 25 + k) * PROF_WIN + (s - PROF_S0)] = t[32 + k];
     }
   }
   // one load+MMA round on this CTA's input at epoch e (-1 = exit)
@@ -609,11 +616,21 @@ struct Epi {
   }
   // accumulator of round r -> v[i] = (W . A)[m][r0 + i] * 2^-s
   __device__ __forceinline__ void read_acc(int r, float (&v)[NR]) {
+    if (tracer && (role == ROLE_J || (role == ROLE_I && layer == 1)) && (et >> 5) == NEPI / 32 - 1) {
+      // trace only: when each chunk of round r lands (full-barrier phase), seen
+      // by an idle epilogue warp rather than the MMA warp
+      const int KC = P.act_kc[role == ROLE_J ? TRUNK : layer - 1];
+      for (int kc = 0; kc < KC && kc < 10; ++kc) {
+        const int st = kc % NSTAGE, uses = (KC - st + NSTAGE - 1) / NSTAGE;
+        mbar_wait(&sm.full[st], (uint32_t)(((long long)r * uses + kc / NSTAGE) & 1));
+        if ((et & 31) == 0) sm.dbg[32 + kc] = clock64();
+      }
+    }
     const int set = NACC == 1 ? 0 : (r & 1);
     mbar_wait_sleep(&sm.accf[set], (uint32_t)(NACC == 1 ? (r & 1) : ((r >> 1) & 1)));
     tc_fence_after();
     const uint32_t a = tq + set * ACC_COLS + r0;
-    if (LO_TMEM) {  // [W_hi.x_hi + W_lo.x_hi | W_hi.x_lo]
+    if (LO_TMEM && !LO_SEPD) {  // [W_hi.x_hi + W_lo.x_hi | W_hi.x_lo]
       uint32_t x0[16], x1[16];
       tmem_ld16(a, x0);
       tmem_ld16(a + 32, x1);
@@ -697,7 +714,7 @@ struct Epi {
     read_acc(round - 1, v);
     mark(1);
     mark(16);
-    if (P.prof) log_chunks(56, clock64());
+    const long long tacc = P.prof ? clock64() : 0;
     // slot reuse: every CTA has finished decide(s - NSLOT); checked once per half window
     if (s >= NSLOT / 2 && s % (NSLOT / 2) == 0)
       wait_counter(cidx_ack(), (unsigned)P.G * (unsigned)(s - NSLOT / 2 + 1));
@@ -840,6 +857,7 @@ struct Epi {
     mark(18);
     gmark(42);
     mark_pub();
+    if (P.prof) log_chunks(56, tacc);  // trace only, after the critical part
     float* xs = sm.xs;  // [128 cols][33]
 #pragma unroll
     for (int i = 0; i < NR; ++i) xs[m * 33 + r0 + i] = v[i];
@@ -984,7 +1002,8 @@ struct Epi {
         best = -INFINITY;
         float bd = -INFINITY;
         int di = 0;
-        // selects, no branches; tiles in column order: strict > keeps the lowest index
+        // selects, no branches; tiles in column order: strict > keeps the lowest
+        // index (a 4-level tree merge measured 0.2 us/step slower)
 #pragma unroll
         for (int t = 0; t < MAXNJ; ++t) {
           const float x = __uint_as_float((unsigned)a[t]);
@@ -1376,7 +1395,7 @@ __device__ __forceinline__ void Epi::run_role() {
             read_acc(round - 1, v);
             mark(7);
             if (layer == 1) log_ld(48);
-            if (P.prof && layer == 1) log_chunks(82, clock64());
+            if (P.prof && layer == 1) log_chunks(92, clock64());
 #pragma unroll
             for (int i = 0; i < NR; ++i) v[i] = (v[i] + x[i]) + bias_m;
           }
@@ -1543,9 +1562,9 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
       if (NACC == 1 && r >= 1) mbar_wait(&sm.acce[0], (uint32_t)((r - 1) & 1));
       if (NACC == 2 && r >= 2) mbar_wait(&sm.acce[set], (uint32_t)(((r >> 1) - 1) & 1));
       tc_fence_after();
-      const uint32_t d1 = tmem + set * ACC_COLS, d2 = LO_TMEM ? d1 : d1 + 64;
+      const uint32_t d1 = tmem + set * ACC_COLS, d2 = LO_TMEM && !LO_SEPD ? d1 : d1 + 64;
       const bool tr = trj && e >= PROF_S0 && e < PROF_S0 + PROF_WIN;
-#pragma unroll
+#pragma unroll  // (a rolled loop measured 0.45 us/step slower)
       for (int kc = 0; kc < MAXKC; ++kc) {
         if (kc < KC) {
           const int st = kc % NSTAGE;
@@ -1555,7 +1574,7 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
           if (tr && (kc == 0 || kc == KC - 1)) P.prof[(size_t)(kc ? 28 : 27) * PROF_WIN + (e - PROF_S0)] = gtimer();
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(whi0 + kc * 16384), bd = sdesc_sw128(ring0 + st * CHUNK);
-          if (LO_TMEM && CHUNK_ASM) {  // W_lo.x_hi accumulates into the x_hi columns
+          if (LO_TMEM && CHUNK_ASM && !LO_SEPD) {  // W_lo.x_hi accumulates into the x_hi columns
             if (kc < nlo)  // both weight halves from TMEM
               mma_chunk_tt(d1, tmem + WLO_COL + kc * 32, tmem + WLO_COL + (KC + kc) * 32, bd, kc == 0, ID64, ID32,
                            &sm.empty[st]);
@@ -1565,7 +1584,7 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               mma_ts(d1, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID64, (kc | k) != 0);
-              mma_ts(d2, tmem + WLO_COL + (KC + kc) * 32 + k * 8, bd + 2 * k, ID32, 1u);
+              mma_ts(d2, tmem + WLO_COL + (KC + kc) * 32 + k * 8, bd + 2 * k, ID32, LO_SEPD ? (kc | k) != 0 : 1u);
             }
           } else {
 #pragma unroll
@@ -1573,14 +1592,14 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
               const uint32_t acc = (kc | k) != 0;
               if (SWAP_HILO) {  // W_hi from TMEM (N = 64), W_lo from smem (N = 32)
                 mma_ts(d1, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID64, acc);
-                mma_ss(d2, ad + 2 * k, bd + 2 * k, ID32, LO_TMEM ? 1u : acc);
+                mma_ss(d2, ad + 2 * k, bd + 2 * k, ID32, LO_TMEM && !LO_SEPD ? 1u : acc);
               } else {
                 mma_ss(d1, ad + 2 * k, bd + 2 * k, ID64, acc);
                 mma_ts(d2, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID32, acc);
               }
             }
           }
-          if (!(LO_TMEM && CHUNK_ASM)) mma_commit(&sm.empty[st]);
+          if (!(LO_TMEM && CHUNK_ASM && !LO_SEPD)) mma_commit(&sm.empty[st]);  // (chunk asm commits itself)
         }
       }
       mma_commit(&sm.accf[set]);

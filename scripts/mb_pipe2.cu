@@ -14,6 +14,9 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
+#include <vector>
+#include <cuda_fp16.h>
 
 #define CK(x)                                                                         \
   do {                                                                                \
@@ -72,6 +75,8 @@ __device__ __forceinline__ bool elect_one() {
   return p != 0;
 }
 
+static __device__ __constant__ int RANDW_DUMMY = 0;
+#define RANDW (SPIN == 2)
 template <int L, int SPIN>
 __global__ void __launch_bounds__(320, 1) k_pipe2(const __grid_constant__ CUtensorMap map, int rounds, long long* out) {
   unsigned char* wsm = dsm;                    // [KC][16 KB] W_lo smem image
@@ -98,6 +103,33 @@ __global__ void __launch_bounds__(320, 1) k_pipe2(const __grid_constant__ CUtens
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
+  if (RANDW) {  // random fp16 weights in smem (W_lo image) and TMEM (W_hi columns)
+    uint32_t st = 777u + threadIdx.x * 7919u;
+    uint32_t* w = reinterpret_cast<uint32_t*>(wsm);
+    for (int i = threadIdx.x; i < KC * 16384 / 4; i += blockDim.x) {
+      st = st * 1664525u + 1013904223u;
+      w[i] = (st & 0x3bff3bffu);  // two fp16 in (-1, 1)
+    }
+    if (warp >= 2 && warp < 6) {
+      const int q = warp & 3;
+      for (int c = 64; c < 512; c += 8) {
+        uint32_t r[8];
+        for (int j = 0; j < 8; ++j) {
+          st = st * 1664525u + 1013904223u;
+          r[j] = st & 0x3bff3bffu;
+        }
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                         tmem + ((uint32_t)(32 * q) << 16) + c),
+                     "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                     : "memory");
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
   constexpr uint32_t ID64 = idesc(128, 64), ID32 = idesc(128, 32);
   if (warp == 0) {
     uint32_t eb = 0;
@@ -161,7 +193,7 @@ __global__ void __launch_bounds__(320, 1) k_pipe2(const __grid_constant__ CUtens
       const long long t1 = clock64();
       if (r >= 2) tot += t1 - t0;
     }
-    if (lane == 0) out[L * 2 + SPIN] = tot / (rounds - 2);
+    if (lane == 0 && blockIdx.x == 0) out[L * 3 + SPIN] = tot / (rounds - 2);
   } else {
     for (int r = 0; r < rounds; ++r) {
       mwait(accf, r & 1);  // (SPIN is always 1: the executor's epilogue spins)
@@ -182,14 +214,14 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 template <int L, int SPIN>
-void run(const char* name, const CUtensorMap& map, long long* dout) {
+void run(const char* name, const CUtensorMap& map, long long* dout, int grid = 1) {
   const int smem = KC * 16384 + NST * CH + 256;
   CK(cudaFuncSetAttribute(k_pipe2<L, SPIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_pipe2<L, SPIN><<<1, 320, smem>>>(map, 200, dout);
+  k_pipe2<L, SPIN><<<grid, 320, smem>>>(map, 200, dout);  // every CTA streams the same activations
   CK(cudaDeviceSynchronize());
-  long long h[16];
+  long long h[32];
   CK(cudaMemcpy(h, dout, sizeof(h), cudaMemcpyDeviceToHost));
-  printf("%-56s %6lld cycles / round = %5.1f per k-step\n", name, h[L * 2 + SPIN], h[L * 2 + SPIN] / 40.0);
+  printf("%-56s %6lld cycles / round = %5.1f per k-step\n", name, h[L * 3 + SPIN], h[L * 3 + SPIN] / 40.0);
 }
 
 int main() {
@@ -197,9 +229,21 @@ int main() {
   unsigned char* act;
   long long* dout;
   CK(cudaMalloc(&act, 128 * 640 * 2));
-  CK(cudaMemset(act, 0, 128 * 640 * 2));
-  CK(cudaMalloc(&dout, 16 * 8));
-  CK(cudaMemset(dout, 0, 16 * 8));
+  if (getenv("ZERO_ACT")) {
+    CK(cudaMemset(act, 0, 128 * 640 * 2));
+  } else {  // random fp16 activations in (-1, 1)
+    std::vector<uint16_t> h(128 * 640);
+    uint32_t st = 12345;
+    for (auto& v : h) {
+      st = st * 1664525u + 1013904223u;
+      const float f = ((st >> 8) / 16777216.0f) * 2.0f - 1.0f;
+      __half hv = __float2half(f);
+      memcpy(&v, &hv, 2);
+    }
+    CK(cudaMemcpy(act, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
+  }
+  CK(cudaMalloc(&dout, 32 * 8));
+  CK(cudaMemset(dout, 0, 32 * 8));
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
   CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
@@ -218,5 +262,8 @@ int main() {
   run<0, 1>("L0 executor before (TS->D1, SS->D2), epilogue spinning", map, dout);
   run<1, 1>("L1 LO_TMEM layout, epilogue spinning", map, dout);
   run<2, 1>("L2 same-column SS lo, epilogue spinning", map, dout);
+  run<0, 2>("L0 random weights + activations", map, dout);
+  run<1, 2>("L1 random weights + activations", map, dout);
+  run<3, 2>("L3 random weights (resident)", map, dout);
   return 0;
 }

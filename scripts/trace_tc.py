@@ -24,7 +24,7 @@ D.replay_decode(cap, x, lens)
 st = cap.stats()
 print("us/step", 1000 * st["gpu_ms"] / st["joint_evals"])
 G = 75
-NEV = 112
+NEV = 136
 buf = (C.c_uint64 * ((2 * NEV + G) * 64))()
 assert lib().rnntg_debug_trace(cap._h, buf, (2 * NEV + G) * 64) == 0, lib().rnntg_last_error()
 allev = np.array(buf, dtype=np.int64).reshape(2 * NEV + G, 64)
@@ -81,8 +81,8 @@ if (rt > 0).any() and os.environ.get("RNNTG_ECHO"):
     print("J->R0->J round trip (J clock, cycles): median", np.median(rt[rt > 0]), "min", rt[rt > 0].min())
 
 print("per-chunk pipeline (clock64 cycles after chunk-0 load issue; median):")
-for base, nm in [(56, "J"), (82, "I1")]:
-    blk = allev[base:base + 25].astype(np.float64)
+for base, nm in [(56, "J"), (92, "I1")]:
+    blk = allev[base:base + 35].astype(np.float64)
     ok = blk[0] > 0
     if not ok.any():
         continue
@@ -91,5 +91,7 @@ for base, nm in [(56, "J"), (82, "I1")]:
     full = " ".join(f"{np.median(rel[10 + k]):5.0f}" for k in range(10))
     print(f"  {nm:3s} load issue: {iss}")
     print(f"  {nm:3s} data full : {full}")
+    land = " ".join(f"{np.median(rel[25 + k]):5.0f}" for k in range(10))
+    print(f"  {nm:3s} landed    : {land}")
     print(f"  {nm:3s} MMAs issued {np.median(rel[20]):.0f}, acc read {np.median(rel[21]):.0f}, polls after chunk 0 ready: {np.median(blk[22, ok]):.0f}")
     print(f"  {nm:3s} chunk 2: before empty wait {np.median(rel[23]):.0f}, stamp {np.median(rel[2]):.0f}, after TMA issue {np.median(rel[24]):.0f}")
