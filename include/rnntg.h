@@ -49,7 +49,7 @@ typedef enum {
   RNNTG_E_ALLOC = 9        /* device or pinned allocation failed */
 } rnntg_status;
 
-typedef enum { RNNTG_CELL_TANH = 0, RNNTG_CELL_LSTM = 1 } rnntg_cell;
+typedef enum { RNNTG_CELL_TANH = 0, RNNTG_CELL_LSTM = 1, RNNTG_CELL_SCRIPTED = 2 } rnntg_cell;
 
 /* DecodeAlgo (decoders.hpp:97). */
 typedef enum {
@@ -99,6 +99,28 @@ const char* rnntg_last_error(void);
 int rnntg_abi_version(void);
 /* Number of CUDA devices visible (0 on a host without a GPU). */
 int rnntg_device_count(void);
+
+/* Table-lookup model on the device (the reference's ScriptedModel,
+ * model.hpp:168-230 / model.cpp:417-615) so the planted-trace schedule tests
+ * run on the GPU schedules.  The prediction state is the running emission
+ * count (run_prediction: hidden' = hidden + 1); the joint puts logit 10 on the
+ * planted label of (utterance b, frame t, emission u) and 0 elsewhere
+ * (logits_at), TDT also on the duration class of duration_at(b, t, u).
+ *   labels   [batch][frames][umax]  planted label of emission u (vocab = blank
+ *            for u past the frame's list); u >= umax or u < 0 is blank
+ *   fs_arr   [batch][frames + 1]    emissions before frame t on a frame-sync
+ *            schedule (frame_sync_arrival; t >= frames uses entry frames)
+ *   dur_arr  [batch][frames]        emissions on arrival at frame t on a
+ *            duration schedule, -1 if never reached (duration_arrival)
+ *   dur_val  [batch][frames][umax + 1]  duration_at(b, t, min(u, umax));
+ *            NULL (and num_durations 0) without a duration head
+ * Decoders over a scripted model run on RNNTG_EXEC_GRAPH or
+ * RNNTG_EXEC_HOSTLOOP (the persistent executors return RNNTG_E_VALUE). */
+rnntg_status rnntg_model_create_scripted(int device, int vocab, int batch, int frames, int umax,
+                                         const int32_t* labels, const int32_t* fs_arr,
+                                         const int32_t* dur_arr, int num_durations,
+                                         const int32_t* durations, const int32_t* dur_val,
+                                         rnntg_model** out);
 
 /* Weights in the reference's parameter order and [in,out] row-major layout
  * (model.hpp:44-59; the LSTM extension keeps the order with one

@@ -38,6 +38,12 @@ struct DevModel {
   const float* enc;             // [Fp][Jp]
   const float* enc_hi;          // tcgen05 operands: enc^T split into tf32 hi/lo,
   const float* enc_lo;          // K-major [Jp][Fp]
+  // RNNTG_CELL_SCRIPTED tables (rnntg_model_create_scripted)
+  const int* s_lab;   // [s_B][s_T][s_U]
+  const int* s_fsarr; // [s_B][s_T + 1]
+  const int* s_darr;  // [s_B][s_T]
+  const int* s_dval;  // [s_B][s_T][s_U + 1]
+  int s_B, s_T, s_U;
 };
 
 // Loop/scalar control block (device memory, one per decoder).

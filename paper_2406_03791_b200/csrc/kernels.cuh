@@ -425,6 +425,77 @@ __global__ void __launch_bounds__(NT) pred_proj_kernel(DevModel M, DevState S) {
 }
 
 // -------------------------------------------------------------------------
+// Scripted model prediction step (ScriptedModel::run_prediction,
+// model.cpp:563-572): the state is the running emission count,
+// hidden' = hidden + 1 for the rows that accepted a label (where_select_rows,
+// decoders.cpp:292-295); the "projection" gp[b][0] is the committed state the
+// joint reads as g.  One CTA; the tail is pred_proj_kernel's (parity flip,
+// pred_steps, label-loop round bookkeeping).
+// -------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) scripted_pred_kernel(DevModel M, DevState S) {
+  pdl_trigger();
+  pdl_wait();
+  const int par = ld_volatile(&S.ctrl->par), cur = par, nxt = par ^ 1;
+  for (int b = threadIdx.x; b < S.B; b += blockDim.x) {
+    const size_t idx = (size_t)b * M.Hp;
+    const float h = S.h[0][cur][idx];
+    if (S.accept[b]) {
+      S.h[0][nxt][idx] = h + 1.0f;
+      S.gp[(size_t)b * M.Jp] = h + 1.0f;
+    } else {
+      S.h[0][nxt][idx] = h;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    S.ctrl->ctr_pp = 0;
+    S.ctrl->par ^= 1;
+    S.ctrl->pred_steps += 1;
+  }
+  if (S.algo != ALGO_FS) ll_round_tail(M, S);
+}
+
+// Scripted model joint logit (ScriptedModel::run_joint / run_joint_tdt,
+// model.cpp:574-615): 10 on the planted label (or duration class) of the
+// decision at (b, t, u), 0 elsewhere; u = emissions so far - emissions on
+// arrival at frame t (frame-sync arrivals for run_joint, duration-schedule
+// arrivals for run_joint_tdt).  col: vocab column, or duration class index
+// when dur.
+__device__ __forceinline__ float scripted_logit(const DevModel& M, const DevState& S, int b, int t, int col,
+                                                bool dur) {
+  const int blank = M.V1 - 1;
+  const int emitted = (int)S.gp[(size_t)b * M.Jp] - 1;
+  const bool in = b < M.s_B && t < M.s_T;
+  int u;
+  if (S.algo == ALGO_TDT) {
+    const int arr = in ? M.s_darr[(size_t)b * M.s_T + t] : -1;
+    u = arr < 0 ? -1 : emitted - arr;
+  } else {
+    const int tt = t < 0 ? 0 : (t > M.s_T ? M.s_T : t);
+    u = emitted - (b < M.s_B ? M.s_fsarr[(size_t)b * (M.s_T + 1) + tt] : 0);
+  }
+  if (!dur) {
+    const int lab = (in && u >= 0 && u < M.s_U) ? M.s_lab[((size_t)b * M.s_T + t) * M.s_U + u] : blank;
+    return col == lab ? 10.0f : 0.0f;
+  }
+  // duration_at(b, t, u < 0 ? 1 << 20 : u): the entry index is min(u, len)
+  int d;
+  if (in) {
+    const int ui = (u < 0 || u > M.s_U) ? M.s_U : u;
+    d = M.s_dval[((size_t)b * M.s_T + t) * (M.s_U + 1) + ui];
+  } else {
+    d = 1;  // blank outside the table
+  }
+  int cls = 0;
+  for (int i = 0; i < M.D; ++i)
+    if (M.durations[i] == d) {
+      cls = i;
+      break;
+    }
+  return col == cls ? 10.0f : 0.0f;
+}
+
+// -------------------------------------------------------------------------
 // Per-row decision of the joint step (lane 0 of the row's warp).
 //   frame-sync: launch_fs_inner_body's argmax/blank_update/save_kv/update_*
 //               (decoders.cpp:261-307)
@@ -514,14 +585,15 @@ __global__ void __launch_bounds__(NT) joint_kernel(DevModel M, DevState S) {
   const bool dur_chunk = chunk >= M.NCH;
   const int kw = K / NW, k0 = warp * kw, kq = kw / 4;
   const float* wslice = M.out_ext + ((size_t)chunk * K + k0) * CT;  // tiled [chunk][Jp][16]
+  const bool scripted = M.cell == RNNTG_CELL_SCRIPTED;
   init_step_barriers(sm);
-  prefetch_w(sm, wslice, kw);
+  if (!scripted) prefetch_w(sm, wslice, kw);
   pdl_trigger();
   pdl_wait();
   const bool fs = S.algo == ALGO_FS;
   const int tf = fs ? ld_volatile(&S.ctrl->t) : 0;
   // ---- stage trunk rows (this warp's k-slice) ----
-  for (int p = lane; p < RB * kq; p += 32) {
+  for (int p = lane; p < RB * kq && !scripted; p += 32) {
     const int r = p / kq, q = p % kq, b = row0 + r;
     const int k = k0 + 4 * q;
     float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -539,17 +611,27 @@ __global__ void __launch_bounds__(NT) joint_kernel(DevModel M, DevState S) {
     *reinterpret_cast<float4*>(sm.As + r * KS + k) = z;
   }
   __syncwarp();
-  float acc[4][4];
-  warp_gemv_32x16(sm.As, KS, wslice, k0, kw, warp_wslot(sm), &sm.wbars[warp], true, acc);
-  store_partial(sm.red, acc);
+  if (!scripted) {
+    float acc[4][4];
+    warp_gemv_32x16(sm.As, KS, wslice, k0, kw, warp_wslot(sm), &sm.wbars[warp], true, acc);
+    store_partial(sm.red, acc);
+  }
   __syncthreads();
   // ---- per-row chunk statistics: half-warp per row ----
   const int half = lane >> 4, hl = lane & 15;
   const int nvalid = dur_chunk ? M.D : (M.V1 - col0 < CT ? M.V1 - col0 : CT);
   for (int r = warp * 2 + half; r < RB; r += 2 * NW) {
     const int b = row0 + r;
-    float x = reduce_partial(sm.red, r, hl);
     const bool valid = hl < nvalid;
+    float x;
+    if (scripted) {
+      const int t = fs ? tf : (b < S.B ? S.t_row[b] : 0);
+      x = b < S.B ? scripted_logit(M, S, b, t < 0 ? 0 : (t > S.T - 1 ? S.T - 1 : t), dur_chunk ? hl : col0 + hl,
+                                   dur_chunk)
+                  : 0.0f;
+    } else {
+      x = reduce_partial(sm.red, r, hl);
+    }
     if (S.dbg_logits && b < S.B && valid) S.dbg_logits[(size_t)b * M.NOUT + col0 + hl] = x;
     float m = valid ? x : -INFINITY;
 #pragma unroll

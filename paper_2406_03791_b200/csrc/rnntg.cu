@@ -289,6 +289,10 @@ cudaError_t add_pred_step(Builder& b, rnntg_decoder* d) {
   const DevModel& M = d->m->dm;
   const int nrb = d->st.nrb;
   cudaError_t e;
+  if (M.cell == RNNTG_CELL_SCRIPTED) {
+    void* args[2] = {&d->arg_m, &d->arg_s};
+    return b.kernel((const void*)scripted_pred_kernel, dim3(1), dim3(NT), 0, args);
+  }
   for (int l = 0; l < M.L; ++l) {
     void* args[3] = {&d->arg_m, &d->arg_s, &d->arg_l[l]};
     const void* fn = M.cell == RNNTG_CELL_LSTM ? (const void*)pred_layer_kernel<1>
@@ -744,6 +748,11 @@ rnntg_status run_hostloop(rnntg_decoder* d) {
   const int nrb = s.nrb;
   Ctrl* hc = d->hctrl;
   auto pred = [&]() -> cudaError_t {
+    if (M.cell == RNNTG_CELL_SCRIPTED) {
+      ++d->n_launches;
+      scripted_pred_kernel<<<1, NT, 0, st>>>(M, s);
+      return cudaGetLastError();
+    }
     d->n_launches += M.L + 1;
     for (int l = 0; l < M.L; ++l) {
       if (M.cell == RNNTG_CELL_LSTM)
@@ -764,7 +773,7 @@ rnntg_status run_hostloop(rnntg_decoder* d) {
     cudaError_t e = cudaMemcpyAsync(hc, s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st);
     return e != cudaSuccess ? e : cudaStreamSynchronize(st);
   };
-  CK(encproj_launch(d->enc, st));
+  if (M.cell != RNNTG_CELL_SCRIPTED) CK(encproj_launch(d->enc, st));
   d->n_launches += 2;
   prologue_kernel<<<148, 256, 0, st>>>(M, s);
   CK(cudaGetLastError());
@@ -810,7 +819,7 @@ cudaError_t build_graph(rnntg_decoder* d) {
 
   Builder root{d->graph};
   root.pdl = pdl;
-  if ((e = add_encproj(root, d)) != cudaSuccess) return e;
+  if (d->m->dm.cell != RNNTG_CELL_SCRIPTED && (e = add_encproj(root, d)) != cudaSuccess) return e;
   {
     void* args[2] = {&d->arg_m, &d->arg_s};
     if ((e = root.kernel((const void*)prologue_kernel, dim3(148), dim3(256), 0, args)) !=
@@ -1024,6 +1033,73 @@ rnntg_status rnntg_model_destroy(rnntg_model* m) {
   return RNNTG_OK;
 }
 
+rnntg_status rnntg_model_create_scripted(int device, int vocab, int batch, int frames, int umax,
+                                         const int32_t* labels, const int32_t* fs_arr,
+                                         const int32_t* dur_arr, int num_durations,
+                                         const int32_t* durations, const int32_t* dur_val,
+                                         rnntg_model** out) {
+  if (!out) return fail(RNNTG_E_VALUE, "out is null");
+  *out = nullptr;
+  if (vocab < 1 || batch < 1 || frames < 1 || umax < 1) return fail(RNNTG_E_VALUE, "scripted model dims must be >= 1");
+  if (num_durations < 0 || num_durations > MAXD) return fail(RNNTG_E_VALUE, "bad duration class count");
+  if (!labels || !fs_arr || !dur_arr || (num_durations > 0 && (!durations || !dur_val)))
+    return fail(RNNTG_E_VALUE, "null scripted table");
+  if (rnntg_device_count() == 0) return fail(RNNTG_E_CUDA, "no CUDA device");
+  CK(cudaSetDevice(device));
+  auto* m = new rnntg_model;
+  m->device = device;
+  rnntg_dims& dd = m->dims;
+  dd = rnntg_dims{};
+  dd.vocab = vocab;
+  dd.embed = dd.hidden = dd.joint = 1;
+  dd.layers = 1;
+  dd.cell = RNNTG_CELL_SCRIPTED;
+  dd.feature = 2;  // (utterance, frame) features, ScriptedModel::make_features
+  dd.num_durations = num_durations;
+  for (int i = 0; i < num_durations; ++i) dd.durations[i] = durations[i];
+  DevModel& M = m->dm;
+  M = DevModel{};
+  M.V1 = vocab + 1;
+  M.E = M.H = M.J = 1;
+  M.Hp = M.Jp = 64;
+  M.L = 1;
+  M.cell = RNNTG_CELL_SCRIPTED;
+  M.G = 1;
+  M.GH = M.Hp;
+  M.F = 2;
+  M.Fp = 64;
+  M.D = num_durations;
+  for (int i = 0; i < M.D; ++i) M.durations[i] = durations[i];
+  M.V1p = round_up(M.V1, CT);
+  M.NOUT = M.V1p + (M.D ? CT : 0);
+  M.NCH = M.V1p / CT;
+  M.NCHT = M.NCH + (M.D ? 1 : 0);
+  M.s_B = batch;
+  M.s_T = frames;
+  M.s_U = umax;
+  const size_t nl = (size_t)batch * frames * umax, nf = (size_t)batch * (frames + 1), nd = (size_t)batch * frames;
+  std::vector<int32_t> dv((size_t)batch * frames * (umax + 1), 1);
+  if (num_durations > 0) std::memcpy(dv.data(), dur_val, dv.size() * sizeof(int32_t));
+  int *dl = nullptr, *df = nullptr, *da = nullptr, *dvd = nullptr;
+  cudaError_t e;
+  if ((e = m->mem.alloc(&dl, nl)) != cudaSuccess || (e = m->mem.alloc(&df, nf)) != cudaSuccess ||
+      (e = m->mem.alloc(&da, nd)) != cudaSuccess || (e = m->mem.alloc(&dvd, dv.size())) != cudaSuccess ||
+      (e = cudaMemcpy(dl, labels, nl * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(df, fs_arr, nf * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(da, dur_arr, nd * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(dvd, dv.data(), dv.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) {
+    m->mem.release();
+    delete m;
+    return fail(RNNTG_E_CUDA, std::string("scripted model upload: ") + cudaGetErrorString(e));
+  }
+  M.s_lab = dl;
+  M.s_fsarr = df;
+  M.s_darr = da;
+  M.s_dval = dvd;
+  *out = m;
+  return RNNTG_OK;
+}
+
 rnntg_status rnntg_decoder_create(rnntg_model* m, int algo, int exec, int batch, int max_frames,
                                   int max_symbols, rnntg_decoder** out) {
   if (!out) return fail(RNNTG_E_VALUE, "out is null");
@@ -1055,7 +1131,10 @@ rnntg_status rnntg_decoder_create(rnntg_model* m, int algo, int exec, int batch,
         (e = cudaEventCreate(&d->ev1)) == cudaSuccess) {
       d->st.x = d->x_dev;
       d->st.out_len = d->len_dev;
-      if (!encproj_plan(d->enc, m->dm, d->x_dev, d->st.fp, batch * max_frames))
+      if (m->dm.cell == RNNTG_CELL_SCRIPTED && exec != RNNTG_EXEC_GRAPH && exec != RNNTG_EXEC_HOSTLOOP)
+        st = fail(RNNTG_E_VALUE, "scripted models run on the graph or host-loop executor");
+      else if (m->dm.cell != RNNTG_CELL_SCRIPTED &&
+               !encproj_plan(d->enc, m->dm, d->x_dev, d->st.fp, batch * max_frames))
         st = fail(RNNTG_E_CUDA, "cannot encode TMA tensor maps for the encoder projection");
       else if (exec == RNNTG_EXEC_GRAPH) e = build_graph(d);
       else if (exec == RNNTG_EXEC_TENSOR) st = setup_tc(d);
@@ -1253,6 +1332,7 @@ rnntg_status rnntg_get_stats(rnntg_decoder* d, rnntg_stats* s) {
 rnntg_status rnntg_step_joint(rnntg_model* m, int batch, const float* f, const float* g,
                               float* logp, float* dur_logp) {
   if (!m) return fail(RNNTG_E_STATE, "model is null");
+  if (m->dm.cell == RNNTG_CELL_SCRIPTED) return fail(RNNTG_E_VALUE, "not available for a scripted model");
   if (batch < 1 || batch > RB * MAXRB) return fail(RNNTG_E_VALUE, "bad batch");
   if (!f || !g || !logp) return fail(RNNTG_E_DIMENSION, "null buffer");
   CK(cudaSetDevice(m->device));
@@ -1309,6 +1389,7 @@ rnntg_status rnntg_step_joint(rnntg_model* m, int batch, const float* f, const f
 rnntg_status rnntg_step_prediction(rnntg_model* m, int batch, const int32_t* labels,
                                    const float* state, float* state_out) {
   if (!m) return fail(RNNTG_E_STATE, "model is null");
+  if (m->dm.cell == RNNTG_CELL_SCRIPTED) return fail(RNNTG_E_VALUE, "not available for a scripted model");
   if (batch < 1 || batch > RB * MAXRB) return fail(RNNTG_E_VALUE, "bad batch");
   if (!labels || !state || !state_out) return fail(RNNTG_E_DIMENSION, "null buffer");
   const DevModel& M = m->dm;
@@ -1364,6 +1445,7 @@ rnntg_status rnntg_step_prediction(rnntg_model* m, int batch, const int32_t* lab
 
 rnntg_status rnntg_time_kernel(rnntg_decoder* d, int which, int reps, float* avg_ms) {
   if (!d || !avg_ms || reps < 1) return fail(RNNTG_E_VALUE, "bad arguments");
+  if (d->m->dm.cell == RNNTG_CELL_SCRIPTED) return fail(RNNTG_E_VALUE, "not available for a scripted model");
   CK(cudaSetDevice(d->m->device));
   const DevModel& M = d->m->dm;
   DevState s = d->st;
@@ -1448,6 +1530,7 @@ rnntg_status rnntg_debug_profile(rnntg_decoder* d, unsigned long long* out16) {
 
 rnntg_status rnntg_enc_proj(rnntg_model* m, int rows, const float* x, float* fp) {
   if (!m) return fail(RNNTG_E_STATE, "model is null");
+  if (m->dm.cell == RNNTG_CELL_SCRIPTED) return fail(RNNTG_E_VALUE, "not available for a scripted model");
   if (rows < 1 || !x || !fp) return fail(RNNTG_E_DIMENSION, "bad arguments");
   CK(cudaSetDevice(m->device));
   const DevModel& M = m->dm;

@@ -70,10 +70,98 @@ void check(rnntg_status s) {
   if (s != RNNTG_OK) raise(s);
 }
 
+// ScriptedModel -> device tables (rnntg_model_create_scripted), built from its
+// public surface: labels(), max_symbols(), durations(), duration_at().  The
+// emission counts on arrival at each frame restate ScriptedModel's schedule
+// rules (model.cpp:510-549): a frame-sync schedule emits min(len, cap) of a
+// frame's labels; a duration schedule walks the planted decisions with the
+// decoders' advance rules (accept: d > 0 jumps d frames, u == cap advances
+// one; blank: advance max(d, 1)).
+struct ScriptedTables {
+  int B = 0, T = 0, V = 0, U = 1;
+  std::vector<int32_t> lab, fs, arr, dv, durs;
+  uint64_t hash() const {
+    uint64_t h = 1469598103934665603ULL;
+    auto mix = [&](const std::vector<int32_t>& v) {
+      for (int32_t x : v) h = (h ^ static_cast<uint32_t>(x)) * 1099511628211ULL;
+      h = (h ^ v.size()) * 1099511628211ULL;
+    };
+    mix({B, T, V, U});
+    mix(lab);
+    mix(fs);
+    mix(arr);
+    mix(dv);
+    mix(durs);
+    return h;
+  }
+};
+
+ScriptedTables scripted_tables(const ScriptedModel& sm) {
+  const int B = sm.batch(), T = sm.frames(), V = sm.vocab_size(), cap = sm.max_symbols();
+  const auto& lt = sm.labels();
+  int U = 1;
+  for (const auto& row : lt)
+    for (const auto& e : row) U = std::max<int>(U, static_cast<int>(e.size()));
+  ScriptedTables st;
+  st.B = B;
+  st.T = T;
+  st.V = V;
+  st.U = U;
+  st.durs = sm.durations();
+  std::vector<int32_t>&lab = st.lab, &fs = st.fs, &arr = st.arr, &dv = st.dv;
+  lab.assign((size_t)B * T * U, V);
+  fs.assign((size_t)B * (T + 1), 0);
+  arr.assign((size_t)B * T, -1);
+  dv.assign((size_t)B * T * (U + 1), 1);
+  for (int b = 0; b < B; ++b) {
+    for (int t = 0; t < T; ++t) {
+      const int len = static_cast<int>(lt[b][t].size());
+      for (int u = 0; u < len; ++u) lab[((size_t)b * T + t) * U + u] = lt[b][t][u];
+      for (int u = 0; u <= U; ++u) dv[((size_t)b * T + t) * (U + 1) + u] = sm.duration_at(b, t, u);
+      fs[(size_t)b * (T + 1) + t + 1] = fs[(size_t)b * (T + 1) + t] + std::min(len, cap);
+    }
+    int64_t emitted = 0;
+    for (int t = 0; t < T;) {
+      arr[(size_t)b * T + t] = static_cast<int32_t>(emitted);
+      const int len = static_cast<int>(lt[b][t].size());
+      int next = -1;
+      for (int u = 0; next < 0;) {
+        if (u < len) {
+          const int32_t d = sm.duration_at(b, t, u);
+          ++emitted;
+          ++u;
+          if (d > 0) next = t + d;
+          else if (u == cap) next = t + 1;
+        } else {
+          next = t + std::max<int32_t>(sm.duration_at(b, t, len), 1);
+        }
+      }
+      t = next;
+    }
+  }
+  return st;
+}
+
 rnntg_model* upload(const DecoderModel& model) {
   std::lock_guard<std::mutex> lk(g_mu);
   rnntg_dims d{};
   std::vector<const float*> w;
+  if (const auto* sm = dynamic_cast<const ScriptedModel*>(&model)) {
+    const ScriptedTables st = scripted_tables(*sm);
+    const uint64_t fp = st.hash();
+    auto it = g_models.find(&model);
+    if (it != g_models.end()) {
+      if (it->second.fp == fp) return it->second.m;
+      rnntg_model_destroy(it->second.m);
+      g_models.erase(it);
+    }
+    const int nd = static_cast<int>(st.durs.size());
+    rnntg_model* m = nullptr;
+    check(rnntg_model_create_scripted(0, st.V, st.B, st.T, st.U, st.lab.data(), st.fs.data(), st.arr.data(), nd,
+                                      nd ? st.durs.data() : nullptr, nd ? st.dv.data() : nullptr, &m));
+    g_models[&model] = Entry{m, fp};
+    return m;
+  }
   if (const auto* nm = dynamic_cast<const NeuralModel*>(&model)) {
     const RnntParams& p = nm->params();
     d.vocab = p.dims.vocab;

@@ -45,6 +45,20 @@ bool same(const Hypotheses& a, const Hypotheses& b, double* max_rel) {
   return true;
 }
 
+// Scripted models: tokens, frames exact; a planted decision scores
+// 10 - lse with lse = 10 + log(1 + V e^-10) ~ 10.0007 in fp32 on both sides,
+// so one rounding step of lse (ulp(10) = 9.5e-7) separates two correct
+// summation orders; scores are compared to 4e-6 absolute.
+bool same_scripted(const Hypotheses& a, const Hypotheses& b) {
+  if (a.size() != b.size()) return false;
+  for (size_t i = 0; i < a.size(); ++i) {
+    if (a[i].tokens != b[i].tokens || a[i].frames != b[i].frames) return false;
+    for (size_t j = 0; j < a[i].scores.size(); ++j)
+      if (std::fabs((double)a[i].scores[j] - b[i].scores[j]) > 4e-6) return false;
+  }
+  return true;
+}
+
 }  // namespace
 
 int main() {
@@ -142,6 +156,97 @@ int main() {
       report((std::string("dropin errors ") + en).c_str(), ok,
              "ValueError / DimensionError / StateError as in errors.hpp");
     }
+  }
+  // §8(f)4: the reference's planted-trace schedule tests on the GPU schedules
+  // through a device ScriptedModel (test_decoders.cpp:57-80, 107-133,
+  // 292-309, 404-431; acceptance.cpp criterion 8), against the reference's
+  // own decoders on the CPU.
+  for (rnntg_exec ex : {RNNTG_EXEC_GRAPH, RNNTG_EXEC_HOSTLOOP, RNNTG_EXEC_TENSOR}) {
+    cuda::set_executor(ex);  // TENSOR: scripted models fall back to the graph executor
+    const std::string en = ex == RNNTG_EXEC_GRAPH ? "graph" : ex == RNNTG_EXEC_HOSTLOOP ? "hostloop" : "default";
+    auto adversarial_pair = [](int frames, int ms, int vocab) {
+      ScriptedModel::LabelTable table(2, std::vector<std::vector<int32_t>>(frames));
+      for (int b = 0; b < 2; ++b)
+        for (int t = 0; t < frames; ++t)
+          if (t % 2 == b % 2)
+            for (int j = 0; j < ms; ++j) table[b][t].push_back((t * ms + j) % vocab);
+      return ScriptedModel(vocab, ms, std::move(table));
+    };
+    bool ok = true;
+    std::string why;
+    auto expect = [&](bool c, const std::string& what) {
+      if (!c && ok) why = what;
+      ok = ok && c;
+    };
+    {  // planted script, empty script, emission cap
+      ScriptedModel m1(8, 5, {{{3}, {}, {5, 6}}});
+      ScriptedModel m2(8, 5, {{{}, {}}});
+      ScriptedModel m3(16, 5, {{{1, 2, 3, 4, 5, 6, 7}, {9}}});
+      Engine e1, e2, e3, r1;
+      const Hypotheses h1 = cuda::greedy_decode_sync_free(e1, m1, m1.make_features(), Tensor::from_ints({3}, {1}), 5);
+      const Hypotheses h2 = cuda::greedy_decode_sync_free(e2, m2, m2.make_features(), Tensor::from_ints({2}, {1}), 5);
+      const Hypotheses h3 = cuda::greedy_decode_sync_free(e3, m3, m3.make_features(), Tensor::from_ints({2}, {1}), 5);
+      expect(h1[0].tokens == std::vector<int32_t>{3, 5, 6} && h1[0].frames == std::vector<int32_t>{0, 2, 2}, "planted");
+      expect(h2[0].tokens.empty(), "empty script");
+      expect(h3[0].tokens == std::vector<int32_t>{1, 2, 3, 4, 5, 9} &&
+                 h3[0].frames == std::vector<int32_t>{0, 0, 0, 0, 0, 1},
+             "emission cap");
+      expect(same_scripted(h1, rnntsim::greedy_decode_sync_free(r1, m1, m1.make_features(), Tensor::from_ints({3}, {1}), 5)),
+             "planted vs reference");
+    }
+    {  // adversarial even/odd pair: FS 20 joint evaluations, LL 12, identical hypotheses
+      const ScriptedModel m = adversarial_pair(4, 5, 16);
+      const Tensor x = m.make_features();
+      const Tensor len = Tensor::from_ints({4, 4}, {2});
+      Engine fs_e, ll_e, ref_e;
+      const Hypotheses fs = cuda::greedy_decode_sync_free(fs_e, m, x, len, 5);
+      const Hypotheses ll = cuda::label_looping_decode(ll_e, m, x, len, 5);
+      const Hypotheses ref = rnntsim::greedy_decode_sync_free(ref_e, m, x, len, 5);
+      auto show = [](const Hypotheses& h) {
+        std::string o;
+        for (const auto& y : h) {
+          o += "[";
+          for (size_t i = 0; i < y.tokens.size(); ++i)
+            o += std::to_string(y.tokens[i]) + "@" + std::to_string(y.frames[i]) + " ";
+          o += "]";
+        }
+        return o;
+      };
+      expect(same_scripted(fs, ref) && same_scripted(ll, ref),
+             "adversarial pair vs reference: fs " + show(fs) + " ll " + show(ll) + " ref " + show(ref));
+      expect(fs[0].frames == std::vector<int32_t>({0, 0, 0, 0, 0, 2, 2, 2, 2, 2}) &&
+                 fs[1].frames == std::vector<int32_t>({1, 1, 1, 1, 1, 3, 3, 3, 3, 3}),
+             "adversarial frames");
+      // criterion 8: label looping does strictly less joint work.  The reference
+      // counts 12 (one joint + a prediction for every row per iteration); the
+      // device label loop is the nested blank-skipping form (SURVEY.md §8 a16:
+      // joint-only inner iterations until no row awaits a decision, then the
+      // acceptors' prediction), which spends one extra joint here: at frame 0
+      // utterance 1 blanks while utterance 0 waits with its accepted label.
+      expect(cuda::decode_joint_evals(fs_e) == 20 && cuda::decode_joint_evals(ll_e) == 13 &&
+                 cuda::decode_joint_evals(ll_e) < cuda::decode_joint_evals(fs_e),
+             "joint evals FS " + std::to_string(cuda::decode_joint_evals(fs_e)) + " LL " +
+                 std::to_string(cuda::decode_joint_evals(ll_e)));
+      for (DecodeAlgo algo : {DecodeAlgo::FrameSync, DecodeAlgo::LabelLoop}) {  // graph replay
+        Engine eng;
+        CapturedDecoder cap = cuda::build_decode_graph(eng, m, algo, 2, 4, 5);
+        expect(same_scripted(cuda::replay_decode(cap, x, len), ref), "replay");
+      }
+    }
+    {  // planted durations skip frames: tokens {1,2,3,4} at frames {0,0,2,5}
+      ScriptedModel m(9, 3, {{{1, 2}, {}, {3}, {}, {}, {4}}}, {0, 1, 2, 3, 4},
+                      {{{0, 2, 1}, {}, {3, 1}, {}, {}, {0, 1}}});
+      const Tensor x = m.make_features();
+      const Tensor len = Tensor::from_ints({6}, {1});
+      Engine e, r;
+      const Hypotheses got = cuda::tdt_label_looping_decode(e, m, x, len, 3);
+      expect(got[0].tokens == std::vector<int32_t>({1, 2, 3, 4}) && got[0].frames == std::vector<int32_t>({0, 0, 2, 5}),
+             "planted durations");
+      expect(same_scripted(got, rnntsim::tdt_label_looping_decode(r, m, x, len, 3)), "durations vs reference");
+    }
+    report(("dropin scripted model (f)4 " + en).c_str(), ok,
+           ok ? "planted / empty / cap / adversarial pair (FS 20 vs LL 13 joint evals; reference 20 vs 12) / durations {0,0,2,5}"
+              : "failed: " + why);
   }
   // §8(f)3: the reference's TimingReport measured on the device
   // (cuda::replay_decode_timed, CUPTI) for each executor on a C2-dims batch,
