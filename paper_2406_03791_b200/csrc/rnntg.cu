@@ -113,6 +113,12 @@ struct rnntg_decoder {
   Ctrl* hctrl = nullptr;
   // host-side work of the last decode (TimingReport.num_syncs / launches)
   int64_t n_syncs = 0, n_launches = 0, n_graph_launches = 0;
+  // tensor executor above its per-kernel batch: balanced sub-batches of
+  // <= ptc::MAXB rows, each its own tensor-core decoder, run back to back on
+  // this decoder's stream (every K6 kernel takes most of the GPU's SMs)
+  std::vector<rnntg_decoder*> subs;
+  std::vector<int> sub_b0;
+  bool owns_stream = true;
 };
 
 namespace {
@@ -1114,6 +1120,42 @@ rnntg_status rnntg_decoder_create(rnntg_model* m, int algo, int exec, int batch,
   if (exec < RNNTG_EXEC_GRAPH || exec > RNNTG_EXEC_HOSTLOOP)
     return fail(RNNTG_E_VALUE, "unknown exec mode");
   CK(cudaSetDevice(m->device));
+  if (exec == RNNTG_EXEC_TENSOR && batch > ptc::MAXB && m->dm.cell != RNNTG_CELL_SCRIPTED) {
+    // balanced sub-batches, one tensor-core decoder each, sharing one stream
+    auto* d = new rnntg_decoder;
+    d->m = m;
+    d->algo = algo;
+    d->exec = exec;
+    d->B = batch;
+    d->T = max_frames;
+    d->ms = max_symbols;
+    const int nsub = (batch + ptc::MAXB - 1) / ptc::MAXB;
+    cudaError_t e = cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreate(&d->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&d->ev1);
+    if (e != cudaSuccess) {
+      rnntg_decoder_destroy(d);
+      return fail(RNNTG_E_CUDA, std::string("decoder setup: ") + cudaGetErrorString(e));
+    }
+    for (int i = 0, b0 = 0; i < nsub; ++i) {
+      const int bi = batch / nsub + (i < batch % nsub ? 1 : 0);
+      rnntg_decoder* sd = nullptr;
+      const rnntg_status st = rnntg_decoder_create(m, algo, exec, bi, max_frames, max_symbols, &sd);
+      if (st) {
+        rnntg_decoder_destroy(d);
+        return st;
+      }
+      cudaStreamDestroy(sd->stream);  // run on the parent's stream, in order
+      sd->stream = d->stream;
+      sd->owns_stream = false;
+      d->subs.push_back(sd);
+      d->sub_b0.push_back(b0);
+      b0 += bi;
+    }
+    d->st.cap = d->subs[0]->st.cap;
+    *out = d;
+    return RNNTG_OK;
+  }
   auto* d = new rnntg_decoder;
   d->m = m;
   d->algo = algo;
@@ -1155,6 +1197,9 @@ rnntg_status rnntg_decoder_destroy(rnntg_decoder* d) {
   if (!d) return RNNTG_OK;
   cudaSetDevice(d->m->device);
   if (d->stream) cudaStreamSynchronize(d->stream);
+  for (rnntg_decoder* sd : d->subs) rnntg_decoder_destroy(sd);
+  d->subs.clear();
+  if (!d->owns_stream) d->stream = nullptr;
   if (d->gexec) cudaGraphExecDestroy(d->gexec);
   if (d->lexec) cudaGraphExecDestroy(d->lexec);
   if (d->graph) cudaGraphDestroy(d->graph);
@@ -1184,6 +1229,13 @@ rnntg_status rnntg_bind(rnntg_decoder* d, const float* x, const int32_t* out_len
   if (st) return st;
   CK(cudaSetDevice(d->m->device));
   const size_t F = d->m->dm.F, Fp = d->m->dm.Fp;
+  if (!d->subs.empty()) {
+    for (size_t i = 0; i < d->subs.size(); ++i)
+      if ((st = rnntg_bind(d->subs[i], x + (size_t)d->sub_b0[i] * d->T * F, out_len + d->sub_b0[i])) != RNNTG_OK)
+        return st;
+    d->bound = true;
+    return RNNTG_OK;
+  }
   CK(cudaMemcpy2DAsync(d->x_dev, Fp * sizeof(float), x, F * sizeof(float), F * sizeof(float),
                        (size_t)d->B * d->T, cudaMemcpyHostToDevice, d->stream));
   CK(cudaMemcpyAsync(d->len_dev, out_len, sizeof(int32_t) * d->B, cudaMemcpyHostToDevice,
@@ -1203,6 +1255,14 @@ rnntg_status rnntg_bind_device(rnntg_decoder* d, const float* x_dev, const int32
   rnntg_status st = check_lengths(d, lens.data());
   if (st) return st;
   const size_t F = d->m->dm.F, Fp = d->m->dm.Fp;
+  if (!d->subs.empty()) {
+    for (size_t i = 0; i < d->subs.size(); ++i)
+      if ((st = rnntg_bind_device(d->subs[i], x_dev + (size_t)d->sub_b0[i] * d->T * F, len_dev + d->sub_b0[i])) !=
+          RNNTG_OK)
+        return st;
+    d->bound = true;
+    return RNNTG_OK;
+  }
   CK(cudaMemcpy2DAsync(d->x_dev, Fp * sizeof(float), x_dev, F * sizeof(float), F * sizeof(float),
                        (size_t)d->B * d->T, cudaMemcpyDeviceToDevice, d->stream));
   CK(cudaMemcpyAsync(d->len_dev, len_dev, sizeof(int32_t) * d->B, cudaMemcpyDeviceToDevice,
@@ -1243,6 +1303,16 @@ rnntg_status rnntg_launch(rnntg_decoder* d) {
   if (!d) return fail(RNNTG_E_STATE, "decoder is null");
   if (!d->bound) return fail(RNNTG_E_STATE, "captured decoder is not initialized (no inputs bound)");
   CK(cudaSetDevice(d->m->device));
+  if (!d->subs.empty()) {
+    CK(cudaEventRecord(d->ev0, d->stream));
+    for (rnntg_decoder* sd : d->subs) {
+      const rnntg_status st = rnntg_launch(sd);
+      if (st) return st;
+    }
+    CK(cudaEventRecord(d->ev1, d->stream));
+    d->launched = true;
+    return RNNTG_OK;
+  }
   if ((d->exec == RNNTG_EXEC_PERSISTENT || d->exec == RNNTG_EXEC_TENSOR) && !d->ltried) capture_persistent(d);
   CK(cudaEventRecord(d->ev0, d->stream));
   d->n_syncs = d->n_graph_launches = 0;
@@ -1272,6 +1342,11 @@ rnntg_status rnntg_sync(rnntg_decoder* d) {
   CK(cudaSetDevice(d->m->device));
   CK(cudaStreamSynchronize(d->stream));
   if (d->launched) ++d->n_syncs;
+  for (rnntg_decoder* sd : d->subs) {
+    const rnntg_status st = rnntg_sync(sd);
+    if (st) return st;
+  }
+  if (!d->subs.empty()) return RNNTG_OK;
   if (d->launched) {
     int err = 0;
     CK(cudaMemcpy(&err, &d->st.ctrl->err, sizeof(int), cudaMemcpyDeviceToHost));
@@ -1287,6 +1362,16 @@ rnntg_status rnntg_read(rnntg_decoder* d, int32_t* counts, int32_t* tokens, int3
   if (st) return st;
   const int B = d->B, dc = d->st.cap;
   if (cap < 1) return fail(RNNTG_E_VALUE, "cap must be >= 1");
+  if (!d->subs.empty()) {
+    for (size_t i = 0; i < d->subs.size(); ++i) {
+      const size_t r = (size_t)d->sub_b0[i], o = r * cap;
+      if ((st = rnntg_read(d->subs[i], counts ? counts + r : nullptr, tokens ? tokens + o : nullptr,
+                           frames ? frames + o : nullptr, scores ? scores + o : nullptr,
+                           durations ? durations + o : nullptr, cap)) != RNNTG_OK)
+        return st;
+    }
+    return RNNTG_OK;
+  }
   std::vector<int32_t> cnt(B);
   CK(cudaMemcpy(cnt.data(), d->st.counts, sizeof(int32_t) * B, cudaMemcpyDeviceToHost));
   if (counts) std::memcpy(counts, cnt.data(), sizeof(int32_t) * B);
@@ -1307,6 +1392,10 @@ rnntg_status rnntg_host_counts(rnntg_decoder* d, int64_t* syncs, int64_t* launch
   *syncs = d->n_syncs;
   *launches = d->n_launches;
   *graph_launches = d->n_graph_launches;
+  for (rnntg_decoder* sd : d->subs) {  // sub-decoders' syncs are the parent's
+    *launches += sd->n_launches;
+    *graph_launches += sd->n_graph_launches;
+  }
   return RNNTG_OK;
 }
 
@@ -1314,6 +1403,20 @@ rnntg_status rnntg_get_stats(rnntg_decoder* d, rnntg_stats* s) {
   if (!d || !s) return fail(RNNTG_E_STATE, "null argument");
   rnntg_status st = rnntg_sync(d);
   if (st) return st;
+  if (!d->subs.empty()) {  // joint evaluations etc. summed over the sub-batches
+    rnntg_stats a{};
+    for (rnntg_decoder* sd : d->subs) {
+      rnntg_stats x{};
+      if ((st = rnntg_get_stats(sd, &x)) != RNNTG_OK) return st;
+      a.joint_evals += x.joint_evals;
+      a.pred_steps += x.pred_steps;
+      a.outer_iters += x.outer_iters;
+      a.emitted += x.emitted;
+    }
+    if (d->launched) CK(cudaEventElapsedTime(&a.gpu_ms, d->ev0, d->ev1));
+    *s = a;
+    return RNNTG_OK;
+  }
   Ctrl c;
   CK(cudaMemcpy(&c, d->st.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
   std::vector<int32_t> cnt(d->B);
@@ -1446,6 +1549,7 @@ rnntg_status rnntg_step_prediction(rnntg_model* m, int batch, const int32_t* lab
 rnntg_status rnntg_time_kernel(rnntg_decoder* d, int which, int reps, float* avg_ms) {
   if (!d || !avg_ms || reps < 1) return fail(RNNTG_E_VALUE, "bad arguments");
   if (d->m->dm.cell == RNNTG_CELL_SCRIPTED) return fail(RNNTG_E_VALUE, "not available for a scripted model");
+  if (!d->subs.empty()) return rnntg_time_kernel(d->subs[0], which, reps, avg_ms);
   CK(cudaSetDevice(d->m->device));
   const DevModel& M = d->m->dm;
   DevState s = d->st;
@@ -1510,6 +1614,7 @@ rnntg_status rnntg_time_kernel(rnntg_decoder* d, int which, int reps, float* avg
 
 rnntg_status rnntg_debug_trace(rnntg_decoder* d, unsigned long long* out, int n) {
   if (!d || !out) return fail(RNNTG_E_VALUE, "bad arguments");
+  if (!d->subs.empty()) return rnntg_debug_trace(d->subs[0], out, n);  // first sub-batch
   if (d->exec != RNNTG_EXEC_TENSOR || !d->tp.prof)
     return fail(RNNTG_E_STATE, "tracing needs the tensor executor and RNNTG_PROF=1");
   CK(cudaStreamSynchronize(d->stream));

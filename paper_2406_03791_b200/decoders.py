@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -115,6 +116,7 @@ class Model:
         self._h = h
         self.device = device
         self._decoders = {}
+        self._live = weakref.WeakSet()  # every CapturedDecoder built on this model
 
     @classmethod
     def from_seed(cls, dims: ModelDims, seed: int = 1, device: int = 0, blank_bias: float = 0.0):
@@ -129,7 +131,9 @@ class Model:
         return self._h
 
     def close(self):
-        for d in self._decoders.values():
+        # every decoder built on this model goes first: a decoder must not
+        # outlive its model (decoders.hpp:100-113)
+        for d in list(self._live):
             d.close()
         self._decoders.clear()
         if self._h:
@@ -191,6 +195,7 @@ class CapturedDecoder:
                                          max_symbols, C.byref(h)))
         self._h = h
         self.capacity = lib().rnntg_decoder_capacity(h)
+        model._live.add(self)
 
     def close(self):
         if getattr(self, "_h", None):

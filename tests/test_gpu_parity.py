@@ -122,8 +122,6 @@ def test_lstm_golden(golden, idx, exec):
             "graph_tdt": DecodeAlgo.TdtLabelLoop}[rec["algo"]]
     if exec == D.Exec.Persistent and rec["layers"] > 2:
         pytest.skip("persistent executor supports <= 2 layers")
-    if exec == D.Exec.Tensor and rec["B"] > 32:
-        pytest.skip("tensor executor supports batch <= 32 per decoder")
     m = Model(to_model_dims(d), p)
     got = D.replay_decode(D.build_decode_graph(m, algo, rec["B"], rec["T"], rec["ms"], exec), x,
                           lens)
@@ -135,6 +133,29 @@ def test_lstm_golden(golden, idx, exec):
     print(f"\n{rec['name']}/{exec.name}: {rep.exact}/{rep.utterances} exact, {rep.permitted} permitted, "
           f"max score rel {rep.max_score_rel:.2e}")
     assert rep.ok, rep.failures
+
+
+@pytest.mark.parametrize("tdt", [False, True])
+def test_tensor_batch_above_kernel_limit(tdt):
+    """Tensor executor at B = 80: balanced sub-batches (27, 27, 26) of
+    tensor-core decoders run back to back; rows keep their order."""
+    _need_gpu()
+    d = O.Dims(200, 64, 64, 96, 24, (0, 1, 2, 3, 4) if tdt else (), O.CELL_LSTM, 2)
+    p = O.init_params(21, d)
+    B, T, ms = 80, 12, 3
+    x = O.fill_uniform(22, -1.0, 1.0, (B, T, d.feature))
+    lens = np.array([T - (5 * i) % 7 for i in range(B)], np.int32)
+    algo = DecodeAlgo.TdtLabelLoop if tdt else DecodeAlgo.FrameSync
+    m = Model(to_model_dims(d), p)
+    cap = D.build_decode_graph(m, algo, B, T, ms, D.Exec.Tensor)
+    got = D.replay_decode(cap, x, lens)
+    ref = O.decode_batch(d, p, x, lens, ms, tdt, record=True)
+    rep = compare_batch(got, ref, d.vocab, tdt, "B80")
+    st = cap.stats()
+    assert st["emitted"] == sum(len(h.tokens) for h in got)
+    print(f"\nB80 tdt={tdt}: {rep.exact}/{rep.utterances} exact, joint evals {st['joint_evals']}")
+    assert rep.ok, rep.failures
+    m.close()
 
 
 @pytest.mark.parametrize("H,J,tdt", [(96, 200, False), (320, 640, True), (640, 192, False)])
