@@ -46,9 +46,15 @@
 namespace rnntg {
 namespace ptc {
 
-constexpr int NEPI = 256;        // 8 epilogue warps: two per TMEM lane quadrant, 16 rows each
+#ifndef NEPI_CFG
+#define NEPI_CFG 256
+#endif
+constexpr int NEPI = NEPI_CFG;   // epilogue threads: WPQ warps per TMEM lane quadrant
 constexpr int NTH = 64 + NEPI;
-constexpr int NR = 16;           // batch rows per epilogue thread
+constexpr int WPQ = NEPI / 128;  // 2 (default) or 4
+constexpr int NR = 32 / WPQ;     // batch rows per epilogue thread (16 or 8)
+constexpr int LOG_NR = NR == 16 ? 4 : 3;
+static_assert(NEPI == 256 || NEPI == 512, "epilogue: 8 or 16 warps");
 #ifndef NSTAGE_CFG
 #define NSTAGE_CFG 4
 #endif
@@ -135,9 +141,6 @@ __host__ __device__ constexpr int nlo_chunks(int KC) {
 #endif
 #ifndef TMA_ACT
 #define TMA_ACT 1  // activations via 2-D tensor maps (plain row-major in global, swizzled by TMA)
-#endif
-#ifndef ARGMAX_REDUX
-#define ARGMAX_REDUX 0
 #endif
 #ifndef LAZY_NS
 #define LAZY_NS 0  // A/B: 500 ns backoff for non-critical pollers cost 0.09 us/step
@@ -304,6 +307,17 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+// NR consecutive accumulator columns of this thread's lane
+template <int N>
+__device__ __forceinline__ void tmem_ldn(uint32_t taddr, uint32_t (&r)[N]) {
+  if constexpr (N == 16) tmem_ld16(taddr, r);
+  else tmem_ld8(taddr, r);
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
@@ -354,15 +368,15 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// Named barrier / OR-reduction over the 4 epilogue warps.
-__device__ __forceinline__ void epi_sync() { asm volatile("barrier.cta.sync.aligned 1, 256;" ::: "memory"); }
+// Named barrier / OR-reduction over the epilogue warps.
+__device__ __forceinline__ void epi_sync() { asm volatile("barrier.cta.sync.aligned 1, %0;" ::"n"(NEPI) : "memory"); }
 __device__ __forceinline__ int epi_or(int v) {
   int r;
   asm volatile(
       "{\n\t.reg .pred q, p;\n\tsetp.ne.s32 q, %1, 0;\n\t"
-      "barrier.cta.red.or.aligned.pred p, 1, 256, q;\n\tselp.s32 %0, 1, 0, p;\n\t}"
+      "barrier.cta.red.or.aligned.pred p, 1, %2, q;\n\tselp.s32 %0, 1, 0, p;\n\t}"
       : "=r"(r)
-      : "r"(v)
+      : "r"(v), "n"(NEPI)
       : "memory");
   return r;
 }
@@ -552,7 +566,7 @@ struct Epi {
   __device__ Epi(const TParams& P_, const Smem& sm_, uint32_t tmem, int et_, int q, int role_, int layer_,
                  int tile_, float wsc_)
       : P(P_), sm(sm_), tq(tmem + ((uint32_t)(32 * q) << 16)), et(et_), m(32 * q + (et_ & 31)),
-        r0(et_ >= 128 ? NR : 0), role(role_),
+        r0(NR * (et_ >> 7)), role(role_),
         layer(layer_), tile(tile_), wsc(wsc_), B(P_.B), blank(P_.V1 - 1), fs(P_.algo == ALGO_FS),
         tdt(P_.algo == ALGO_TDT), lstm(P_.cell == 1),
         tracer(P_.prof && (int)blockIdx.x == P_.prof_first[role_]), cnt(P_.cnt) {}
@@ -633,17 +647,17 @@ struct Epi {
     tc_fence_after();
     const uint32_t a = tq + set * ACC_COLS + r0;
     if (LO_TMEM && !LO_SEPD) {  // [W_hi.x_hi + W_lo.x_hi | W_hi.x_lo]
-      uint32_t x0[16], x1[16];
-      tmem_ld16(a, x0);
-      tmem_ld16(a + 32, x1);
+      uint32_t x0[NR], x1[NR];
+      tmem_ldn(a, x0);
+      tmem_ldn(a + 32, x1);
       tmem_wait_ld();
 #pragma unroll
       for (int i = 0; i < NR; ++i) v[i] = (__uint_as_float(x0[i]) + __uint_as_float(x1[i])) * wsc;
     } else {
-      uint32_t x0[16], x1[16], x2[16];
-      tmem_ld16(a, x0);
-      tmem_ld16(a + 32, x1);
-      tmem_ld16(a + 64, x2);
+      uint32_t x0[NR], x1[NR], x2[NR];
+      tmem_ldn(a, x0);
+      tmem_ldn(a + 32, x1);
+      tmem_ldn(a + 64, x2);
       tmem_wait_ld();
 #pragma unroll
       for (int i = 0; i < NR; ++i)
@@ -723,13 +737,13 @@ struct Epi {
     const int slot = (int)(s % NSLOT);
     const unsigned tg = step_tag(s);
     const int V1 = P.V1, VD = P.V1 + P.D;
-    const int lane = et & 31, q = m >> 5, hf = r0 ? 1 : 0;
+    const int lane = et & 31, q = m >> 5, grp = et >> 7;
     const int col = 128 * tile + m;
     // per-row argmax of the tile straight from registers: a warp reduce-scatter
-    // (16 rows over 32 lanes, 16 + 16 shuffles), then the 4 lane-quadrant warps
-    // of the same rows merge through smem in column order.  Ties keep the
-    // lowest column (argmax_last_into, tensor.cpp:283-289).
-    float2* rd = reinterpret_cast<float2*>(sm.red);  // [2 seg][2 half][4 q][16 rows]
+    // (NR rows over 32 lanes), then the 4 lane-quadrant warps of the same rows
+    // merge through smem in column order.  Ties keep the lowest column
+    // (argmax_last_into, tensor.cpp:283-289).
+    float2* rd = reinterpret_cast<float2*>(sm.red);  // [2 seg][WPQ grp][4 q][NR rows]
     unsigned long long* wst = reinterpret_cast<unsigned long long*>(sm.red + 128);  // [2 seg][32] word staging (after rd)
     const bool has_dur = P.D && 128 * tile + 127 >= V1 && 128 * tile < VD;
 #pragma unroll
@@ -737,24 +751,6 @@ struct Epi {
       if (seg == 1 && !has_dur) break;
       const bool valid = seg == 0 ? col < V1 : (col >= V1 && col < VD);
       const int cid = seg == 0 ? col : col - V1;
-#if ARGMAX_REDUX
-      // per row: warp max of an order-preserving key of the value, then the
-      // lowest column among the lanes holding it (two redux.sync per row)
-#pragma unroll
-      for (int i = 0; i < NR; ++i) {
-        unsigned u = __float_as_uint(valid ? v[i] : -INFINITY);
-        u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-        unsigned mk, mi;
-        asm volatile("redux.sync.max.u32 %0, %1, 0xffffffff;" : "=r"(mk) : "r"(u));
-        const unsigned cand = u == mk ? (unsigned)cid : 0xffffffffu;
-        asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(mi) : "r"(cand));
-        if (lane == i) {
-          const unsigned fb = (mk & 0x80000000u) ? (mk & 0x7fffffffu) : ~mk;
-          rd[((seg * 2 + hf) * 4 + q) * 16 + i] = make_float2(__uint_as_float(fb), __int_as_float((int)mi));
-        }
-      }
-    }
-#else
       float a[NR];
       int ai[NR];
 #pragma unroll
@@ -762,9 +758,11 @@ struct Epi {
         a[i] = valid ? v[i] : -INFINITY;
         ai[i] = cid;
       }
+      // scatter: lane bit (16 >> st) picks which half of the remaining rows
+      // this lane keeps; after LOG_NR stages lane bits 16.. hold the row
 #pragma unroll
-      for (int st = 0; st < 4; ++st) {
-        const int o = 16 >> st, n = 8 >> st;
+      for (int st = 0; st < LOG_NR; ++st) {
+        const int o = 16 >> st, n = (NR / 2) >> st;
         const bool up = (lane & o) != 0;
 #pragma unroll
         for (int i = 0; i < n; ++i) {
@@ -779,29 +777,32 @@ struct Epi {
           ai[i] = b ? goti : keepi;
         }
       }
-      {
-        const float got = __shfl_xor_sync(0xffffffffu, a[0], 1);
-        const int goti = __shfl_xor_sync(0xffffffffu, ai[0], 1);
+      // the remaining 32 / NR lanes per row hold the same row: plain reduce
+#pragma unroll
+      for (int o = (16 >> LOG_NR); o >= 1; o >>= 1) {
+        const float got = __shfl_xor_sync(0xffffffffu, a[0], o);
+        const int goti = __shfl_xor_sync(0xffffffffu, ai[0], o);
         const bool b = got > a[0] || (got == a[0] && goti < ai[0]);
         a[0] = b ? got : a[0];
         ai[0] = b ? goti : ai[0];
       }
-      if (!(lane & 1)) {
-        const int row = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-        rd[((seg * 2 + hf) * 4 + q) * 16 + row] = make_float2(a[0], __int_as_float(ai[0]));
+      if (!(lane & ((32 / NR) - 1))) {
+        int row = 0;
+#pragma unroll
+        for (int st = 0; st < LOG_NR; ++st) row += ((lane >> (4 - st)) & 1) * ((NR / 2) >> st);
+        rd[((seg * WPQ + grp) * 4 + q) * NR + row] = make_float2(a[0], __int_as_float(ai[0]));
       }
     }
-#endif
     mark(17);
     epi_sync();
     if (et < 64) {  // et < 32: vocab rows, 32..63: duration rows
-      const int seg = et >> 5, rr = et & 31, h2 = rr >> 4, row = rr & 15;
+      const int seg = et >> 5, rr = et & 31, g2 = rr / NR, row = rr % NR;
       if (seg == 0 || has_dur) {
         float bv = -INFINITY;
         int bi = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const float2 t = rd[((seg * 2 + h2) * 4 + k) * 16 + row];
+          const float2 t = rd[((seg * WPQ + g2) * 4 + k) * NR + row];
           if (t.x > bv) {  // quadrants in column order: strict > keeps the lowest column
             bv = t.x;
             bi = __float_as_int(t.y);
@@ -864,24 +865,26 @@ struct Epi {
 #pragma unroll
     for (int i = 0; i < NR; ++i) xs[m * 33 + r0 + i] = v[i];
     epi_sync();
+    constexpr int NW = NEPI / 32, CPW = 128 / NW;  // epilogue warps, columns per warp
     const int r = et & 31, qq = et >> 5;
-    const int c0 = 128 * tile + 16 * qq;
+    const int c0 = 128 * tile + CPW * qq;
+    float* redf = reinterpret_cast<float*>(sm.red);  // [NW][32] (rd / wst are done)
     // sumexp over the vocab columns relative to the tile's row max
     {
       const float M = sm.vdec[r];
       float ev = 0.0f;
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const float x = xs[(16 * qq + c) * 33 + r];
+      for (int c = 0; c < CPW; ++c) {
+        const float x = xs[(CPW * qq + c) * 33 + r];
         ev += (c0 + c < V1) ? __expf(x - M) : 0.0f;
       }
-      sm.red[qq * 32 + r].y = ev;
+      redf[qq * 32 + r] = ev;
     }
     epi_sync();
     if (et < 32) {
       float S = 0.0f;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) S += sm.red[k * 32 + et].y;
+      for (int k = 0; k < NW; ++k) S += redf[k * 32 + et];
       P.ps[((size_t)slot * P.NJ + tile) * 32 + et] = make_float2(sm.vdec[et], S);
     }
     epi_sync();
@@ -923,9 +926,9 @@ struct Epi {
       if (valid) {
         const unsigned long long* wv = P.pw + (((size_t)slot * 2 * P.NJ) * 32 + b) * PW_STRIDE;
         const unsigned long long* wd = wv + (size_t)P.NJ * 32 * PW_STRIDE;
-        unsigned long long a[MAXNJ], d[MAXNJ];
+        unsigned long long a[MAXNJ], d0 = 0ull, d1 = 0ull;
 #pragma unroll
-        for (int t = 0; t < MAXNJ; ++t) a[t] = d[t] = 0ull;
+        for (int t = 0; t < MAXNJ; ++t) a[t] = 0ull;
         // every tile's word in flight at once; only R_0 consumes the decision
         // on the critical path, the other roles back off
         const bool lazy = !(role == ROLE_R && layer == 0);
@@ -951,6 +954,8 @@ struct Epi {
         bool ok;
         const int nj = P.NJ;
         const bool hasd = P.D != 0;
+        // only the tiles holding duration columns carry duration partials
+        const int td0 = P.V1 / 128, td1 = (P.V1 + P.D - 1) / 128;
         int npoll = 0;
         long long lat1 = 0;
         if (tracer && role == ROLE_R && layer == 0 && b == 0) {  // one strong load, timed
@@ -983,17 +988,17 @@ struct Epi {
           for (int t = 0; t < MAXNJ; ++t)
             if (t < nj) a[t] = ld_poll_u64(wv + t * 32 * PW_STRIDE);
           if (hasd) {
-#pragma unroll
-            for (int t = 0; t < MAXNJ; ++t)
-              if (t < nj) d[t] = ld_poll_u64(wd + t * 32 * PW_STRIDE);
+            d0 = ld_poll_u64(wd + td0 * 32 * PW_STRIDE);
+            d1 = ld_poll_u64(wd + td1 * 32 * PW_STRIDE);
           }
           // branch-free tag check: a short-circuit && compiled to one branch +
           // reconvergence block per tile (~1000 cycles for 16 tiles)
-          unsigned bad = 0u;
+          unsigned bad = (unsigned)hasd & ((unsigned)((((unsigned)(d0 >> 32)) & 0xffu) != tg) |
+                                           (unsigned)((((unsigned)(d1 >> 32)) & 0xffu) != tg));
 #pragma unroll
           for (int t = 0; t < MAXNJ; ++t) {
-            const unsigned ta = (unsigned)(a[t] >> 32) & 0xffu, td = (unsigned)(d[t] >> 32) & 0xffu;
-            bad |= (unsigned)(t < nj) & ((unsigned)(ta != tg) | ((unsigned)hasd & (unsigned)(td != tg)));
+            const unsigned ta = (unsigned)(a[t] >> 32) & 0xffu;
+            bad |= (unsigned)(t < nj) & (unsigned)(ta != tg);
           }
           ok = bad == 0u;
           if (!ok && lazy && LAZY_NS) __nanosleep(LAZY_NS);
@@ -1002,8 +1007,6 @@ struct Epi {
         npoll_out = npoll;
         lat1_out = lat1;
         best = -INFINITY;
-        float bd = -INFINITY;
-        int di = 0;
         // selects, no branches; tiles in column order: strict > keeps the lowest
         // index (a 4-level tree merge measured 0.2 us/step slower)
 #pragma unroll
@@ -1012,11 +1015,10 @@ struct Epi {
           const bool tx = (t < nj) & (x > best);
           best = tx ? x : best;
           kk = tx ? (int)((unsigned)(a[t] >> 32) >> 8) : kk;
-          const float y = __uint_as_float((unsigned)d[t]);
-          const bool ty = hasd & (t < nj) & (y > bd);
-          bd = ty ? y : bd;
-          di = ty ? (int)((unsigned)(d[t] >> 32) >> 8) : di;
         }
+        // durations: tile td0 first (column order), td1 only if strictly greater
+        int di = (int)((unsigned)(d0 >> 32) >> 8);
+        if (__uint_as_float((unsigned)d1) > __uint_as_float((unsigned)d0)) di = (int)((unsigned)(d1 >> 32) >> 8);
         dd = hasd ? P.durations[di] : 0;
       }
       sm.kdec[b] = kk;
@@ -1033,7 +1035,7 @@ struct Epi {
         // gathers for the layer-0 cell overlap the rules below; this warp's
         // own gather (rows 0..15, labels of lanes 0..15) goes out first too
         __syncwarp();
-        asm volatile("barrier.cta.arrive.aligned 2, 256;" ::: "memory");
+        asm volatile("barrier.cta.arrive.aligned 2, %0;" ::"n"(NEPI) : "memory");
 #if EARLY_GATHER
         gather_table0();
 #endif
@@ -1143,7 +1145,7 @@ struct Epi {
       if (b == 0) sm.misc[5] = (accany ? 1 : 0) | (fin ? 2 : 0) | (frame_end ? 4 : 0);
       if (role == ROLE_R && layer == 0) mark(24);
     } else if (role == ROLE_R && layer == 0) {
-      asm volatile("barrier.cta.sync.aligned 2, 256;" ::: "memory");
+      asm volatile("barrier.cta.sync.aligned 2, %0;" ::"n"(NEPI) : "memory");
       mark2(35);
       gather_table0();
       mark2(36);
@@ -1202,10 +1204,11 @@ struct Epi {
   // LSTM tiles are unit-major (m = 4*unit + gate): a lane quad holds one unit's
   // i,f,g,o, so the gates meet through a per-warp smem transpose (__syncwarp,
   // no CTA barrier).  Lane (quad qd, slot g') then runs the cell for rows
-  // r0 + 4j + g', j < 4.
-  __device__ __forceinline__ void cell_lstm(const float (&pre)[NR], int l, int pe, float (&c)[4], float (&h)[4]) {
+  // r0 + 4j + g', j < NR / 4.
+  __device__ __forceinline__ void cell_lstm(const float (&pre)[NR], int l, int pe, float (&c)[NR / 4],
+                                            float (&h)[NR / 4]) {
     const int lane = et & 31, g = lane & 3, qd = lane >> 2;
-    float* xw = sm.xs + (et >> 5) * (NR * 33);  // this warp's [16 rows][33]
+    float* xw = sm.xs + (et >> 5) * (NR * 33);  // this warp's [NR rows][33]
     // i, f, o: sigmoid; g: tanh(x) = 2 sigmoid(2x) - 1 (absolute error ~1e-7,
     // what the cell update c' = f c + i g needs; one code path per lane quad)
     const float sc = g == 2 ? 2.0f : 1.0f;
@@ -1226,7 +1229,7 @@ struct Epi {
     unsigned char* ch = P.act[l] + ((size_t)(pe & 1) * P.act_kc[l] + (u >> 6)) * CHUNK;
 #endif
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NR / 4; ++j) {
       const int i = 4 * j + g, r = r0 + i;
       const float i_ = xw[i * 33 + 4 * qd], f_ = xw[i * 33 + 4 * qd + 1];
       const float g_ = xw[i * 33 + 4 * qd + 2], o_ = xw[i * 33 + 4 * qd + 3];
@@ -1356,9 +1359,9 @@ __device__ __forceinline__ void Epi::run_role() {
     const float* bl = P.bias[layer];
     const float bias_m = unit < P.H ? __ldg(&bl[gate * P.H + unit]) : 0.0f;
     const bool isr0 = role == ROLE_R;
-    float c4[4], h4[4], hr[NR];
+    float c4[NR / 4], h4[NR / 4], hr[NR];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) c4[j] = h4[j] = 0.0f;
+    for (int j = 0; j < NR / 4; ++j) c4[j] = h4[j] = 0.0f;
 #pragma unroll
     for (int j = 0; j < NR; ++j) hr[j] = 0.0f;
     run(
@@ -1430,7 +1433,10 @@ __device__ __forceinline__ void Epi::run_role() {
 }
 
 // ------------------------------------------------------------------ kernel
-__global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TParams P) {
+#ifndef LB_THREADS
+#define LB_THREADS NTH  // register budget = 65536 / LB_THREADS (A/B knob)
+#endif
+__global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constant__ TParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int4 rl = P.roles[blockIdx.x];
   const int role = rl.x, layer = rl.y, tile = rl.z;
@@ -1476,11 +1482,11 @@ __global__ void __launch_bounds__(NTH, 1) ptc_kernel(const __grid_constant__ TPa
       bulk_g2s(sm.whi + o, wimg + o, bytes - o < 32768 ? bytes - o : 32768, sm.wbar);
   }
   if (warp >= 2) {
-    const int q = warp & 3, half = warp >= 6;
+    const int q = warp & 3, grp = (warp - 2) >> 2;  // WPQ warps share a lane quadrant
     const uint32_t* lo = reinterpret_cast<const uint32_t*>(wimg + P.wtoff);
     const int m = 32 * q + lane;
     const int ncol = (KC + nlo_chunks(KC)) * 32;  // W_hi pairs, then the TMEM-resident W_lo pairs
-    for (int c0 = half * (ncol / 2); c0 < (half + 1) * (ncol / 2); c0 += 8) {
+    for (int c0 = grp * (ncol / WPQ); c0 < (grp + 1) * (ncol / WPQ); c0 += 8) {
       uint32_t r[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) r[j] = __ldg(lo + (size_t)(c0 + j) * 128 + m);
