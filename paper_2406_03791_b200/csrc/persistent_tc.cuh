@@ -112,6 +112,17 @@ constexpr bool LO_TMEM = LO_TMEM_CFG && SWAP_HILO_CFG;
 #define LO_SEPD_CFG 1  // LO_TMEM: W_lo.x_hi into its own 32 columns (no same-column accumulation)
 #endif
 constexpr bool LO_SEPD = LO_TMEM && LO_SEPD_CFG;
+#ifndef CHUNK_ASM_PLAIN
+// one elect.sync per chunk of 8 MMAs + stage commit (mma_chunk_ts2): the MMA
+// warp's issue rate bounds the load + MMA phases (A/B -0.23 us/step)
+#define CHUNK_ASM_PLAIN 1
+#endif
+#ifndef TMEM_BASE0
+// a CTA that allocates all 512 TMEM columns owns base address 0: use the
+// constant (checked) so ptxas can fold TMEM operand addresses into the MMA
+// issue instead of moving them to uniform registers per MMA
+#define TMEM_BASE0 0
+#endif
 #ifndef CHUNK_ASM
 #define CHUNK_ASM 1  // one elect.sync per chunk of 8 MMAs (see mma_chunk_tt)
 #endif
@@ -122,8 +133,14 @@ constexpr int ACC_COLS = LO_TMEM && !LO_SEPD ? 64 : 96;  // [x_hi | x_lo | lo.x_
 #ifndef NLO_MAX
 #define NLO_MAX 16
 #endif
-constexpr int NACC = LO_TMEM ? NACC_CFG : 2;  // accumulator sets
-constexpr int WLO_COL = NACC * ACC_COLS;     // first TMEM weight column (TMEM-resident W_hi pairs)
+#ifndef NACC_PLAIN
+#define NACC_PLAIN 1  // A/B: one accumulator set -0.05 us/step vs two
+#endif
+constexpr int NACC = LO_TMEM ? NACC_CFG : NACC_PLAIN;  // accumulator sets
+#ifndef WCOL_CFG
+#define WCOL_CFG 0  // A/B: first TMEM weight column override (0: right after the accumulators)
+#endif
+constexpr int WLO_COL = WCOL_CFG ? WCOL_CFG : NACC * ACC_COLS;  // first TMEM weight column (W_hi pairs)
 // chunks whose W_lo is TMEM-resident too (after the KC chunks of W_hi pairs)
 __host__ __device__ constexpr int nlo_chunks(int KC) {
   return LO_TMEM ? ((512 - WLO_COL) / 32 - KC < KC ? ((512 - WLO_COL) / 32 - KC < NLO_MAX ? (512 - WLO_COL) / 32 - KC : NLO_MAX)
@@ -276,6 +293,29 @@ __device__ __forceinline__ void mma_chunk_ts(uint32_t d, uint32_t ahi, uint64_t 
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l3, b3, %6, t;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}" ::"r"(d),
       "r"(ahi), "l"(alo), "l"(b), "r"(first), "r"(id64), "r"(id32), "r"(smem_u32(bar))
+      : "memory");
+}
+// as mma_chunk_ts with the W_lo product in its own columns d2 (no same-column
+// accumulation): D1[0:64) += A_hi x B, D2[0:32) += A_lo x B[:, 0:32)
+__device__ __forceinline__ void mma_chunk_ts2(uint32_t d1, uint32_t d2, uint32_t ahi, uint64_t alo, uint64_t b,
+                                              uint32_t first, uint32_t id64, uint32_t id32, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\t.reg .b32 h1, h2, h3;\n\t.reg .b64 l1, l2, l3, b1, b2, b3;\n\t"
+      "setp.eq.b32 p, %5, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+      "add.u32 h1, %2, 8;\n\tadd.u32 h2, %2, 16;\n\tadd.u32 h3, %2, 24;\n\t"
+      "add.u64 l1, %3, 2;\n\tadd.u64 l2, %3, 4;\n\tadd.u64 l3, %3, 6;\n\t"
+      "add.u64 b1, %4, 2;\n\tadd.u64 b2, %4, 4;\n\tadd.u64 b3, %4, 6;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %4, %6, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], %3, %4, %7, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h1], b1, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], l1, b1, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h2], b2, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], l2, b2, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h3], b3, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], l3, b3, %7, t;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n\t}" ::"r"(d1),
+      "r"(d2), "r"(ahi), "l"(alo), "l"(b), "r"(first), "r"(id64), "r"(id32), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -1471,7 +1511,8 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *sm.tslot;
+  const uint32_t tmem = TMEM_BASE0 ? 0u : *sm.tslot;
+  if (TMEM_BASE0 && *sm.tslot != 0u) __trap();  // never: 512 columns start at 0
   const unsigned char* wimg = P.wimg + (size_t)blockIdx.x * P.wstride;
 
   // ---- resident weights: W_hi -> smem (bulk copies), W_lo -> TMEM ----
@@ -1561,7 +1602,11 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
     const bool trj = P.prof && role == ROLE_J && (int)blockIdx.x == P.prof_first[role] && lane == 0;
     const bool stamp_ip = P.prof && (role == ROLE_I || role == ROLE_P) && (int)blockIdx.x == P.prof_first[role] && lane == 0;
     uint32_t fb = 0;  // bit s = fills of stage s consumed so far (mod 2)
+#ifdef NLO_FIXED
+    constexpr int nlo = NLO_FIXED;  // experiment: compile-time TMEM-resident W_lo chunk count (KC >= NLO_FIXED)
+#else
     const int nlo = nlo_chunks(KC);
+#endif
     for (int r = 0;; ++r) {
       mbar_wait(sm.cmd, r & 1);
       const int e = ((volatile int*)sm.misc)[r & 1];
@@ -1582,7 +1627,9 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
           if (tr && (kc == 0 || kc == KC - 1)) P.prof[(size_t)(kc ? 28 : 27) * PROF_WIN + (e - PROF_S0)] = gtimer();
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(whi0 + kc * 16384), bd = sdesc_sw128(ring0 + st * CHUNK);
-          if (LO_TMEM && CHUNK_ASM && !LO_SEPD) {  // W_lo.x_hi accumulates into the x_hi columns
+          if (!LO_TMEM && SWAP_HILO && CHUNK_ASM_PLAIN) {  // one elect per chunk (8 MMAs + stage commit)
+            mma_chunk_ts2(d1, d2, tmem + WLO_COL + kc * 32, ad, bd, kc == 0, ID64, ID32, &sm.empty[st]);
+          } else if (LO_TMEM && CHUNK_ASM && !LO_SEPD) {  // W_lo.x_hi accumulates into the x_hi columns
             if (kc < nlo)  // both weight halves from TMEM
               mma_chunk_tt(d1, tmem + WLO_COL + kc * 32, tmem + WLO_COL + (KC + kc) * 32, bd, kc == 0, ID64, ID32,
                            &sm.empty[st]);
@@ -1607,7 +1654,8 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
               }
             }
           }
-          if (!(LO_TMEM && CHUNK_ASM && !LO_SEPD)) mma_commit(&sm.empty[st]);  // (chunk asm commits itself)
+          if (!(LO_TMEM && CHUNK_ASM && !LO_SEPD) && !(!LO_TMEM && SWAP_HILO && CHUNK_ASM_PLAIN))
+            mma_commit(&sm.empty[st]);  // (the chunk asm commits itself)
         }
       }
       mma_commit(&sm.accf[set]);
