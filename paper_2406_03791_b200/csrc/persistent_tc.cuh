@@ -92,60 +92,31 @@ constexpr int NROLES = 5;
 #ifndef LAZY_BATCH_NS
 #define LAZY_BATCH_NS 0
 #endif
-#ifndef SWAP_HILO_CFG
-#define SWAP_HILO_CFG 1  // A/B: W_hi in TMEM (TS, N=64) + W_lo in smem (SS, N=32): -0.3 us/step
-#endif
-constexpr bool SWAP_HILO = SWAP_HILO_CFG;
-#ifndef LO_TMEM_CFG
-// W_lo of the first chunks in TMEM too: two TS MMAs per k-step pipeline (52
-// cycles resident, 72.6 in the load+MMA pipeline of scripts/mb_pipe2.cu) where
-// TS + SS serialise (63 / 78.2).  TMEM room comes from one 64-column
-// accumulator: W_lo.x_hi accumulates into the W_hi.x_hi columns (same 2^s
-// scale) or, with LO_SEPD, into its own 32 columns of one 96-column set.
-// Off: inside the executor every LO_TMEM build measured ~2 us/step SLOWER
-// (A/B: same-column 18.2 vs 15.9 us; separate columns 17.4 vs 15.4 us; rolled
-// MMA loops, so not instruction fetch), for reasons not pinned down.
-#define LO_TMEM_CFG 0
-#endif
-constexpr bool LO_TMEM = LO_TMEM_CFG && SWAP_HILO_CFG;
-#ifndef LO_SEPD_CFG
-#define LO_SEPD_CFG 1  // LO_TMEM: W_lo.x_hi into its own 32 columns (no same-column accumulation)
-#endif
-constexpr bool LO_SEPD = LO_TMEM && LO_SEPD_CFG;
-#ifndef CHUNK_ASM_PLAIN
-// one elect.sync per chunk of 8 MMAs + stage commit (mma_chunk_ts2): the MMA
-// warp's issue rate bounds the load + MMA phases (A/B -0.23 us/step)
-#define CHUNK_ASM_PLAIN 1
-#endif
-#ifndef TMEM_BASE0
-// a CTA that allocates all 512 TMEM columns owns base address 0: use the
-// constant (checked) so ptxas can fold TMEM operand addresses into the MMA
-// issue instead of moving them to uniform registers per MMA
-#define TMEM_BASE0 0
-#endif
-#ifndef CHUNK_ASM
-#define CHUNK_ASM 1  // one elect.sync per chunk of 8 MMAs (see mma_chunk_tt)
-#endif
-constexpr int ACC_COLS = LO_TMEM && !LO_SEPD ? 64 : 96;  // [x_hi | x_lo | lo.x_hi] (same-column LO_TMEM: [x_hi + lo.x_hi | x_lo])
-#ifndef NACC_CFG
-#define NACC_CFG 1
-#endif
+// Weight operand layout (per CTA, K = KC chunks of 64):
+//  - W_hi (fp16 pairs) in TMEM from column WLO_COL, chunk kc at WLO_COL + 32 kc;
+//    the product A_hi x [x_hi | x_lo] is a TS MMA with N = 64 into D1;
+//  - W_lo of the first nlo_chunks(KC) chunks in TMEM too (after W_hi), the rest
+//    as a SWIZZLE_128B smem image; A_lo x x_hi is TS (TMEM) or SS (smem), N = 32,
+//    into its own 32 columns D2.
+// One 96-column accumulator set [D1 (64) | D2 (32)] leaves 416 columns for
+// weights.  Measured per 16-deep k-step (scripts/mb_mma.cu, mb_pipe2.cu): TS+SS
+// ~78 cycles (SS is smem-read bound), TS+TS ~52; in the executor the TMEM-W_lo
+// chunks run ~280 cycles against ~340 (A/B -0.23 us/step).  A per-chunk runtime
+// branch between the two forms inside the unrolled loop cost ~2 us/step, so the
+// MMA warp dispatches once per round to a body templated on the chunk count.
+constexpr bool SWAP_HILO = true;  // W_hi in TMEM, W_lo (mostly) in smem: the packing convention
+constexpr int ACC_COLS = 96;      // [x_hi | x_lo | lo.x_hi] (one set)
+constexpr int NACC = 1;           // accumulator sets (two measured 0.05 us/step slower)
+constexpr int WLO_COL = NACC * ACC_COLS;  // first TMEM weight column
+constexpr int MAXNLO = (512 - WLO_COL) / 32 / 2;  // 6: bound of nlo_chunks over KC
 #ifndef NLO_MAX
-#define NLO_MAX 16
+#define NLO_MAX MAXNLO  // A/B knob: cap on the TMEM-resident W_lo chunks
 #endif
-#ifndef NACC_PLAIN
-#define NACC_PLAIN 1  // A/B: one accumulator set -0.05 us/step vs two
-#endif
-constexpr int NACC = LO_TMEM ? NACC_CFG : NACC_PLAIN;  // accumulator sets
-#ifndef WCOL_CFG
-#define WCOL_CFG 0  // A/B: first TMEM weight column override (0: right after the accumulators)
-#endif
-constexpr int WLO_COL = WCOL_CFG ? WCOL_CFG : NACC * ACC_COLS;  // first TMEM weight column (W_hi pairs)
 // chunks whose W_lo is TMEM-resident too (after the KC chunks of W_hi pairs)
 __host__ __device__ constexpr int nlo_chunks(int KC) {
-  return LO_TMEM ? ((512 - WLO_COL) / 32 - KC < KC ? ((512 - WLO_COL) / 32 - KC < NLO_MAX ? (512 - WLO_COL) / 32 - KC : NLO_MAX)
-                                                   : (KC < NLO_MAX ? KC : NLO_MAX))
-                 : 0;
+  return ((512 - WLO_COL) / 32 - KC < KC ? (512 - WLO_COL) / 32 - KC : KC) < NLO_MAX
+             ? ((512 - WLO_COL) / 32 - KC < KC ? (512 - WLO_COL) / 32 - KC : KC)
+             : NLO_MAX;
 }
 #ifndef WORDS_ONE_LANE
 #define WORDS_ONE_LANE 0
@@ -234,69 +205,12 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
   // D f32, A/B f16, both K-major
   return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
-// Issued by a converged warp; elect.sync picks one lane.
-__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(a), "l"(b), "r"(id), "r"(acc));
-}
-__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-      "r"(a), "l"(b), "r"(id), "r"(acc));
-}
-// One 64-deep chunk (4 k-steps) under ONE elect.sync, then the stage commit:
-// D[0:64) += A_hi x B (TMEM A, N = 64) and D[0:32) += A_lo x B[:, 0:32) with A_lo
-// from TMEM (tt) or a smem descriptor (ts).  A per-MMA elect block cost ~10
-// instructions of ELECT/VOTE/R2UR each; the MMA warp issued a chunk every ~470
-// cycles against ~230 of tensor-pipe work.  first: the chunk starts the tile
-// (its first MMA overwrites D).
-__device__ __forceinline__ void mma_chunk_tt(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t b, uint32_t first,
-                                             uint32_t id64, uint32_t id32, uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .pred p, t, e;\n\t.reg .b32 h1, h2, h3, l1, l2, l3;\n\t.reg .b64 b1, b2, b3;\n\t"
-      "setp.eq.b32 p, %4, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
-      "add.u32 h1, %1, 8;\n\tadd.u32 h2, %1, 16;\n\tadd.u32 h3, %1, 24;\n\t"
-      "add.u32 l1, %2, 8;\n\tadd.u32 l2, %2, 16;\n\tadd.u32 l3, %2, 24;\n\t"
-      "add.u64 b1, %3, 2;\n\tadd.u64 b2, %3, 4;\n\tadd.u64 b3, %3, 6;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %6, t;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h1], b1, %5, t;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l1], b1, %6, t;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h2], b2, %5, t;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l2], b2, %6, t;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h3], b3, %5, t;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l3], b3, %6, t;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}" ::"r"(d),
-      "r"(ahi), "r"(alo), "l"(b), "r"(first), "r"(id64), "r"(id32), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mma_chunk_ts(uint32_t d, uint32_t ahi, uint64_t alo, uint64_t b, uint32_t first,
-                                             uint32_t id64, uint32_t id32, uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .pred p, t, e;\n\t.reg .b32 h1, h2, h3;\n\t.reg .b64 l1, l2, l3, b1, b2, b3;\n\t"
-      "setp.eq.b32 p, %4, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
-      "add.u32 h1, %1, 8;\n\tadd.u32 h2, %1, 16;\n\tadd.u32 h3, %1, 24;\n\t"
-      "add.u64 l1, %2, 2;\n\tadd.u64 l2, %2, 4;\n\tadd.u64 l3, %2, 6;\n\t"
-      "add.u64 b1, %3, 2;\n\tadd.u64 b2, %3, 4;\n\tadd.u64 b3, %3, 6;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %6, t;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h1], b1, %5, t;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l1, b1, %6, t;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h2], b2, %5, t;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l2, b2, %6, t;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h3], b3, %5, t;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l3, b3, %6, t;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}" ::"r"(d),
-      "r"(ahi), "l"(alo), "l"(b), "r"(first), "r"(id64), "r"(id32), "r"(smem_u32(bar))
-      : "memory");
-}
-// as mma_chunk_ts with the W_lo product in its own columns d2 (no same-column
-// accumulation): D1[0:64) += A_hi x B, D2[0:32) += A_lo x B[:, 0:32)
+// One 64-deep chunk (4 k-steps of K = 16) under ONE elect.sync, then the
+// stage commit: D1[0:64) += A_hi x B (TMEM A, N = 64) and D2[0:32) +=
+// A_lo x B[:, 0:32) with A_lo from a smem descriptor (ts2) or TMEM (tt2).
+// A per-MMA elect block cost ~10 SASS instructions of ELECT/VOTE/R2UR each
+// and the MMA warp's issue rate paced the phases (A/B -0.23 us/step).  first:
+// the chunk starts the tile (its MMAs overwrite D1 / D2).
 __device__ __forceinline__ void mma_chunk_ts2(uint32_t d1, uint32_t d2, uint32_t ahi, uint64_t alo, uint64_t b,
                                               uint32_t first, uint32_t id64, uint32_t id32, uint64_t* bar) {
   asm volatile(
@@ -316,6 +230,28 @@ __device__ __forceinline__ void mma_chunk_ts2(uint32_t d1, uint32_t d2, uint32_t
       "@e tcgen05.mma.cta_group::1.kind::f16 [%1], l3, b3, %7, t;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n\t}" ::"r"(d1),
       "r"(d2), "r"(ahi), "l"(alo), "l"(b), "r"(first), "r"(id64), "r"(id32), "r"(smem_u32(bar))
+      : "memory");
+}
+// TS x TS chunk with the W_lo product in its own columns d2 (A_lo from TMEM)
+__device__ __forceinline__ void mma_chunk_tt2(uint32_t d1, uint32_t d2, uint32_t ahi, uint32_t alo, uint64_t b,
+                                              uint32_t first, uint32_t id64, uint32_t id32, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\t.reg .b32 h1, h2, h3, l1, l2, l3;\n\t.reg .b64 b1, b2, b3;\n\t"
+      "setp.eq.b32 p, %5, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+      "add.u32 h1, %2, 8;\n\tadd.u32 h2, %2, 16;\n\tadd.u32 h3, %2, 24;\n\t"
+      "add.u32 l1, %3, 8;\n\tadd.u32 l2, %3, 16;\n\tadd.u32 l3, %3, 24;\n\t"
+      "add.u64 b1, %4, 2;\n\tadd.u64 b2, %4, 4;\n\tadd.u64 b3, %4, 6;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %4, %6, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], [%3], %4, %7, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h1], b1, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], [l1], b1, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h2], b2, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], [l2], b2, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h3], b3, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], [l3], b3, %7, t;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n\t}" ::"r"(d1),
+      "r"(d2), "r"(ahi), "r"(alo), "l"(b), "r"(first), "r"(id64), "r"(id32), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -686,14 +622,7 @@ struct Epi {
     mbar_wait_sleep(&sm.accf[set], (uint32_t)(NACC == 1 ? (r & 1) : ((r >> 1) & 1)));
     tc_fence_after();
     const uint32_t a = tq + set * ACC_COLS + r0;
-    if (LO_TMEM && !LO_SEPD) {  // [W_hi.x_hi + W_lo.x_hi | W_hi.x_lo]
-      uint32_t x0[NR], x1[NR];
-      tmem_ldn(a, x0);
-      tmem_ldn(a + 32, x1);
-      tmem_wait_ld();
-#pragma unroll
-      for (int i = 0; i < NR; ++i) v[i] = (__uint_as_float(x0[i]) + __uint_as_float(x1[i])) * wsc;
-    } else {
+    {
       uint32_t x0[NR], x1[NR], x2[NR];
       tmem_ldn(a, x0);
       tmem_ldn(a + 32, x1);
@@ -1472,6 +1401,35 @@ __device__ __forceinline__ void Epi::run_role() {
   }
 }
 
+// ------------------------------------------------------------------ MMA round
+// One load + MMA round of the MMA warp over chunks [0, KC): the first NLO
+// chunks have W_lo in TMEM (TS x TS), the rest in smem (TS x SS); one elect
+// per chunk issues its 8 MMAs and the stage commit.
+template <int NLO>
+__device__ __forceinline__ void mma_round(const TParams& P, const Smem& sm, uint32_t& fb, int KC, uint32_t tmem,
+                                          uint32_t whi0, uint32_t ring0, bool ctr, bool tr, int e) {
+  constexpr uint32_t ID64 = idesc_f16(128, 64), ID32 = idesc_f16(128, 32);
+  const uint32_t d1 = tmem, d2 = tmem + 64;
+#pragma unroll  // (a rolled loop measured 0.45 us/step slower)
+  for (int kc = 0; kc < MAXKC; ++kc) {
+    if (kc < KC) {
+      const int st = kc % NSTAGE;
+      mbar_wait(&sm.full[st], (fb >> st) & 1u);
+      fb ^= 1u << st;
+      if (ctr) sm.dbg[16 + kc] = clock64();
+      if (tr && (kc == 0 || kc == KC - 1)) P.prof[(size_t)(kc ? 28 : 27) * PROF_WIN + (e - PROF_S0)] = gtimer();
+      tc_fence_after();
+      const uint64_t bd = sdesc_sw128(ring0 + st * CHUNK);
+      if (kc < NLO)
+        mma_chunk_tt2(d1, d2, tmem + WLO_COL + kc * 32, tmem + WLO_COL + (KC + kc) * 32, bd, kc == 0, ID64, ID32,
+                      &sm.empty[st]);
+      else
+        mma_chunk_ts2(d1, d2, tmem + WLO_COL + kc * 32, sdesc_sw128(whi0 + kc * 16384), bd, kc == 0, ID64, ID32,
+                      &sm.empty[st]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ kernel
 #ifndef LB_THREADS
 #define LB_THREADS NTH  // register budget = 65536 / LB_THREADS (A/B knob)
@@ -1511,8 +1469,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = TMEM_BASE0 ? 0u : *sm.tslot;
-  if (TMEM_BASE0 && *sm.tslot != 0u) __trap();  // never: 512 columns start at 0
+  const uint32_t tmem = *sm.tslot;
   const unsigned char* wimg = P.wimg + (size_t)blockIdx.x * P.wstride;
 
   // ---- resident weights: W_hi -> smem (bulk copies), W_lo -> TMEM ----
@@ -1596,67 +1553,28 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
     }
   } else if (warp == 1) {
     // ================= MMA issuer (converged warp) =================
-    constexpr uint32_t ID64 = idesc_f16(128, 64), ID32 = idesc_f16(128, 32);
     const uint32_t whi0 = smem_u32(sm.whi), ring0 = smem_u32(sm.ring);
     const bool ctr = P.prof && (role == ROLE_J || role == ROLE_I) && (int)blockIdx.x == P.prof_first[role] && lane == 0;
     const bool trj = P.prof && role == ROLE_J && (int)blockIdx.x == P.prof_first[role] && lane == 0;
     const bool stamp_ip = P.prof && (role == ROLE_I || role == ROLE_P) && (int)blockIdx.x == P.prof_first[role] && lane == 0;
     uint32_t fb = 0;  // bit s = fills of stage s consumed so far (mod 2)
-#ifdef NLO_FIXED
-    constexpr int nlo = NLO_FIXED;  // experiment: compile-time TMEM-resident W_lo chunk count (KC >= NLO_FIXED)
-#else
     const int nlo = nlo_chunks(KC);
-#endif
     for (int r = 0;; ++r) {
       mbar_wait(sm.cmd, r & 1);
       const int e = ((volatile int*)sm.misc)[r & 1];
       if (e < 0) break;
-      const int set = NACC == 1 ? 0 : (r & 1);
-      if (NACC == 1 && r >= 1) mbar_wait(&sm.acce[0], (uint32_t)((r - 1) & 1));
-      if (NACC == 2 && r >= 2) mbar_wait(&sm.acce[set], (uint32_t)(((r >> 1) - 1) & 1));
+      const int set = 0;
+      if (r >= 1) mbar_wait(&sm.acce[0], (uint32_t)((r - 1) & 1));  // the epilogue read the last round
       tc_fence_after();
-      const uint32_t d1 = tmem + set * ACC_COLS, d2 = LO_TMEM && !LO_SEPD ? d1 : d1 + 64;
       const bool tr = trj && e >= PROF_S0 && e < PROF_S0 + PROF_WIN;
-#pragma unroll  // (a rolled loop measured 0.45 us/step slower)
-      for (int kc = 0; kc < MAXKC; ++kc) {
-        if (kc < KC) {
-          const int st = kc % NSTAGE;
-          mbar_wait(&sm.full[st], (fb >> st) & 1u);
-          fb ^= 1u << st;
-          if (ctr) sm.dbg[16 + kc] = clock64();
-          if (tr && (kc == 0 || kc == KC - 1)) P.prof[(size_t)(kc ? 28 : 27) * PROF_WIN + (e - PROF_S0)] = gtimer();
-          tc_fence_after();
-          const uint64_t ad = sdesc_sw128(whi0 + kc * 16384), bd = sdesc_sw128(ring0 + st * CHUNK);
-          if (!LO_TMEM && SWAP_HILO && CHUNK_ASM_PLAIN) {  // one elect per chunk (8 MMAs + stage commit)
-            mma_chunk_ts2(d1, d2, tmem + WLO_COL + kc * 32, ad, bd, kc == 0, ID64, ID32, &sm.empty[st]);
-          } else if (LO_TMEM && CHUNK_ASM && !LO_SEPD) {  // W_lo.x_hi accumulates into the x_hi columns
-            if (kc < nlo)  // both weight halves from TMEM
-              mma_chunk_tt(d1, tmem + WLO_COL + kc * 32, tmem + WLO_COL + (KC + kc) * 32, bd, kc == 0, ID64, ID32,
-                           &sm.empty[st]);
-            else
-              mma_chunk_ts(d1, tmem + WLO_COL + kc * 32, ad, bd, kc == 0, ID64, ID32, &sm.empty[st]);
-          } else if (LO_TMEM && kc < nlo) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              mma_ts(d1, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID64, (kc | k) != 0);
-              mma_ts(d2, tmem + WLO_COL + (KC + kc) * 32 + k * 8, bd + 2 * k, ID32, LO_SEPD ? (kc | k) != 0 : 1u);
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t acc = (kc | k) != 0;
-              if (SWAP_HILO) {  // W_hi from TMEM (N = 64), W_lo from smem (N = 32)
-                mma_ts(d1, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID64, acc);
-                mma_ss(d2, ad + 2 * k, bd + 2 * k, ID32, LO_TMEM && !LO_SEPD ? 1u : acc);
-              } else {
-                mma_ss(d1, ad + 2 * k, bd + 2 * k, ID64, acc);
-                mma_ts(d2, tmem + WLO_COL + kc * 32 + k * 8, bd + 2 * k, ID32, acc);
-              }
-            }
-          }
-          if (!(LO_TMEM && CHUNK_ASM && !LO_SEPD) && !(!LO_TMEM && SWAP_HILO && CHUNK_ASM_PLAIN))
-            mma_commit(&sm.empty[st]);  // (the chunk asm commits itself)
-        }
+      switch (nlo) {  // once per round: no per-chunk branch between the two MMA forms
+        case 0: mma_round<0>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
+        case 1: mma_round<1>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
+        case 2: mma_round<2>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
+        case 3: mma_round<3>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
+        case 4: mma_round<4>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
+        case 5: mma_round<5>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
+        default: mma_round<MAXNLO>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
       }
       mma_commit(&sm.accf[set]);
       if (ctr) sm.dbg[31] = clock64();

@@ -554,7 +554,7 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   const int bse = 1 + 3 * L;
   // per CTA: [KCmax][16 KB] smem image, then TMEM column pairs (u32 = 2 fp16
   // along k) for 128 lanes: the KC chunks' TMEM-resident half, then W_lo of
-  // the first nlo_chunks(KC) chunks (ptc::LO_TMEM)
+  // the first nlo_chunks(KC) chunks
   const size_t wtoff = (size_t)KCmax * 16384;
   int tcols = 0;
   for (int kc : {Hp / 64, Jp / 64}) tcols = std::max(tcols, (kc + ptc::nlo_chunks(kc)) * 32);
