@@ -86,6 +86,9 @@ constexpr int NROLES = 5;
 #ifndef WORD_READBACK
 #define WORD_READBACK 0  // A/B: no gain
 #endif
+#ifndef TANH_SIG
+#define TANH_SIG 1
+#endif
 #ifndef EARLY_GATHER
 #define EARLY_GATHER 1  // rules warp's table0 loads go out before the rules
 #endif
@@ -1204,7 +1207,9 @@ struct Epi {
       const float g_ = xw[i * 33 + 4 * qd + 2], o_ = xw[i * 33 + 4 * qd + 3];
       const bool commit = r < B && (sm.flag[r] & 2);
       const float cn = f_ * c[j] + i_ * g_;
-      const float hn = u < P.H ? o_ * tanh_fast(cn) : 0.0f;
+      // tanh(c) = 2 sigm(2c) - 1 like the g gate (absolute error ~1e-7, what
+      // h = o tanh(c) needs): no polynomial branch on the dependency chain
+      const float hn = u < P.H ? o_ * (TANH_SIG ? fmaf(2.0f, sigm(2.0f * cn), -1.0f) : tanh_fast(cn)) : 0.0f;
       c[j] = commit ? cn : c[j];
       h[j] = commit ? hn : h[j];
 #if TMA_ACT
