@@ -503,7 +503,18 @@ __device__ inline Smem carve(unsigned char* raw, int KC) {
 
 // Branchless activations (~1e-7 relative): the libm versions carry slow-path
 // calls that serialise the 32-row unrolled epilogue loops.
-__device__ __forceinline__ float sigm(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+#ifndef SIGM_FTZ
+#define SIGM_FTZ 1  // sigmoid from ex2/rcp .approx.ftz: no subnormal fix-ups on the chain
+#endif
+__device__ __forceinline__ float sigm(float x) {
+  if (SIGM_FTZ) {
+    float e, r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * -1.4426950408889634f));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+    return r;
+  }
+  return __fdividef(1.0f, 1.0f + __expf(-x));
+}
 // (an FMA-pipe Newton reciprocal for the gate sigmoids, halving the MUFU ops,
 // measured 0.25 us/step slower: the cell is not MUFU-bound)
 __device__ __forceinline__ float tanh_fast(float x) {
