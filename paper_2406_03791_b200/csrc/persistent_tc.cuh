@@ -1212,17 +1212,32 @@ struct Epi {
     unsigned char* ch = P.act[l] + ((size_t)(pe & 1) * P.act_kc[l] + (u >> 6)) * CHUNK;
 #endif
 #pragma unroll
+    // loads, arithmetic and stores in separate passes: the compiler cannot move
+    // a later row's xw loads above an earlier row's st16 stores (both shared
+    // memory), which serialised the NR / 4 per-row dependency chains
+    float gi[NR / 4], gf[NR / 4], gg[NR / 4], go[NR / 4];
+    bool cm[NR / 4];
+#pragma unroll
     for (int j = 0; j < NR / 4; ++j) {
       const int i = 4 * j + g, r = r0 + i;
-      const float i_ = xw[i * 33 + 4 * qd], f_ = xw[i * 33 + 4 * qd + 1];
-      const float g_ = xw[i * 33 + 4 * qd + 2], o_ = xw[i * 33 + 4 * qd + 3];
-      const bool commit = r < B && (sm.flag[r] & 2);
-      const float cn = f_ * c[j] + i_ * g_;
+      gi[j] = xw[i * 33 + 4 * qd];
+      gf[j] = xw[i * 33 + 4 * qd + 1];
+      gg[j] = xw[i * 33 + 4 * qd + 2];
+      go[j] = xw[i * 33 + 4 * qd + 3];
+      cm[j] = r < B && (sm.flag[r] & 2);
+    }
+#pragma unroll
+    for (int j = 0; j < NR / 4; ++j) {
+      const float cn = gf[j] * c[j] + gi[j] * gg[j];
       // tanh(c) = 2 sigm(2c) - 1 like the g gate (absolute error ~1e-7, what
       // h = o tanh(c) needs): no polynomial branch on the dependency chain
-      const float hn = u < P.H ? o_ * (TANH_SIG ? fmaf(2.0f, sigm(2.0f * cn), -1.0f) : tanh_fast(cn)) : 0.0f;
-      c[j] = commit ? cn : c[j];
-      h[j] = commit ? hn : h[j];
+      const float hn = u < P.H ? go[j] * (TANH_SIG ? fmaf(2.0f, sigm(2.0f * cn), -1.0f) : tanh_fast(cn)) : 0.0f;
+      c[j] = cm[j] ? cn : c[j];
+      h[j] = cm[j] ? hn : h[j];
+    }
+#pragma unroll
+    for (int j = 0; j < NR / 4; ++j) {
+      const int r = r0 + 4 * j + g;
 #if TMA_ACT
       const __half hh = __float2half_rn(h[j]);
       st16[r * 32 + ul] = hh;
