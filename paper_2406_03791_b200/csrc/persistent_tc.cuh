@@ -74,17 +74,11 @@ constexpr int CSTRIDE = 32;      // u32 words between counters (one 128-byte lin
 
 enum Role { ROLE_J = 0, ROLE_P = 1, ROLE_R = 2, ROLE_I = 3, ROLE_E = 4 };  // E: emitter (no weights)
 constexpr int NROLES = 5;
-#ifndef WORDS_DIRECT
-#define WORDS_DIRECT 1  // A/B: direct tagged words 20.17 us/step vs bulk + counter 20.65
-#endif
 #ifndef POLL_NS
 #define POLL_NS 0
 #endif
 #ifndef ECHO_GATE
 #define ECHO_GATE 0  // A/B: gating 55 pollers behind an R_0 echo cost 0.3 us/step
-#endif
-#ifndef WORD_READBACK
-#define WORD_READBACK 0  // A/B: no gain
 #endif
 #ifndef TANH_SIG
 #define TANH_SIG 1
@@ -121,9 +115,6 @@ __host__ __device__ constexpr int nlo_chunks(int KC) {
              ? ((512 - WLO_COL) / 32 - KC < KC ? (512 - WLO_COL) / 32 - KC : KC)
              : NLO_MAX;
 }
-#ifndef WORDS_ONE_LANE
-#define WORDS_ONE_LANE 0
-#endif
 #ifndef ACK_RELAXED
 #define ACK_RELAXED 1
 #endif
@@ -146,7 +137,6 @@ __host__ __device__ inline int cidx_act(int buf, int kc) { return buf * MAXKC + 
 __host__ __device__ inline int cidx_hh(int l, int t) { return MAXBUF * MAXKC + l * 64 + t; }
 __host__ __device__ inline int cidx_part() { return MAXBUF * MAXKC + MAXL * 64; }
 __host__ __device__ inline int cidx_ack() { return cidx_part() + 1; }
-__host__ __device__ inline int cidx_words(bool r0) { return cidx_part() + (r0 ? 2 : 3); }
 constexpr int NCOUNTERS = MAXBUF * MAXKC + MAXL * 64 + 5;  // last: ECHO_GATE decided word
 
 struct TParams {
@@ -727,7 +717,6 @@ struct Epi {
     // merge through smem in column order.  Ties keep the lowest column
     // (argmax_last_into, tensor.cpp:283-289).
     float2* rd = reinterpret_cast<float2*>(sm.red);  // [2 seg][WPQ grp][4 q][NR rows]
-    unsigned long long* wst = reinterpret_cast<unsigned long long*>(sm.red + 128);  // [2 seg][32] word staging (after rd)
     const bool has_dur = P.D && 128 * tile + 127 >= V1 && 128 * tile < VD;
 #pragma unroll
     for (int seg = 0; seg < 2; ++seg) {
@@ -791,31 +780,11 @@ struct Epi {
             bi = __float_as_int(t.y);
           }
         }
-        wst[seg * 32 + rr] = pack_arg(bv, bi, tg);
+        // the tagged word goes out straight from the merging thread (no staging
+        // barrier); tiles without duration columns publish no duration word
+        st_relaxed_u64(P.pw + (((size_t)slot * 2 + seg) * P.NJ + tile) * 32 + rr, pack_arg(bv, bi, tg));
         if (seg == 0) sm.vdec[rr] = bv;  // this tile's row max, for the sumexp pass
-
-      } else if (P.D) {  // tile without duration columns: an empty duration partial
-        wst[32 + rr] = pack_arg(-INFINITY, 0, tg);
       }
-    }
-#if WORDS_DIRECT
-    epi_sync();
-#if WORDS_ONE_LANE
-    if (et == 0)
-      for (int i = 0; i < (P.D ? 64 : 32); ++i)
-        st_relaxed_u64(P.pw + (((size_t)slot * 2 + (i >> 5)) * P.NJ + tile) * 32 + (i & 31), wst[i]);
-    if (false) {
-#else
-    if (et < 64 && (et < 32 || P.D)) {
-#endif
-      unsigned long long* wp = P.pw + (((size_t)slot * 2 + (et >> 5)) * P.NJ + tile) * 32 + (et & 31);
-      st_relaxed_u64(wp, wst[et]);
-#if WORD_READBACK
-      // read the word back: measured to push the line out (a warp-wide strong
-      // store with no memory traffic after it took ~2 us to become visible)
-      volatile unsigned long long rb = ld_poll_u64(wp);
-      (void)rb;
-#endif
     }
     if (P.echo && tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) {
       // exact J -> R_0 -> J round trip on this SM's clock: J bumps a probe word,
@@ -826,20 +795,6 @@ struct Epi {
       }
       P.prof[(size_t)37 * PROF_WIN + (s - PROF_S0)] = clock64() - c0;
     }
-#else
-    // publish the words like activation chunks (bulk store, wait_group, relaxed
-    // counter)
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    epi_sync();
-    if (et == 0) {
-      unsigned long long* dst = P.pw + (((size_t)slot * 2) * P.NJ + tile) * 32;
-      bulk_s2g(dst, wst, 256);
-      if (P.D) bulk_s2g(dst + (size_t)P.NJ * 32, wst + 32, 256);
-      bulk_commit_wait_all();
-      red_relaxed_add(cnt + (size_t)cidx_words(true) * CSTRIDE, 1);  // polled by R_0 only
-      red_relaxed_add(cnt + (size_t)cidx_words(false) * CSTRIDE, 1);
-    }
-#endif
     mark(18);
     gmark(42);
     mark_pub();
@@ -851,7 +806,7 @@ struct Epi {
     constexpr int NW = NEPI / 32, CPW = 128 / NW;  // epilogue warps, columns per warp
     const int r = et & 31, qq = et >> 5;
     const int c0 = 128 * tile + CPW * qq;
-    float* redf = reinterpret_cast<float*>(sm.red);  // [NW][32] (rd / wst are done)
+    float* redf = reinterpret_cast<float*>(sm.red);  // [NW][32] (rd is done)
     // sumexp over the vocab columns relative to the tile's row max
     {
       const float M = sm.vdec[r];
@@ -927,12 +882,6 @@ struct Epi {
           __syncwarp(0xffffffffu >> (32 - B));
         }
 #endif
-        if (!WORDS_DIRECT && b == 0) {
-          const unsigned* wc = cnt + (size_t)cidx_words(!lazy) * CSTRIDE;
-          const unsigned target = (unsigned)P.NJ * (unsigned)(s + 1);
-          while (ld_relaxed(wc) < target)
-            if (lazy) __nanosleep(500);
-        }
         __syncwarp(0xffffffffu >> (32 - B));
         bool ok;
         const int nj = P.NJ;
