@@ -228,6 +228,11 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent):
     Hp = (H + 63) // 64 * 64
     Jp = (J + 63) // 64 * 64
     Bp = (Bl + 31) // 32 * 32
+    # the tensor executor runs B > 32 as ceil(B / 32) balanced sub-decodes back to
+    # back (one persistent launch each; stats are summed over them, and
+    # rnntg_time_kernel times one of them): count per launch at the sub-batch size
+    n_sub = (Bl + 31) // 32 if (persistent and args.exec == "tensor" and Bl > 32) else 1
+    Brow = Bl / n_sub
     V1 = V + 1
     V1p = (V1 + 15) // 16 * 16
     Dn = len(durs)
@@ -240,18 +245,18 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent):
         "pred_proj": 4 * (Hp * Jp + Bp * Hp + Bp * Jp),
         "joint": 4 * (Jp * V1p + 2 * Bp * Jp),
         "enc_proj": 4 * (Bl * T * F + F * Jp + Bl * T * Jp),
-        "persistent": st.pred_steps * pred_w + st.joint_evals * joint_w,
+        "persistent": (st.pred_steps * pred_w + st.joint_evals * joint_w) / n_sub,
     }
-    pred_f = 2 * Bl * (4 * H * H * (2 * L - 1) + H * J)
-    joint_f = 2 * Bl * J * (V1 + Dn)
+    pred_f = 2 * Brow * (4 * H * H * (2 * L - 1) + H * J)
+    joint_f = 2 * Brow * J * (V1 + Dn)
     flops_per = {
         "pred_layer1": 2 * Bl * 2 * H * 4 * H, "pred_layer0": 2 * Bl * H * 4 * H,
         "pred_proj": 2 * Bl * H * J, "joint": 2 * Bl * J * V1, "enc_proj": 2 * Bl * T * F * J,
-        "persistent": st.pred_steps * pred_f + st.joint_evals * joint_f,
+        "persistent": (st.pred_steps * pred_f + st.joint_evals * joint_f) / n_sub,
     }
     per_step_counts = {"enc_proj": 1, "pred_layer0": st.pred_steps,
                        "pred_layer1": st.pred_steps if L > 1 else 0,
-                       "pred_proj": st.pred_steps, "joint": st.joint_evals, "persistent": 1}
+                       "pred_proj": st.pred_steps, "joint": st.joint_evals, "persistent": n_sub}
     share = {n: kern[n] * per_step_counts[n] / ms_per_step for n in kern}
     dom = max(share, key=share.get)
     peaks = {}
@@ -299,6 +304,7 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent):
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)",
             "algorithmic_bytes_per_launch": bytes_per[dom],
             "avg_launch_us": kern[dom] * 1000.0,
+            "launches_per_step": per_step_counts[dom],
             "fp32": {"achieved_tflops": fp32_ach, "peak_tflops": fp32_peak,
                      "frac": fp32_ach / fp32_peak,
                      "note": "FFMA peak = 148 SM x 128 lanes x 2 x median SM clock under load"},
