@@ -124,6 +124,11 @@ __host__ __device__ constexpr int nlo_chunks(int KC) {
 #ifndef TMA_ACT
 #define TMA_ACT 1  // activations via 2-D tensor maps (plain row-major in global, swizzled by TMA)
 #endif
+// The event trace (RNNTG_PROF) lives in a separate instantiation of the kernel
+// (template flag TR): compiled into the product kernel, its runtime-gated code
+// cost 0.42 us/step at C2 (~3400 of ~24200 SASS instructions; A/B)
+#define PPROF(X) (TR ? (X).prof : (unsigned long long*)nullptr)
+#define PECHO(X) (TR ? (X).echo : (unsigned long long*)nullptr)
 #ifndef LAZY_NS
 #define LAZY_NS 0  // A/B: 500 ns backoff for non-critical pollers cost 0.09 us/step
 #endif
@@ -529,6 +534,7 @@ __device__ __forceinline__ float tanh_fast(float x) {
 // tile row m = 32*q + lane is this thread's TMEM lane (q = warp & 3, the
 // quadrant a warp may address), and it owns batch rows r0 .. r0+15 of it
 // (r0 = 16 * (et >= 128)): the two warps of a quadrant split the rows.
+template <bool TR>
 struct Epi {
   const TParams& P;
   const Smem& sm;
@@ -549,30 +555,30 @@ struct Epi {
         r0(NR * (et_ >> 7)), role(role_),
         layer(layer_), tile(tile_), wsc(wsc_), B(P_.B), blank(P_.V1 - 1), fs(P_.algo == ALGO_FS),
         tdt(P_.algo == ALGO_TDT), lstm(P_.cell == 1),
-        tracer(P_.prof && (int)blockIdx.x == P_.prof_first[role_]), cnt(P_.cnt) {}
+        tracer(PPROF(P_) && (int)blockIdx.x == P_.prof_first[role_]), cnt(P_.cnt) {}
 
   // per-CTA publish time of step s (all CTAs): prof[(NEV + cta) * PROF_WIN + s - PROF_S0]
   __device__ __forceinline__ void mark_pub() {
-    if (P.prof && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN)
-      P.prof[(size_t)(NEV + blockIdx.x) * PROF_WIN + (s - PROF_S0)] = gtimer();
+    if (PPROF(P) && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN)
+      PPROF(P)[(size_t)(NEV + blockIdx.x) * PROF_WIN + (s - PROF_S0)] = gtimer();
   }
   // hand-off marks (globaltimer, cross-CTA): 40 P trunk published, 42 J words
   // stored, 43 R0 words seen, 44 R0 h0 published, 46 I1 h1 published
   __device__ __forceinline__ void gmark(int ev) {
     if (tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN)
-      P.prof[(size_t)ev * PROF_WIN + (s - PROF_S0)] = gtimer();
+      PPROF(P)[(size_t)ev * PROF_WIN + (s - PROF_S0)] = gtimer();
   }
   // clock64 mark by thread et == 32 (second epilogue warp)
   __device__ __forceinline__ void mark2(int ev) {
     if (tracer && et == 32 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN)
-      P.prof[(size_t)(NEV + P.G + ev) * PROF_WIN + (s - PROF_S0)] = clock64();
+      PPROF(P)[(size_t)(NEV + P.G + ev) * PROF_WIN + (s - PROF_S0)] = clock64();
   }
   // ev < 32: globaltimer (cross-CTA), ev + 32 slot block: clock64 (intra-CTA, exact)
   __device__ __forceinline__ void mark(int ev) {
     if (tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) {
       // globaltimer reads queue behind outstanding loads: only at step start
-      if (ev == 0) P.prof[(size_t)ev * PROF_WIN + (s - PROF_S0)] = gtimer();
-      P.prof[(size_t)(NEV + P.G + ev) * PROF_WIN + (s - PROF_S0)] = clock64();
+      if (ev == 0) PPROF(P)[(size_t)ev * PROF_WIN + (s - PROF_S0)] = gtimer();
+      PPROF(P)[(size_t)(NEV + P.G + ev) * PROF_WIN + (s - PROF_S0)] = clock64();
     }
   }
   // I1 / P: producer chunk-0 / last-chunk issue and MMA-issued times of this
@@ -580,7 +586,7 @@ struct Epi {
   __device__ __forceinline__ void log_ld(int ev0) {
     if (tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) {
       const volatile unsigned long long* t = reinterpret_cast<const volatile unsigned long long*>(sm.misc + 8);
-      for (int k = 0; k < 3; ++k) P.prof[(size_t)(ev0 + k) * PROF_WIN + (s - PROF_S0)] = t[k];
+      for (int k = 0; k < 3; ++k) PPROF(P)[(size_t)(ev0 + k) * PROF_WIN + (s - PROF_S0)] = t[k];
     }
   }
   // J / I1: per-chunk load-issue and full times, MMA-issued and acc-ready
@@ -590,16 +596,16 @@ struct Epi {
       const volatile unsigned long long* t = sm.dbg;
       const int KC = P.act_kc[role == ROLE_J ? TRUNK : layer - 1];
       for (int k = 0; k < KC && k < 10; ++k) {
-        P.prof[(size_t)(ev0 + k) * PROF_WIN + (s - PROF_S0)] = t[k];
-        P.prof[(size_t)(ev0 + 10 + k) * PROF_WIN + (s - PROF_S0)] = t[16 + k];
+        PPROF(P)[(size_t)(ev0 + k) * PROF_WIN + (s - PROF_S0)] = t[k];
+        PPROF(P)[(size_t)(ev0 + 10 + k) * PROF_WIN + (s - PROF_S0)] = t[16 + k];
       }
-      P.prof[(size_t)(ev0 + 20) * PROF_WIN + (s - PROF_S0)] = t[31];
-      P.prof[(size_t)(ev0 + 21) * PROF_WIN + (s - PROF_S0)] = (unsigned long long)tacc;
-      P.prof[(size_t)(ev0 + 22) * PROF_WIN + (s - PROF_S0)] = t[11] - t[10];  // polls after chunk 0
-      P.prof[(size_t)(ev0 + 23) * PROF_WIN + (s - PROF_S0)] = t[12];  // chunk 2: before empty wait
-      P.prof[(size_t)(ev0 + 24) * PROF_WIN + (s - PROF_S0)] = t[13];  // chunk 2: after TMA issue
+      PPROF(P)[(size_t)(ev0 + 20) * PROF_WIN + (s - PROF_S0)] = t[31];
+      PPROF(P)[(size_t)(ev0 + 21) * PROF_WIN + (s - PROF_S0)] = (unsigned long long)tacc;
+      PPROF(P)[(size_t)(ev0 + 22) * PROF_WIN + (s - PROF_S0)] = t[11] - t[10];  // polls after chunk 0
+      PPROF(P)[(size_t)(ev0 + 23) * PROF_WIN + (s - PROF_S0)] = t[12];  // chunk 2: before empty wait
+      PPROF(P)[(size_t)(ev0 + 24) * PROF_WIN + (s - PROF_S0)] = t[13];  // chunk 2: after TMA issue
       for (int k = 0; k < KC && k < 10; ++k)  // chunk landed (observer warp)
-        P.prof[(size_t)(ev0 + 25 + k) * PROF_WIN + (s - PROF_S0)] = t[32 + k];
+        PPROF(P)[(size_t)(ev0 + 25 + k) * PROF_WIN + (s - PROF_S0)] = t[32 + k];
     }
   }
   // one load+MMA round on this CTA's input at epoch e (-1 = exit)
@@ -703,7 +709,7 @@ struct Epi {
     read_acc(round - 1, v);
     mark(1);
     mark(16);
-    const long long tacc = P.prof ? clock64() : 0;
+    const long long tacc = PPROF(P) ? clock64() : 0;
     // slot reuse: every CTA has finished decide(s - NSLOT); checked once per half window
     if (s >= NSLOT / 2 && s % (NSLOT / 2) == 0)
       wait_counter(cidx_ack(), (unsigned)P.G * (unsigned)(s - NSLOT / 2 + 1));
@@ -786,19 +792,19 @@ struct Epi {
         if (seg == 0) sm.vdec[rr] = bv;  // this tile's row max, for the sumexp pass
       }
     }
-    if (P.echo && tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) {
+    if (PECHO(P) && tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) {
       // exact J -> R_0 -> J round trip on this SM's clock: J bumps a probe word,
       // R_0 tile 0 (spinning on it) echoes the step
       const long long c0 = clock64();
-      st_relaxed_u64(P.echo + 8, (unsigned long long)(s + 1));
-      while (ld_poll_u64(P.echo) != (unsigned long long)(s + 1)) {
+      st_relaxed_u64(PECHO(P) + 8, (unsigned long long)(s + 1));
+      while (ld_poll_u64(PECHO(P)) != (unsigned long long)(s + 1)) {
       }
-      P.prof[(size_t)37 * PROF_WIN + (s - PROF_S0)] = clock64() - c0;
+      PPROF(P)[(size_t)37 * PROF_WIN + (s - PROF_S0)] = clock64() - c0;
     }
     mark(18);
     gmark(42);
     mark_pub();
-    if (P.prof) log_chunks(56, tacc);  // trace only, after the critical part
+    if (PPROF(P)) log_chunks(56, tacc);  // trace only, after the critical part
     float* xs = sm.xs;  // [128 cols][33]
 #pragma unroll
     for (int i = 0; i < NR; ++i) xs[m * 33 + r0 + i] = v[i];
@@ -847,10 +853,10 @@ struct Epi {
   // The emitter also merges the (max, sumexp) partials for the score.
   __device__ void decide() {
     if (role == ROLE_R && layer == 0) gmark(41);
-    if (P.echo && role == ROLE_R && layer == 0 && tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) {
-      while (ld_poll_u64(P.echo + 8) != (unsigned long long)(s + 1)) {
+    if (PECHO(P) && role == ROLE_R && layer == 0 && tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) {
+      while (ld_poll_u64(PECHO(P) + 8) != (unsigned long long)(s + 1)) {
       }
-      st_relaxed_u64(P.echo, (unsigned long long)(s + 1));
+      st_relaxed_u64(PECHO(P), (unsigned long long)(s + 1));
     }
     if (et < 32) {
       const int b = et;
@@ -960,8 +966,8 @@ struct Epi {
 #endif
 
       if (role == ROLE_R && layer == 0 && tracer && b == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN)
-        P.prof[(size_t)39 * PROF_WIN + (s - PROF_S0)] = (unsigned long long)npoll_out,
-        P.prof[(size_t)38 * PROF_WIN + (s - PROF_S0)] = (unsigned long long)lat1_out;
+        PPROF(P)[(size_t)39 * PROF_WIN + (s - PROF_S0)] = (unsigned long long)npoll_out,
+        PPROF(P)[(size_t)38 * PROF_WIN + (s - PROF_S0)] = (unsigned long long)lat1_out;
       if (role == ROLE_R && layer == 0) {
         // hand the labels to the other 7 epilogue warps now: their table0
         // gathers for the layer-0 cell overlap the rules below; this warp's
@@ -1231,7 +1237,8 @@ struct Epi {
   __device__ void run_role();
 };
 
-__device__ __forceinline__ void Epi::run_role() {
+template <bool TR>
+__device__ __forceinline__ void Epi<TR>::run_role() {
   const int unit = lstm ? 32 * tile + (m >> 2) : 128 * tile + m;  // LSTM tiles: m = 4*unit + gate
   const int gate = lstm ? (m & 3) : 0;
   if (role == ROLE_J || role == ROLE_E) {
@@ -1349,7 +1356,7 @@ __device__ __forceinline__ void Epi::run_role() {
             read_acc(round - 1, v);
             mark(7);
             if (layer == 1) log_ld(48);
-            if (P.prof && layer == 1) log_chunks(92, clock64());
+            if (PPROF(P) && layer == 1) log_chunks(92, clock64());
 #pragma unroll
             for (int i = 0; i < NR; ++i) v[i] = (v[i] + x[i]) + bias_m;
           }
@@ -1385,7 +1392,7 @@ __device__ __forceinline__ void Epi::run_role() {
 // One load + MMA round of the MMA warp over chunks [0, KC): the first NLO
 // chunks have W_lo in TMEM (TS x TS), the rest in smem (TS x SS); one elect
 // per chunk issues its 8 MMAs and the stage commit.
-template <int NLO>
+template <int NLO, bool TR>
 __device__ __forceinline__ void mma_round(const TParams& P, const Smem& sm, uint32_t& fb, int KC, uint32_t tmem,
                                           uint32_t whi0, uint32_t ring0, bool ctr, bool tr, int e) {
   constexpr uint32_t ID64 = idesc_f16(128, 64), ID32 = idesc_f16(128, 32);
@@ -1397,7 +1404,7 @@ __device__ __forceinline__ void mma_round(const TParams& P, const Smem& sm, uint
       mbar_wait(&sm.full[st], (fb >> st) & 1u);
       fb ^= 1u << st;
       if (ctr) sm.dbg[16 + kc] = clock64();
-      if (tr && (kc == 0 || kc == KC - 1)) P.prof[(size_t)(kc ? 28 : 27) * PROF_WIN + (e - PROF_S0)] = gtimer();
+      if (tr && (kc == 0 || kc == KC - 1)) PPROF(P)[(size_t)(kc ? 28 : 27) * PROF_WIN + (e - PROF_S0)] = gtimer();
       tc_fence_after();
       const uint64_t bd = sdesc_sw128(ring0 + st * CHUNK);
       if (kc < NLO)
@@ -1414,6 +1421,7 @@ __device__ __forceinline__ void mma_round(const TParams& P, const Smem& sm, uint
 #ifndef LB_THREADS
 #define LB_THREADS NTH  // register budget = 65536 / LB_THREADS (A/B knob)
 #endif
+template <bool TR>
 __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constant__ TParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int4 rl = P.roles[blockIdx.x];
@@ -1486,10 +1494,10 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
     const unsigned* mycnt = P.cnt + (size_t)(cidx_act(in_buf, 0) + (lane < KC ? lane : 0)) * CSTRIDE;
     const unsigned my_np = lane < KC ? (unsigned)P.nprod[in_buf][lane] : 0u;
     const CUtensorMap* lmap = &P.ldmap[in_buf];
-    const bool stamp_ip = P.prof && (role == ROLE_I || role == ROLE_P) && (int)blockIdx.x == P.prof_first[role];
-    const bool ctr = P.prof && (role == ROLE_J || role == ROLE_I) && (int)blockIdx.x == P.prof_first[role] && lane == 0;
-    const bool trj = P.prof && role == ROLE_J && (int)blockIdx.x == P.prof_first[role] && lane == 0;
-    unsigned long long* const prof = P.prof;
+    const bool stamp_ip = PPROF(P) && (role == ROLE_I || role == ROLE_P) && (int)blockIdx.x == P.prof_first[role];
+    const bool ctr = PPROF(P) && (role == ROLE_J || role == ROLE_I) && (int)blockIdx.x == P.prof_first[role] && lane == 0;
+    const bool trj = PPROF(P) && role == ROLE_J && (int)blockIdx.x == P.prof_first[role] && lane == 0;
+    unsigned long long* const prof = PPROF(P);
     const uint32_t ring0 = smem_u32(sm.ring);
     uint32_t eb = 0;
     for (int r = 0;; ++r) {
@@ -1534,9 +1542,9 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
   } else if (warp == 1) {
     // ================= MMA issuer (converged warp) =================
     const uint32_t whi0 = smem_u32(sm.whi), ring0 = smem_u32(sm.ring);
-    const bool ctr = P.prof && (role == ROLE_J || role == ROLE_I) && (int)blockIdx.x == P.prof_first[role] && lane == 0;
-    const bool trj = P.prof && role == ROLE_J && (int)blockIdx.x == P.prof_first[role] && lane == 0;
-    const bool stamp_ip = P.prof && (role == ROLE_I || role == ROLE_P) && (int)blockIdx.x == P.prof_first[role] && lane == 0;
+    const bool ctr = PPROF(P) && (role == ROLE_J || role == ROLE_I) && (int)blockIdx.x == P.prof_first[role] && lane == 0;
+    const bool trj = PPROF(P) && role == ROLE_J && (int)blockIdx.x == P.prof_first[role] && lane == 0;
+    const bool stamp_ip = PPROF(P) && (role == ROLE_I || role == ROLE_P) && (int)blockIdx.x == P.prof_first[role] && lane == 0;
     uint32_t fb = 0;  // bit s = fills of stage s consumed so far (mod 2)
     const int nlo = nlo_chunks(KC);
     for (int r = 0;; ++r) {
@@ -1548,22 +1556,22 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
       tc_fence_after();
       const bool tr = trj && e >= PROF_S0 && e < PROF_S0 + PROF_WIN;
       switch (nlo) {  // once per round: no per-chunk branch between the two MMA forms
-        case 0: mma_round<0>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
-        case 1: mma_round<1>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
-        case 2: mma_round<2>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
-        case 3: mma_round<3>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
-        case 4: mma_round<4>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
-        case 5: mma_round<5>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
-        default: mma_round<MAXNLO>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
+        case 0: mma_round<0, TR>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
+        case 1: mma_round<1, TR>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
+        case 2: mma_round<2, TR>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
+        case 3: mma_round<3, TR>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
+        case 4: mma_round<4, TR>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
+        case 5: mma_round<5, TR>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
+        default: mma_round<MAXNLO, TR>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
       }
       mma_commit(&sm.accf[set]);
       if (ctr) sm.dbg[31] = clock64();
-      if (tr) P.prof[(size_t)29 * PROF_WIN + (e - PROF_S0)] = gtimer();
+      if (tr) PPROF(P)[(size_t)29 * PROF_WIN + (e - PROF_S0)] = gtimer();
       if (stamp_ip) reinterpret_cast<volatile unsigned long long*>(sm.misc + 8)[2] = gtimer();
     }
   } else {
     // ================= epilogue + replicated control (128 threads) =================
-    Epi e(P, sm, tmem, tid - 64, warp & 3, role, layer, tile, wsc);
+    Epi<TR> e(P, sm, tmem, tid - 64, warp & 3, role, layer, tile, wsc);
     e.run_role();
   }
   tc_fence_before();

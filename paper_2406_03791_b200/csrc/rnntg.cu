@@ -545,9 +545,10 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   const int KCmax = std::max(Hp, Jp) / 64;
   d->tsmem = ptc::smem_bytes(KCmax);
   if (d->tsmem > (size_t)optin) return fail(RNNTG_E_VALUE, "tensor-core executor: smem budget");
-  CK(cudaFuncSetAttribute(ptc::ptc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(ptc::ptc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(ptc::ptc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ptc::ptc_kernel, ptc::NTH, d->tsmem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ptc::ptc_kernel<false>, ptc::NTH, d->tsmem));
   if (per_sm < 1) return fail(RNNTG_E_VALUE, "tensor-core executor cannot be resident");
   // ---- weight images: W_hi [KC][128 x 64] swizzled, then W_lo [K/2][128] packed pairs ----
   const auto& w = m->host_w;
@@ -735,7 +736,9 @@ cudaError_t launch_tc(rnntg_decoder* d, cudaStream_t st) {
   // previous decode can never validate
   if ((e = cudaMemsetAsync(d->tp.pw, 0, d->tpw_bytes, st)) != cudaSuccess) return e;
   void* args[1] = {&d->tp};
-  return cudaLaunchCooperativeKernel((const void*)ptc::ptc_kernel, dim3(d->tp.G), dim3(ptc::NTH), args,
+  // the traced instantiation only when the event trace is on (RNNTG_PROF)
+  const void* k = d->tp.prof ? (const void*)ptc::ptc_kernel<true> : (const void*)ptc::ptc_kernel<false>;
+  return cudaLaunchCooperativeKernel(k, dim3(d->tp.G), dim3(ptc::NTH), args,
                                      d->tsmem, st);
 }
 
