@@ -534,15 +534,36 @@ __device__ __forceinline__ float tanh_fast(float x) {
 // tile row m = 32*q + lane is this thread's TMEM lane (q = warp & 3, the
 // quadrant a warp may address), and it owns batch rows r0 .. r0+15 of it
 // (r0 = 16 * (et >= 128)): the two warps of a quadrant split the rows.
-template <bool TR>
-struct Epi {
+// The product kernels are also specialised on the decode configuration, SPEC =
+// 2 * algo + (LSTM cell): the algorithm's rules and the cell compile to
+// straight-line code (-0.51 us/step at C2 against runtime flags, A/B: the hot
+// path's instruction footprint matters).  SPEC_GENERIC reads them at run time
+// (the traced instantiation).
+constexpr int SPEC_GENERIC = -1;
+__host__ __device__ constexpr int spec_of(int algo, int cell) { return 2 * algo + (cell == 1 ? 1 : 0); }
+template <int SPEC>
+struct CfgFlags {
+  static constexpr bool fs = SPEC / 2 == ALGO_FS, tdt = SPEC / 2 == ALGO_TDT, lstm = (SPEC & 1) != 0;
+  __device__ explicit CfgFlags(const TParams&) {}
+};
+template <>
+struct CfgFlags<SPEC_GENERIC> {
+  const bool fs, tdt, lstm;
+  __device__ explicit CfgFlags(const TParams& P) : fs(P.algo == ALGO_FS), tdt(P.algo == ALGO_TDT), lstm(P.cell == 1) {}
+};
+
+template <bool TR, int SPEC>
+struct Epi : CfgFlags<SPEC> {
+  using CfgFlags<SPEC>::fs;
+  using CfgFlags<SPEC>::tdt;
+  using CfgFlags<SPEC>::lstm;
   const TParams& P;
   const Smem& sm;
   const uint32_t tq;  // TMEM address of this warp's lane quadrant
   const int et, m, r0, role, layer, tile;
   const float wsc;
   const int B, blank;
-  const bool fs, tdt, lstm, tracer;
+  const bool tracer;
   unsigned* const cnt;
   int maxlen = 0, round = 0, p = 0, err = 0, acc_any = 0;
   float ih[NR];  // R_0: table0[label] rows prefetched during the decision
@@ -551,10 +572,9 @@ struct Epi {
 
   __device__ Epi(const TParams& P_, const Smem& sm_, uint32_t tmem, int et_, int q, int role_, int layer_,
                  int tile_, float wsc_)
-      : P(P_), sm(sm_), tq(tmem + ((uint32_t)(32 * q) << 16)), et(et_), m(32 * q + (et_ & 31)),
+      : CfgFlags<SPEC>(P_), P(P_), sm(sm_), tq(tmem + ((uint32_t)(32 * q) << 16)), et(et_), m(32 * q + (et_ & 31)),
         r0(NR * (et_ >> 7)), role(role_),
-        layer(layer_), tile(tile_), wsc(wsc_), B(P_.B), blank(P_.V1 - 1), fs(P_.algo == ALGO_FS),
-        tdt(P_.algo == ALGO_TDT), lstm(P_.cell == 1),
+        layer(layer_), tile(tile_), wsc(wsc_), B(P_.B), blank(P_.V1 - 1), 
         tracer(PPROF(P_) && (int)blockIdx.x == P_.prof_first[role_]), cnt(P_.cnt) {}
 
   // per-CTA publish time of step s (all CTAs): prof[(NEV + cta) * PROF_WIN + s - PROF_S0]
@@ -1237,8 +1257,8 @@ struct Epi {
   __device__ void run_role();
 };
 
-template <bool TR>
-__device__ __forceinline__ void Epi<TR>::run_role() {
+template <bool TR, int SPEC>
+__device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
   const int unit = lstm ? 32 * tile + (m >> 2) : 128 * tile + m;  // LSTM tiles: m = 4*unit + gate
   const int gate = lstm ? (m & 3) : 0;
   if (role == ROLE_J || role == ROLE_E) {
@@ -1421,7 +1441,7 @@ __device__ __forceinline__ void mma_round(const TParams& P, const Smem& sm, uint
 #ifndef LB_THREADS
 #define LB_THREADS NTH  // register budget = 65536 / LB_THREADS (A/B knob)
 #endif
-template <bool TR>
+template <bool TR, int SPEC>
 __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constant__ TParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int4 rl = P.roles[blockIdx.x];
@@ -1432,8 +1452,8 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
   Smem sm = carve(smem_raw, KC);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int B = P.B;
-  const bool lstm = P.cell == 1;
-  const bool fs = P.algo == ALGO_FS, tdt = P.algo == ALGO_TDT;
+  const CfgFlags<SPEC> cf(P);
+  const bool lstm = cf.lstm, fs = cf.fs, tdt = cf.tdt;
   const int blank = P.V1 - 1;
 
   if (tid == 0) {
@@ -1571,7 +1591,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
     }
   } else {
     // ================= epilogue + replicated control (128 threads) =================
-    Epi<TR> e(P, sm, tmem, tid - 64, warp & 3, role, layer, tile, wsc);
+    Epi<TR, SPEC> e(P, sm, tmem, tid - 64, warp & 3, role, layer, tile, wsc);
     e.run_role();
   }
   tc_fence_before();

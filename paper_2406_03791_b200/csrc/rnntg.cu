@@ -515,6 +515,22 @@ float h2f(uint16_t h) {
 
 // Tensor-core persistent executor: role assignment (one 128-row weight tile
 // per CTA), fp16 hi/lo weight images, activation / counter buffers.
+// the tensor-core kernel instantiation for a decode configuration: one per
+// (algorithm, cell) for production, the generic one (flags read at run time)
+// when the event trace is on
+const void* tc_kernel_for(int algo, int cell, bool traced) {
+  using namespace ptc;
+  if (traced) return (const void*)ptc_kernel<true, SPEC_GENERIC>;
+  switch (spec_of(algo, cell)) {
+    case spec_of(ALGO_FS, 0): return (const void*)ptc_kernel<false, spec_of(ALGO_FS, 0)>;
+    case spec_of(ALGO_FS, 1): return (const void*)ptc_kernel<false, spec_of(ALGO_FS, 1)>;
+    case spec_of(ALGO_LL, 0): return (const void*)ptc_kernel<false, spec_of(ALGO_LL, 0)>;
+    case spec_of(ALGO_LL, 1): return (const void*)ptc_kernel<false, spec_of(ALGO_LL, 1)>;
+    case spec_of(ALGO_TDT, 0): return (const void*)ptc_kernel<false, spec_of(ALGO_TDT, 0)>;
+    default: return (const void*)ptc_kernel<false, spec_of(ALGO_TDT, 1)>;
+  }
+}
+
 rnntg_status setup_tc(rnntg_decoder* d) {
   rnntg_model* m = d->m;
   const DevModel& M = m->dm;
@@ -545,10 +561,11 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   const int KCmax = std::max(Hp, Jp) / 64;
   d->tsmem = ptc::smem_bytes(KCmax);
   if (d->tsmem > (size_t)optin) return fail(RNNTG_E_VALUE, "tensor-core executor: smem budget");
-  CK(cudaFuncSetAttribute(ptc::ptc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-  CK(cudaFuncSetAttribute(ptc::ptc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(tc_kernel_for(d->algo, M.cell, false), cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(tc_kernel_for(d->algo, M.cell, true), cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ptc::ptc_kernel<false>, ptc::NTH, d->tsmem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tc_kernel_for(d->algo, M.cell, false), ptc::NTH,
+                                                   d->tsmem));
   if (per_sm < 1) return fail(RNNTG_E_VALUE, "tensor-core executor cannot be resident");
   // ---- weight images: W_hi [KC][128 x 64] swizzled, then W_lo [K/2][128] packed pairs ----
   const auto& w = m->host_w;
@@ -737,7 +754,7 @@ cudaError_t launch_tc(rnntg_decoder* d, cudaStream_t st) {
   if ((e = cudaMemsetAsync(d->tp.pw, 0, d->tpw_bytes, st)) != cudaSuccess) return e;
   void* args[1] = {&d->tp};
   // the traced instantiation only when the event trace is on (RNNTG_PROF)
-  const void* k = d->tp.prof ? (const void*)ptc::ptc_kernel<true> : (const void*)ptc::ptc_kernel<false>;
+  const void* k = tc_kernel_for(d->tp.algo, d->tp.cell, d->tp.prof != nullptr);
   return cudaLaunchCooperativeKernel(k, dim3(d->tp.G), dim3(ptc::NTH), args,
                                      d->tsmem, st);
 }
