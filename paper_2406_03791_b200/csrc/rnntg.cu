@@ -26,6 +26,11 @@
 
 using namespace rnntg;
 
+namespace rnntg {
+// ptc_kernels.cu (its own translation unit: ptxas -O1, see the Makefile)
+const void* tc_kernel_for(int algo, int cell, bool traced);
+}  // namespace rnntg
+
 namespace {
 
 thread_local std::string g_err;
@@ -515,22 +520,6 @@ float h2f(uint16_t h) {
 
 // Tensor-core persistent executor: role assignment (one 128-row weight tile
 // per CTA), fp16 hi/lo weight images, activation / counter buffers.
-// the tensor-core kernel instantiation for a decode configuration: one per
-// (algorithm, cell) for production, the generic one (flags read at run time)
-// when the event trace is on
-const void* tc_kernel_for(int algo, int cell, bool traced) {
-  using namespace ptc;
-  if (traced) return (const void*)ptc_kernel<true, SPEC_GENERIC>;
-  switch (spec_of(algo, cell)) {
-    case spec_of(ALGO_FS, 0): return (const void*)ptc_kernel<false, spec_of(ALGO_FS, 0)>;
-    case spec_of(ALGO_FS, 1): return (const void*)ptc_kernel<false, spec_of(ALGO_FS, 1)>;
-    case spec_of(ALGO_LL, 0): return (const void*)ptc_kernel<false, spec_of(ALGO_LL, 0)>;
-    case spec_of(ALGO_LL, 1): return (const void*)ptc_kernel<false, spec_of(ALGO_LL, 1)>;
-    case spec_of(ALGO_TDT, 0): return (const void*)ptc_kernel<false, spec_of(ALGO_TDT, 0)>;
-    default: return (const void*)ptc_kernel<false, spec_of(ALGO_TDT, 1)>;
-  }
-}
-
 rnntg_status setup_tc(rnntg_decoder* d) {
   rnntg_model* m = d->m;
   const DevModel& M = m->dm;
