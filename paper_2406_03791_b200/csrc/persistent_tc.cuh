@@ -1186,7 +1186,6 @@ struct Epi : CfgFlags<SPEC> {
     // + release (64 separate 64-byte bulk stores cost more, scripts/mb_pub.cu)
     unsigned char* ch = P.act[l] + ((size_t)(pe & 1) * P.act_kc[l] + (u >> 6)) * CHUNK;
 #endif
-#pragma unroll
     // loads, arithmetic and stores in separate passes: the compiler cannot move
     // a later row's xw loads above an earlier row's st16 stores (both shared
     // memory), which serialised the NR / 4 per-row dependency chains
@@ -1451,10 +1450,8 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
   const int KC = role == ROLE_E ? 0 : P.act_kc[in_buf];
   Smem sm = carve(smem_raw, KC);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int B = P.B;
   const CfgFlags<SPEC> cf(P);
   const bool lstm = cf.lstm, fs = cf.fs, tdt = cf.tdt;
-  const int blank = P.V1 - 1;
 
   if (tid == 0) {
     for (int i = 0; i < NSTAGE; ++i) {
