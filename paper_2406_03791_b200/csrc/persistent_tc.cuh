@@ -67,7 +67,7 @@ constexpr int MAXKC = MAXKP / 64;
 constexpr int TRUNK = MAXL;      // activation buffer ids: h_0..h_{L-1}, trunk
 constexpr int MAXBUF = MAXL + 1;
 #ifndef NSLOT_CFG
-#define NSLOT_CFG 16  // A/B (current code): 16 slots -0.035 us/step vs 8; 4 and 32 slower
+#define NSLOT_CFG 8  // A/B at -O1: 8 slots -0.22 (C2) / -0.09 (C3) / -0.08 (C4) us/step vs 16
 #endif
 constexpr int NSLOT = NSLOT_CFG;  // joint-partial ring depth (ack checked every NSLOT/2 steps)
 constexpr int CSTRIDE = 32;      // u32 words between counters (one 128-byte line each)
