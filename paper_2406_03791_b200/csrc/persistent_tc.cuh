@@ -59,7 +59,10 @@ static_assert(NEPI == 256 || NEPI == 512, "epilogue: 8 or 16 warps");
 #define NSTAGE_CFG 4
 #endif
 constexpr int NSTAGE = NSTAGE_CFG;
-constexpr int MAXNJ = 16;       // joint tiles (V+1+D <= 2048)
+#ifndef MAXNJ_CFG
+#define MAXNJ_CFG 16
+#endif
+constexpr int MAXNJ = MAXNJ_CFG;       // joint tiles (V+1+D <= 2048)
 constexpr int CHUNK = 8192;      // [64 rows][64 k] fp16, SWIZZLE_128B
 constexpr int MAXB = 32;         // rows per decoder on this executor
 constexpr int MAXKP = 640;       // K <= 640: W_lo (K/2 TMEM columns) + 2 x 96 accumulator columns
