@@ -156,13 +156,15 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def cpu_reference_sample(cfg, seconds_target, threads=None):
+def cpu_reference_sample(cfg, seconds_target, threads=None, blank_bias=0.0):
     """The reference's own decoders (oracle/_ref: rnnt-sim compiled from its
     sources + the LstmModel extension) on a bounded sample of the workload."""
     from oracle import oracle as O
     algo, B, T, ms, durs, L, H, J, V, F, scaling = cfg
     d = O.Dims(V, H, H, J, F, durs, O.CELL_LSTM, L)
     p = O.init_params(1, d)
+    if blank_bias:
+        p[-2 if durs else -1][:, V] += np.float32(blank_bias)
     m = O.RefModel(d, p)
     nproc = os.cpu_count() or 1
     threads = threads or min(nproc, B)
@@ -183,28 +185,78 @@ def cpu_reference_sample(cfg, seconds_target, threads=None):
             "seconds": secs}
 
 
+def prefix_check(cfg, name, hyps, Ts):
+    """Reference-arm hypotheses (utterances decoded over their first Ts frames)
+    against the full-size fixture: every decoder here is causal in t, so the
+    truncated decode equals the full decode's emissions at frames < Ts."""
+    from tests.parity import FullsizeFixture
+    algo, B, T, ms, durs, L, H, J, V, F, scaling = cfg
+    path = os.path.join(ROOT, "tests", "golden", f"fullsize_{name}.npz")
+    if not os.path.exists(path):
+        return {"checked": False, "why": "no fixture"}
+    fx = FullsizeFixture(name)
+    if (fx.meta["B"], fx.meta["T"], fx.meta["ms"], fx.meta["algo"]) != (B, T, ms, algo):
+        return {"checked": False, "why": "fixture is for another configuration"}
+    bad = []
+    for b, h in enumerate(hyps):
+        t, f, sc, _ = fx.utt(b)
+        k = int(np.sum(f < Ts))
+        if (list(h.tokens) != t[:k].tolist() or list(h.frames) != f[:k].tolist()
+                or np.asarray(h.scores, np.float32).tobytes() != sc[:k].astype(np.float32).tobytes()):
+            bad.append(b)
+    return {"checked": True, "fixture": f"tests/golden/fullsize_{name}.npz", "utterances": len(hyps),
+            "frames_each": Ts, "bitwise_equal": len(hyps) - len(bad), "mismatched": bad}
+
+
 def run_reference_arm(args, cfg, rank, world):
+    """--impl reference: the reference's own batched decoders (oracle/_ref =
+    rnnt-sim compiled from /root/reference sources + the LstmModel extension;
+    greedy_decode_sync_free / label_looping_decode / tdt_label_looping_decode)
+    on the box's host cores, one utterance per thread.  Each step decodes the
+    same bounded sample of the workload -- the first min(B, cores) utterances
+    of the config over their first Ts frames, Ts sized so the whole
+    --warmup + --steps run takes about two minutes -- and is timed on the
+    wall clock; the hypotheses are checked bit for bit against the prefix of
+    the committed full-size fixture."""
     if rank != 0:
         return
+    from oracle import oracle as O
     algo, B, T, ms, durs, L, H, J, V, F, scaling = cfg
-    secs_per_step = max(2.0, min(20.0, 150.0 / max(args.steps + args.warmup, 1)))
-    vals = []
-    base = None
+    d = O.Dims(V, H, H, J, F, durs, O.CELL_LSTM, L)
+    p = O.init_params(1, d)
+    if args.blank_bias:
+        p[-2 if durs else -1][:, V] += np.float32(args.blank_bias)
+    m = O.RefModel(d, p)
+    nproc = os.cpu_count() or 1
+    threads = min(nproc, B)
+    ref_algo = {"fs": "sync_free", "ll": "label_loop", "tdt": "tdt"}[algo]
+    x, _ = make_inputs(cfg, 0, threads)
+    secs_per_step = max(1.0, min(20.0, 120.0 / max(args.steps + args.warmup, 1)))
+    _, s2 = m.decode(ref_algo, np.ascontiguousarray(x[:, :2]), np.full(threads, 2, np.int32), ms, threads)
+    Ts = int(max(2, min(T, 2 * secs_per_step / max(s2, 1e-3))))
+    xs = np.ascontiguousarray(x[:, :Ts])
+    ls = np.full(threads, Ts, np.int32)
+    secs = []
+    hyps = None
     for i in range(args.warmup + args.steps):
-        r = cpu_reference_sample(cfg, secs_per_step)
+        hyps, sec = m.decode(ref_algo, xs, ls, ms, threads)
         if i >= args.warmup:
-            vals.append(r["value"])
-        base = r
-    v = float(np.mean(vals)) if vals else base["value"]
+            secs.append(sec)
+    sec = float(np.mean(secs)) if secs else sec
+    v = threads * Ts / sec
+    chk = prefix_check(cfg, args.config + ("b" if args.blank_bias else ""), hyps, Ts)
+    sample = (f"{threads} of the {B} utterances x their first {Ts} of {T} frames per step, "
+              f"{ALGO_NAME[algo]} (ms={ms}); reference rnnt-sim decoders ({ref_algo}) + LstmModel, "
+              f"one utterance per thread, {threads} threads of {nproc}")
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "frames/s",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": 1000.0 * B * T / v, "higher_is_better": True,
+           "ms_per_step": 1000.0 * sec, "higher_is_better": True,
            "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-           "config": config_json(args, cfg),
-           "cpu_baseline": {k: base[k] for k in ("kind", "cores", "sample")} | {"value": v,
-                                                                                "unit": "frames/s"},
-           "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0,
-                   "d2h_bytes_per_step": 0}}
+           "config": config_json(args, cfg) | {"parallelism": f"utterance-sharded x{world}"},
+           "cpu_baseline": {"kind": "reference", "cores": threads, "sample": sample, "value": v,
+                            "unit": "frames/s"},
+           "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "parity": chk}
     print(json.dumps(out), flush=True)
 
 
@@ -367,6 +419,64 @@ def measure_idle(L_, dh, decode_ms=None):
             "note": "CUPTI kernel records; a persistent kernel's barrier spin counts as busy"}
 
 
+def read_hyps(L_, dh, Bl):
+    """rnntg_read of the last decode -> per-utterance (tokens, frames, scores, durations)."""
+    from types import SimpleNamespace
+    from paper_2406_03791_b200._lib import check
+    cap = L_.rnntg_decoder_capacity(dh)
+    cnt = np.zeros(Bl, np.int32)
+    arr = [np.zeros((Bl, cap), np.int32) for _ in range(2)] + [np.zeros((Bl, cap), np.float32),
+                                                             np.zeros((Bl, cap), np.int32)]
+    check(L_.rnntg_read(dh, *[C.c_void_p(a.ctypes.data) for a in [cnt] + arr], cap))
+    return [SimpleNamespace(tokens=arr[0][b, :cnt[b]], frames=arr[1][b, :cnt[b]], scores=arr[2][b, :cnt[b]],
+                            durations=arr[3][b, :cnt[b]]) for b in range(Bl)]
+
+
+def check_parity(args, cfg, hyps, b0, b1, rank, world, dist):
+    """The timed decode's hypotheses against the committed full-size fixture of
+    the reference's scalar oracle (tests/golden/fullsize_*.npz, same inputs):
+    tokens / frames / durations exact, scores within 1e-4, near-ties counted."""
+    algo, B, T, ms, durs, L, H, J, V, F, scaling = cfg
+    name = args.config + ("b" if args.blank_bias else "")
+    res = {"fixture": f"tests/golden/fullsize_{name}.npz", "checked": False}
+    path = os.path.join(ROOT, res["fixture"])
+    try:
+        from tests.parity import FullsizeFixture, compare_fullsize
+        fx = FullsizeFixture(name) if os.path.exists(path) else None
+        if fx is None:
+            res["why"] = "no fixture"
+        elif (fx.meta["B"], fx.meta["T"], fx.meta["ms"], fx.meta["algo"]) != (B, T, ms, algo) or \
+                abs(fx.meta["blank_bias"] - args.blank_bias) > 1e-12:
+            res["why"] = "fixture is for another configuration"
+        elif b1 > fx.meta["B"]:
+            res["why"] = f"rows {b0}..{b1 - 1} are outside the fixture (weak scaling: rank > 0)"
+        else:
+            sub = FullsizeFixture.__new__(FullsizeFixture)
+            sub.__dict__.update(fx.__dict__)
+            sub.counts = fx.counts[b0:b1]
+            sub.off = fx.off[b0:b1 + 1]
+            sub.wins = {(b - b0, i): m for (b, i), m in fx.wins.items() if b0 <= b < b1}
+            rep = compare_fullsize(hyps, sub, name)
+            res.update(checked=True, utterances=rep.utterances, exact=rep.exact,
+                       permitted_near_ties=rep.permitted, failures=len(rep.failures),
+                       first_failures=rep.failures[:3], max_score_rel=rep.max_score_rel)
+    except Exception as e:  # reported, never silently passed
+        res["error"] = repr(e)
+    if dist:
+        allr = [None] * world
+        dist.all_gather_object(allr, res)
+        chk = [r for r in allr if r.get("checked")]
+        res = {"fixture": res["fixture"], "checked": bool(chk), "ranks_checked": len(chk),
+               "utterances": sum(r["utterances"] for r in chk), "exact": sum(r["exact"] for r in chk),
+               "permitted_near_ties": sum(r["permitted_near_ties"] for r in chk),
+               "failures": sum(r["failures"] for r in chk),
+               "max_score_rel": max([r["max_score_rel"] for r in chk], default=None),
+               "per_rank": allr}
+    if res.get("failures"):
+        print(f"bench.py: PARITY FAILURE {res}", file=sys.stderr)
+    return res
+
+
 def config_json(args, cfg):
     algo, B, T, ms, durs, L, H, J, V, F, scaling = cfg
     return {"workload": f"{args.config}: Parakeet-1.1B-shaped {ALGO_NAME[algo]} decode "
@@ -379,9 +489,25 @@ def config_json(args, cfg):
             "blank_bias": args.blank_bias}
 
 
+def spawn_ranks(args):
+    """`bench.py --gpus N` without a launcher: re-run this script under
+    torch.distributed.run with N ranks on 127.0.0.1 (one process per GPU)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(spawn_ranks(args))
     rank, world, local = dist_env()
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference_arm(args, cfg, rank, world)
@@ -398,14 +524,12 @@ def main():
         local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dist = None
-    coll_dev = "cuda"
+    coll_dev = "cpu"
     if world > 1:
+        # no NCCL: shards are independent; gloo carries only the
+        # barriers and the max-over-ranks of the device-timed region
         import torch.distributed as dist
-        if share:
-            dist.init_process_group("gloo")
-            coll_dev = "cpu"
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("gloo")
     b0, b1 = shard(cfg, rank, world)
     Bl = b1 - b0
     dims = ModelDims(V, H, H, J, F, durs, "lstm", L)
@@ -469,6 +593,7 @@ def main():
         launches_per_step = 2
     else:
         launches_per_step = 2 + st.pred_steps * (L + 1) + st.joint_evals + (st.outer_iters if fs else 0)
+    hyps_dev = read_hyps(L_, dh, Bl)  # the timed decodes' hypotheses (device-resident inputs)
     roofline, clk = roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent)
 
     # ---- e2e through the C ABI with host buffers ----
@@ -537,9 +662,22 @@ def main():
                "d2h_bytes_per_step": int(4 * Bl + 4 * 4 * Bl * cap),
                "mode": "serial" if serial else
                "pipelined: step i+1's pinned H2D on a copy stream overlaps step i's decode (first copy not overlapped)"}
-        # verify the e2e decode agrees with the device-input decode
-        # (same inputs -> identical counts)
+        # the pipelined / serial e2e path must decode exactly what the
+        # device-input decode did (same inputs): counts, tokens, frames, scores
+        cnt_h = outs[0].numpy()
+        tok_h, frm_h, durs_h = outs[1].numpy(), outs[2].numpy(), outs[4].numpy()
+        sc_h = outs[3].numpy().view(np.float32)
+        bad = [b for b, h in enumerate(hyps_dev)
+               if cnt_h[b] != len(h.tokens) or not np.array_equal(tok_h[b, :cnt_h[b]], h.tokens)
+               or not np.array_equal(frm_h[b, :cnt_h[b]], h.frames)
+               or sc_h[b, :cnt_h[b]].tobytes() != np.asarray(h.scores, np.float32).tobytes()
+               or not np.array_equal(durs_h[b, :cnt_h[b]], h.durations)]
+        e2e["matches_device_decode"] = not bad
+        if bad:
+            print(f"bench.py: e2e hypotheses differ from the device-input decode on rows {bad[:8]}",
+                  file=sys.stderr)
 
+    parity = check_parity(args, cfg, hyps_dev, b0, b1, rank, world, dist)
     idle = measure_idle(L_, dh, ms_per_step)
     alt = None
     if not args.no_compare:
@@ -550,7 +688,7 @@ def main():
         try:
             from oracle import oracle as O
             if O.ref_available():
-                cpu = cpu_reference_sample(cfg, args.cpu_seconds)
+                cpu = cpu_reference_sample(cfg, args.cpu_seconds, blank_bias=args.blank_bias)
                 cpu.pop("seconds", None)
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "error": str(e)}
@@ -560,7 +698,9 @@ def main():
         out = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+            "dtype": "f32 (tensor exec: each fp32 product as 3 fp16 hi/lo tcgen05 products, fp32 accumulate)"
+                     if args.exec == "tensor" else "f32",
             "data": "synthetic (random-init weights, random encoder outputs)",
             "config": config_json(args, cfg) | {"parallelism": f"utterance-sharded x{world}"},
             "us_per_step": 1000.0 * ms_per_step / max(inner, 1),
@@ -570,6 +710,7 @@ def main():
             "gpu_idle_pct": idle["idle_pct"] if idle else None, "gpu_idle": idle,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches_per_step * args.steps),
+            "parity": parity,
             "clocks": clk, "step_ms": step_ms, "alt_exec": alt,
         }
         print(json.dumps(out), flush=True)

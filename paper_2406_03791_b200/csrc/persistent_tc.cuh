@@ -118,9 +118,6 @@ __host__ __device__ constexpr int nlo_chunks(int KC) {
              ? ((512 - WLO_COL) / 32 - KC < KC ? (512 - WLO_COL) / 32 - KC : KC)
              : NLO_MAX;
 }
-#ifndef ACK_RELAXED
-#define ACK_RELAXED 1
-#endif
 #ifndef SPIN_ONE
 #define SPIN_ONE 1
 #endif
@@ -176,6 +173,7 @@ struct TParams {
                               // one word per 128-byte line (PW_STRIDE): every CTA polls them
   float2* ps;                 // [NSLOT][NJ][32] vocab (row max, sumexp) for the emitted score
   unsigned* cnt;              // [NCOUNTERS * CSTRIDE]
+  unsigned* ack;              // [G] per-CTA ack words: steps whose argmax words / partials the CTA consumed
   int* tokens;
   int* frames;
   float* scores;
@@ -312,15 +310,49 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// Spin until *p >= target with relaxed (L1-bypassing) loads.  An acquire load
-// compiles to LDG.STRONG.GPU + CCTL.IVALL: polling with it invalidates the
-// SM's L1 continuously, and even one extra acquire costs a full L2 round trip
-// on the critical path.  Every reader of published data reads through L2
-// (bulk copies, ld.global.cg) after observing the counter that the producer
-// bumped with a release, so the relaxed observation suffices in practice.
-__device__ __forceinline__ void spin_geq(const unsigned* p, unsigned target) {
-  while (ld_relaxed(p) < target) {
+// Cross-CTA hand-off protocol (PTX memory model, gpu scope).
+//  producer: data writes (generic stores, or TMA bulk stores completed with
+//            cp.async.bulk.wait_group 0 and ordered into the generic proxy by
+//            fence.proxy.async.global) -> release pattern (fence.acq_rel.gpu or
+//            red.release.gpu) -> counter add;
+//  consumer: relaxed spin on the counter (an acquire LOAD compiles to
+//            LDG.STRONG.GPU + CCTL.IVALL and polling with it invalidated the
+//            SM's L1 continuously: 60 us/step) -> ONE fence.acq_rel.gpu after the
+//            spin exits (strong read + fence = acquire pattern, which
+//            synchronizes-with the producer's release) -> fence.proxy.async.global
+//            before TMA loads of the data.
+// MM_PROD / MM_CONS select the producer / consumer halves (A/B):
+//   MM_PROD 0 none (round 1: relied on L2 behaviour outside the model),
+//           1 fence.proxy.async.global + fence.acq_rel.gpu + relaxed adds,
+//           2 fence.proxy.async.global + red.release.gpu;
+//   MM_CONS 0 none, 1 relaxed spin + fence.acq_rel.gpu,
+//           2 acquire polls, 3 relaxed spin + one ld.acquire re-read.
+#ifndef MM_PROD
+#define MM_PROD 1
+#endif
+#ifndef MM_CONS
+#define MM_CONS 3
+#endif
+// one counter poll (the consumer's strong read)
+__device__ __forceinline__ unsigned ld_poll_cnt(const unsigned* p) {
+  unsigned v;
+  if (MM_CONS == 2) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  else asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// after a successful relaxed poll of p
+__device__ __forceinline__ void acquire_after(const unsigned* p) {
+  if (MM_CONS == 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  if (MM_CONS == 3) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    (void)v;
   }
+}
+__device__ __forceinline__ void spin_geq(const unsigned* p, unsigned target) {
+  while (ld_poll_cnt(p) < target) {
+  }
+  acquire_after(p);
 }
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -421,6 +453,23 @@ __device__ __forceinline__ void bulk_commit_wait_all() {
 }
 __device__ __forceinline__ void red_relaxed_add(unsigned* p, unsigned v) {
   asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// after bulk_commit_wait_all(): the completed bulk-store writes, ordered into
+// the generic proxy, then released at gpu scope before the counter adds
+__device__ __forceinline__ void release_after_bulk() {
+  if (MM_PROD == 1 || MM_PROD == 2) asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (MM_PROD == 1 || MM_PROD == 3) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+#ifndef PUB_ET
+#define PUB_ET 0  // epilogue thread that issues the activation bulk stores + publish
+#endif
+// the counter add that publishes (after release_after_bulk)
+__device__ __forceinline__ void publish_add(unsigned* p) {
+  if (MM_PROD == 2) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+  else asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // byte offset of (row r, k) inside a [rows x 64] fp16 K-major SWIZZLE_128B chunk
@@ -693,7 +742,7 @@ struct Epi : CfgFlags<SPEC> {
                                                  int buf, int kc0, int par) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     epi_sync();
-    if (et == 0) {
+    if (et == PUB_ET) {
 #if TMA_ACT
       for (int c = 0; c < n; ++c) tma_st2(&P.stmap[buf], 64 * (kc0 + c), 64 * par, stage + (size_t)c * CHUNK);
       (void)gdst;
@@ -701,7 +750,8 @@ struct Epi : CfgFlags<SPEC> {
       for (int c = 0; c < n; ++c) bulk_s2g(gdst + (size_t)c * CHUNK, stage + (size_t)c * CHUNK, CHUNK);
 #endif
       bulk_commit_wait_all();
-      for (int c = 0; c < n; ++c) red_relaxed_add(cnt + (size_t)(ci + c) * CSTRIDE, 1);
+      release_after_bulk();
+      for (int c = 0; c < n; ++c) publish_add(cnt + (size_t)(ci + c) * CSTRIDE);
     }
   }
 
@@ -733,9 +783,21 @@ struct Epi : CfgFlags<SPEC> {
     mark(1);
     mark(16);
     const long long tacc = PPROF(P) ? clock64() : 0;
-    // slot reuse: every CTA has finished decide(s - NSLOT); checked once per half window
-    if (s >= NSLOT / 2 && s % (NSLOT / 2) == 0)
-      wait_counter(cidx_ack(), (unsigned)P.G * (unsigned)(s - NSLOT / 2 + 1));
+    // slot reuse: steps s .. s + NSLOT/2 - 1 overwrite the slots of steps
+    // s - NSLOT .. s - NSLOT/2 - 1, so EVERY CTA (not their sum: an off-path
+    // role such as the emitter may lag) must have acked step s - NSLOT/2.
+    // Checked once per half window on the per-CTA ack words (min over CTAs).
+    if (s >= NSLOT / 2 && s % (NSLOT / 2) == 0) {
+      if (et < 32) {
+        const unsigned target = (unsigned)(s - NSLOT / 2 + 1);
+        for (;;) {
+          unsigned mn = 0xffffffffu;
+          for (int c = et; c < P.G; c += 32) mn = min(mn, ld_relaxed(P.ack + c));
+          if (__reduce_min_sync(0xffffffffu, mn) >= target) break;
+        }
+      }
+      epi_sync();
+    }
     const int slot = (int)(s % NSLOT);
     const unsigned tg = step_tag(s);
     const int V1 = P.V1, VD = P.V1 + P.D;
@@ -1150,11 +1212,9 @@ struct Epi : CfgFlags<SPEC> {
       // this CTA is done with step s's words: ack (slot reuse, joint_round).
       // The ack follows reads only (their values are consumed), so it needs
       // no release; ~75 MEMBAR.GPU per step slowed every hand-off.
-#if ACK_RELAXED
-      if (et == 0) red_relaxed_add(cnt + (size_t)cidx_ack() * CSTRIDE, 1);
-#else
-      if (et == 0) red_release_add(cnt + (size_t)cidx_ack() * CSTRIDE, 1);
-#endif
+      // (per-CTA word; the reads it covers were consumed before the barrier
+      // that precedes it, so it needs no release)
+      if (et == 0) st_relaxed_u32(P.ack + blockIdx.x, (unsigned)(s + 1));
       ++s;
       if (et < 32) sm.flag[et] &= ~2;
       epi_sync();
@@ -1228,10 +1288,11 @@ struct Epi : CfgFlags<SPEC> {
 #if TMA_ACT
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     epi_sync();
-    if (et == 0) {
+    if (et == PUB_ET) {
       tma_st2(&P.stmap[l], 32 * tile, 64 * (pe & 1), st16);
       bulk_commit_wait_all();
-      red_relaxed_add(cnt + (size_t)cidx_act(l, (32 * tile) >> 6) * CSTRIDE, 1);
+      release_after_bulk();
+      publish_add(cnt + (size_t)cidx_act(l, (32 * tile) >> 6) * CSTRIDE);
     }
 #else
     bump(cidx_act(l, (32 * tile) >> 6));
@@ -1531,12 +1592,19 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
         // one counter per lane, all in flight in one instruction
         const bool need = lane >= next && lane < KC;
         unsigned v = 0u;
-        if (need) v = ld_relaxed(mycnt);
+        if (need) v = ld_poll_cnt(mycnt);
         const unsigned ok = __ballot_sync(0xffffffffu, lane < next || (need && v >= target));
         const int ready = __ffs(~ok) - 1;  // chunks [0, ready) are published
         if (ctr) ++npoll;
         if (ready == next) continue;
         if (ctr && next == 0) sm.dbg[10] = npoll;
+        // relaxed counter reads + a fence / acquire re-read (warp-synchronised:
+        // any lane may issue the loads below): the acquire pattern
+        if (MM_CONS == 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (MM_CONS == 3) {
+          if (lane >= next && lane < ready) acquire_after(mycnt);
+          __syncwarp();
+        }
         fence_proxy_global();
 #pragma unroll
         for (int kc = 0; kc < MAXKC; ++kc) {

@@ -716,9 +716,11 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   d->tpw_bytes = (size_t)ptc::NSLOT * 2 * NJ * 32 * ptc::PW_STRIDE * sizeof(unsigned long long);
   CK(d->mem.alloc(&tp.pw, (size_t)ptc::NSLOT * 2 * NJ * 32 * ptc::PW_STRIDE));
   CK(d->mem.alloc(&tp.ps, (size_t)ptc::NSLOT * NJ * 32));
-  d->tcnt_bytes = (size_t)ptc::NCOUNTERS * ptc::CSTRIDE * sizeof(unsigned);
-  CK(d->mem.alloc(&d->tcnt, (size_t)ptc::NCOUNTERS * ptc::CSTRIDE));
+  // counters, then the G per-CTA ack words: zeroed together before every launch
+  d->tcnt_bytes = ((size_t)ptc::NCOUNTERS * ptc::CSTRIDE + (size_t)G) * sizeof(unsigned);
+  CK(d->mem.alloc(&d->tcnt, (size_t)ptc::NCOUNTERS * ptc::CSTRIDE + (size_t)G));
   tp.cnt = d->tcnt;
+  tp.ack = d->tcnt + (size_t)ptc::NCOUNTERS * ptc::CSTRIDE;
   tp.decided = d->tcnt + (size_t)(ptc::NCOUNTERS - 1) * ptc::CSTRIDE;  // zeroed with the counters
   tp.tokens = d->st.tokens;
   tp.frames = d->st.frames;

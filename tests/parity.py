@@ -104,3 +104,79 @@ def rel_err(a, b, floor=1e-3):
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
     return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), floor)))
+
+
+# ------------------------------------------------------------ full-size fixtures
+class FullsizeFixture:
+    """tests/golden/fullsize_<name>.npz (tests/golden/make_fullsize.py): the
+    reference's scalar oracle (decoders.cpp:670-755) on bench.py's inputs."""
+
+    def __init__(self, name: str):
+        import json
+        import os
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f"fullsize_{name}.npz")
+        z = np.load(path)
+        self.name = name
+        self.meta = json.loads(bytes(z["meta"]).decode())
+        self.counts = z["counts"].astype(np.int64)
+        self.off = np.concatenate([[0], np.cumsum(self.counts)])
+        self.tokens = z["tokens"].astype(np.int32)
+        self.frames = z["frames"].astype(np.int32)
+        self.scores = z["scores"].view(np.float32)
+        self.totals = z["totals"]
+        self.durations = z["durations"].astype(np.int32) if "durations" in z.files else None
+        self.wins = {}
+        for b, i, m in z["wins"]:
+            self.wins[(int(b), int(i))] = float(m)
+
+    @property
+    def tdt(self):
+        return self.durations is not None
+
+    def utt(self, b):
+        s = slice(self.off[b], self.off[b + 1])
+        return (self.tokens[s], self.frames[s], self.scores[s],
+                self.durations[s] if self.tdt else None)
+
+    def window_margin(self, b, i):
+        """min oracle top-2 margin over the decisions (emission i-1, emission i]
+        (windows >= 1e-3 are not stored: they count as 'not a near tie')."""
+        return self.wins.get((b, i), np.inf)
+
+
+def compare_fullsize(gpu_hyps, fx: FullsizeFixture, tag="") -> ParityReport:
+    """Same rule as compare_utt, against a full-size fixture."""
+    rep = ParityReport()
+    if len(gpu_hyps) != len(fx.counts):
+        rep.failures.append(f"{tag}: batch size {len(gpu_hyps)} != {len(fx.counts)}")
+        return rep
+    for b, g in enumerate(gpu_hyps):
+        rep.utterances += 1
+        rt, rf, rs, rd = fx.utt(b)
+        gt = np.asarray(g.tokens, np.int32)
+        gf = np.asarray(g.frames, np.int32)
+        gd = np.asarray(g.durations, np.int32) if fx.tdt else None
+        same = (len(gt) == len(rt) and np.array_equal(gt, rt) and np.array_equal(gf, rf)
+                and (not fx.tdt or np.array_equal(gd, rd)))
+        if same:
+            rel = _score_rel(g.scores, rs)
+            rep.max_score_rel = max(rep.max_score_rel, rel)
+            if rel > RTOL:
+                rep.failures.append(f"{tag}[{b}]: score rel err {rel:.3g}")
+            else:
+                rep.exact += 1
+            continue
+        n = min(len(gt), len(rt))
+        neq = (gt[:n] != rt[:n]) | (gf[:n] != rf[:n])
+        if fx.tdt:
+            neq |= gd[:n] != rd[:n]
+        i = int(np.argmax(neq)) if neq.any() else n
+        rel = _score_rel(np.asarray(g.scores)[:i], rs[:i])
+        rep.max_score_rel = max(rep.max_score_rel, rel)
+        m = fx.window_margin(b, i)
+        if m < EPS_MARGIN and rel <= RTOL:
+            rep.permitted += 1
+        else:
+            rep.failures.append(f"{tag}[{b}]: diverged at emission {i} of {len(rt)} "
+                                f"(oracle margin {m:.3g}, score rel {rel:.3g})")
+    return rep
