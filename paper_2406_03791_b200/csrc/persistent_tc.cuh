@@ -6,37 +6,46 @@
 // per-chunk dataflow counters in global memory (no grid barriers):
 //
 //   role   weights (swap-AB: M = 128 output rows)   input        output
-//   J      [out_proj || dur_proj] cols 128t..        trunk(s)     per-tile softmax partials
-//   P      pred_proj cols 128t..                     h_{L-1}(p)   gp (registers) -> trunk(s+1)
-//   R_l    W_hh_l gate rows (gate-major, 32 units)   h_l(p)       l=0: hh0(p+1) stays in TMEM,
-//                                                                 layer-0 cell -> h_0(p+1)
-//                                                                 l>0: hh_l(p+1) -> I_l tile
-//   I_l    W_ih_l gate rows, l >= 1                  h_{l-1}(p)   layer-l cell -> h_l(p)
+//   J      [out_proj || dur_proj] cols 128t..        trunk(s)     per-row argmax words, (max, sumexp)
+//   P      pred_proj cols 128t..                     h_{L-1}(p)   gp -> trunk(s+1) = relu(fp + gp)
+//   R_l    W_hh_l gate rows (unit-major, 32 units)   h_l(p)       hh_l(p+1) -> global (for I_l)
+//   I_0    none (the layer-0 cell)                   table0[k] + hh_0(p)      cell -> h_0(p+1)
+//   I_l    W_ih_l gate rows, l >= 1                  h_{l-1}(p)   (+ hh_l) cell -> h_l(p)
+//   E      none                                      J partials   lse, emitted score, hypotheses
+//
+// Row groups.  The batch is split into ngrp <= 8 groups of <= 32 rows; every
+// CTA serves every group, visiting the live groups round-robin one step
+// ("item") at a time.  The groups are independent decodes (model.hpp:89-91)
+// with their own buffers, counters and replicated control, so while one
+// group's step is in flight down the chain (J -> decision -> I_0 -> I_1 -> P),
+// the CTAs that are done with it work on the next group's step.
 //
 // Arithmetic.  Every GEMV is D[128 x 32 rows] = W[128 x K] . A^T on the
 // 5th-gen tensor cores (tcgen05.mma.kind::f16, fp32 accumulate) with an
 // fp16 hi/lo split of BOTH operands: W' = W*2^s = W_hi + W_lo, A = A_hi + A_lo,
 // D = W_hi.[A_hi | A_lo] (one MMA, N = 64) + W_lo.A_hi (N = 32), i.e. all
 // products down to 2^-22 relative (~fp32; the dropped W_lo.A_lo is 2^-22).
-// W_hi is resident in shared memory (SWIZZLE_128B K-major), W_lo resident in
-// TENSOR memory (the MMA's A operand read from TMEM), so a 128 x 640 tile
-// (320 KB of fp16 pairs) stays on chip for the whole decode.
+// W_hi is resident in TENSOR memory (the MMA's A operand read from TMEM),
+// W_lo in shared memory (SWIZZLE_128B K-major) except its first
+// nlo_chunks(KC) chunks, which fit in TMEM too; a 128 x 640 tile (320 KB of
+// fp16 pairs) stays on chip for the whole decode.
 //
 // Activations move as fp16 hi/lo images already in the UMMA canonical
-// layout ([64 rows = 32 hi + 32 lo][64 k] chunks of 8 KB, 128B-swizzled), so
-// a consumer's load is one 1-D bulk copy per chunk.  A chunk is published
-// by its producers with a release add on its counter; consumers poll the
-// counter (acquire) and stream chunks into a 4-stage ring as they appear,
-// overlapping the transfer with the MMAs of earlier chunks.
+// layout ([64 rows = 32 hi + 32 lo][64 k] chunks of 8 KB, 128B-swizzled by
+// the TMA tensor map), so a consumer's load is one tensor copy per chunk.  A
+// chunk is published by its producers (TMA store, wait_group, proxy fence,
+// release) with an add on its counter; consumers poll the counter (relaxed,
+// then one acquire re-read) and stream chunks into a 4-stage ring as they
+// appear, overlapping the transfer with the MMAs of earlier chunks.
 //
 // Control state (labels, cursors, masks, frame counters) is replicated in
-// every CTA: each CTA merges the J tiles' partials for every row and applies
-// the same decision rules (decoders.cpp:261-307, 432-512), so no decision
-// broadcast is needed.  CTA 0 writes the hypotheses.
+// every CTA: each CTA merges the J tiles' argmax words for every row and
+// applies the same decision rules (decoders.cpp:261-307, 432-512), so no
+// decision broadcast is needed.  The emitter CTA writes the hypotheses.
 //
-// Warp roles inside a CTA: warp 0 = bulk-copy producer, warp 1 = MMA issuer
+// Warp roles inside a CTA: warp 0 = TMA producer, warp 1 = MMA issuer
 // (elect.sync inside a converged warp: issuing from a divergent lane costs
-// 3-4x, scripts/mb_tc.cu), warps 2-5 = epilogue + control.
+// 3-4x, scripts/mb_tc.cu), warps 2-17 = epilogue + replicated control.
 #pragma once
 
 #include <cuda_fp16.h>
@@ -64,7 +73,9 @@ constexpr int NSTAGE = NSTAGE_CFG;
 #endif
 constexpr int MAXNJ = MAXNJ_CFG;       // joint tiles (V+1+D <= 2048)
 constexpr int CHUNK = 8192;      // [64 rows][64 k] fp16, SWIZZLE_128B
-constexpr int MAXB = 32;         // rows per decoder on this executor
+constexpr int MAXB = 32;         // rows per group (one MMA N slice: 32 hi + 32 lo activation rows)
+constexpr int MAXG = 8;          // row groups per kernel: batch <= 256
+constexpr int NSV = 8;           // per-thread state floats saved per group (P: gp[NR]; cells: c, h)
 constexpr int MAXKP = 640;       // K <= 640: W_lo (K/2 TMEM columns) + 2 x 96 accumulator columns
 constexpr int MAXKC = MAXKP / 64;
 constexpr int TRUNK = MAXL;      // activation buffer ids: h_0..h_{L-1}, trunk
@@ -75,22 +86,11 @@ constexpr int MAXBUF = MAXL + 1;
 constexpr int NSLOT = NSLOT_CFG;  // joint-partial ring depth (ack checked every NSLOT/2 steps)
 constexpr int CSTRIDE = 32;      // u32 words between counters (one 128-byte line each)
 
+// I with layer 0 is the layer-0 cell (no weights: table0[label] + hh0 from R_0)
 enum Role { ROLE_J = 0, ROLE_P = 1, ROLE_R = 2, ROLE_I = 3, ROLE_E = 4 };  // E: emitter (no weights)
 constexpr int NROLES = 5;
-#ifndef POLL_NS
-#define POLL_NS 0
-#endif
-#ifndef ECHO_GATE
-#define ECHO_GATE 0  // A/B: gating 55 pollers behind an R_0 echo cost 0.3 us/step
-#endif
 #ifndef TANH_SIG
 #define TANH_SIG 1
-#endif
-#ifndef EARLY_GATHER
-#define EARLY_GATHER 1  // rules warp's table0 loads go out before the rules
-#endif
-#ifndef LAZY_BATCH_NS
-#define LAZY_BATCH_NS 0
 #endif
 // Weight operand layout (per CTA, K = KC chunks of 64):
 //  - W_hi (fp16 pairs) in TMEM from column WLO_COL, chunk kc at WLO_COL + 32 kc;
@@ -118,36 +118,23 @@ __host__ __device__ constexpr int nlo_chunks(int KC) {
              ? ((512 - WLO_COL) / 32 - KC < KC ? (512 - WLO_COL) / 32 - KC : KC)
              : NLO_MAX;
 }
-#ifndef SPIN_ONE
-#define SPIN_ONE 1
-#endif
-#ifndef TMA_ACT
-#define TMA_ACT 1  // activations via 2-D tensor maps (plain row-major in global, swizzled by TMA)
-#endif
 // The event trace (RNNTG_PROF) lives in a separate instantiation of the kernel
 // (template flag TR): compiled into the product kernel, its runtime-gated code
 // cost 0.42 us/step at C2 (~3400 of ~24200 SASS instructions; A/B)
 #define PPROF(X) (TR ? (X).prof : (unsigned long long*)nullptr)
 #define PECHO(X) (TR ? (X).echo : (unsigned long long*)nullptr)
-#ifndef LAZY_NS
-#define LAZY_NS 0  // A/B: 500 ns backoff for non-critical pollers cost 0.09 us/step
-#endif
-#ifndef SLEEP_HINT
-#define SLEEP_HINT 0  // A/B: try_wait suspend hints cost 0.10 us/step
-#endif
-constexpr int PW_STRIDE = 1;   // u64 words per argmax word slot (16 = one line per word: measured no gain)
 
 // counter word indices (times CSTRIDE)
 __host__ __device__ inline int cidx_act(int buf, int kc) { return buf * MAXKC + kc; }
 __host__ __device__ inline int cidx_hh(int l, int t) { return MAXBUF * MAXKC + l * 64 + t; }
 __host__ __device__ inline int cidx_part() { return MAXBUF * MAXKC + MAXL * 64; }
-__host__ __device__ inline int cidx_ack() { return cidx_part() + 1; }
-constexpr int NCOUNTERS = MAXBUF * MAXKC + MAXL * 64 + 5;  // last: ECHO_GATE decided word
+constexpr int NCOUNTERS = MAXBUF * MAXKC + MAXL * 64 + 1;  // per group
 
 struct TParams {
-  // TMA_ACT: activation buffer b is a 2-D fp16 tensor [2 parity x 64 rows][Kp]
-  // (row-major); ldmap: box 64 x 64, SWIZZLE_128B (lands in UMMA canonical
-  // layout); stmap: the producers' box (32 x 64 plain for LSTM tiles, 64 x 64
+  // Activation buffer b is a 2-D fp16 tensor [ngrp x 2 parity x 64 rows][Kp]
+  // (row-major; group g parity e at rows 64 (2g + e) .. +63: 32 hi rows, 32 lo
+  // rows); ldmap: box 64 x 64, SWIZZLE_128B (lands in UMMA canonical layout);
+  // stmap: the producers' box (32 x 64 plain for LSTM tiles, 64 x 64
   // SWIZZLE_128B from canonical staging otherwise)
   CUtensorMap ldmap[MAXBUF];
   CUtensorMap stmap[MAXBUF];
@@ -155,6 +142,8 @@ struct TParams {
   int H, Hp, J, Jp, V1, D;
   int NJ;                     // joint tiles
   int GH, Gg;                 // table0 row stride / gates per unit
+  int ngrp;                   // row groups (<= MAXB rows each), decoded interleaved by every CTA
+  int gr0[MAXG + 1];          // group g = batch rows [gr0[g], gr0[g + 1])
   long long max_iters;
   int durations[MAXD];
   const int4* roles;          // [G] {role, layer, tile, float bits of 2^-s}
@@ -165,15 +154,15 @@ struct TParams {
   const float* table0;        // [V1][GH] gate-interleaved (col = u*Gg + g)
   const float* fp;            // [B*T][Jp] encoder projection (K1)
   const int* out_len;
-  unsigned char* act[MAXBUF];  // [2 parity][KC][CHUNK]
+  unsigned char* act[MAXBUF];  // [ngrp][2 parity][64 rows][Kp] fp16
   int act_kc[MAXBUF];
   int nprod[MAXBUF][MAXKC];   // producers per chunk
-  float* hh[MAXL];            // [2 parity][tiles][32 rows][128] (layers >= 1)
-  unsigned long long* pw;     // [NSLOT][2][NJ][32] argmax words {best f32 | idx << 8 | tag}, vocab / duration,
-                              // one word per 128-byte line (PW_STRIDE): every CTA polls them
-  float2* ps;                 // [NSLOT][NJ][32] vocab (row max, sumexp) for the emitted score
-  unsigned* cnt;              // [NCOUNTERS * CSTRIDE]
-  unsigned* ack;              // [G] per-CTA ack words: steps whose argmax words / partials the CTA consumed
+  float* hh[MAXL];            // [ngrp][2 parity][tiles][32 rows][128]: h_l @ W_hh_l from R_l
+  unsigned long long* pw;     // [ngrp][NSLOT][2][NJ][32] argmax words {best f32 | idx << 8 | tag}, vocab / duration
+  float2* ps;                 // [ngrp][NSLOT][NJ][32] vocab (row max, sumexp) for the emitted score
+  unsigned* cnt;              // [ngrp][NCOUNTERS * CSTRIDE]
+  unsigned* ack;              // [ngrp][G] per-CTA ack words: steps whose argmax words / partials the CTA consumed
+  float* gst;                 // [ngrp][G][NSV][NEPI] per-thread epilogue state of the groups not in flight
   int* tokens;
   int* frames;
   float* scores;
@@ -181,8 +170,6 @@ struct TParams {
   int* counts;
   Ctrl* ctrl;
   unsigned long long* prof;   // optional event trace [NEV][PROF_WIN] (first CTA of each role)
-  unsigned long long* echo;   // optional: R_0 tile 0 echoes the step it decided (round-trip probe)
-  unsigned* decided;          // ECHO_GATE: steps R_0 tile 0 has seen the J words of
   int prof_first[NROLES];     // first CTA index per role (tracing CTAs)
 };
 constexpr int PROF_WIN = 64;  // traced joint steps [PROF_S0, PROF_S0 + PROF_WIN)
@@ -358,22 +345,6 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
-// mbarrier wait with a suspend-time hint: the waiting warp is parked until the
-// phase completes (or the hint expires) instead of re-issuing try_wait, so idle
-// producer / MMA warps do not take issue slots from the epilogue warps.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
-  if (!SLEEP_HINT) {
-    mbar_wait(bar, phase);
-    return;
-  }
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAITS_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-      "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(phase), "r"(1000000u)
-      : "memory");
-}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -491,15 +462,16 @@ struct Smem {
   unsigned char* ring;  // [NSTAGE][CHUNK]
   float* xs;            // [4][32][32] gate exchange / [128][33] joint transpose / partial staging
   float4* red;          // [2][8][32] joint column-group partials
-  int* label;           // [32] replicated row state
-  int* flag;            // bit0 done (FS) / inactive (LL), bit1 accepted this step
-  int* tb;
-  int* ub;
-  int* cnt;
-  int* kdec;
+  int* label;           // [MAXG][32] replicated row state of every group
+  int* flag;            // [MAXG][32] bit0 done (FS) / inactive (LL), bit1 accepted this step
+  int* tb;              // [MAXG][32] label-looping cursor t
+  int* ub;              // [MAXG][32] label-looping symbols at t
+  int* cnt;             // [MAXG][32] emissions
+  int* kdec;            // [32] this step's decision (labels, scores, durations)
   float* vdec;
   int* ddec;
-  int* misc;            // [0..1] round commands, [2] t, [3] sym, [4] shared flag words
+  int* misc;            // [0..1] round epochs, [5] decision outcome, [6..7] round groups, [8..13] trace
+  int* grp;             // [GS_N][MAXG] per-group scalars (GS_*)
   uint64_t* full;       // [NSTAGE]
   uint64_t* empty;      // [NSTAGE]
   uint64_t* accf;       // [2]
@@ -509,12 +481,16 @@ struct Smem {
   uint32_t* tslot;
   unsigned long long* dbg;  // [64] per-chunk trace stamps (RNNTG_PROF)
 };
+enum { LD_INIT = 0, LD_VISIT, LD_MULTI };  // Epi::run's load modes
+// per-group scalars: FS frame t, FS symbols at t, step s, prediction epoch p, max(out_len), running
+enum { GS_T = 0, GS_SYM, GS_STEP, GS_PE, GS_MAXLEN, GS_RUN, GS_N };
+constexpr int SM_INTS = 5 * MAXG * 32 + 3 * 32 + 16 + GS_N * MAXG;  // 1440: 8-byte aligned end
 
 constexpr int XS_FLOATS = 128 * 33;   // epilogue exchange: [128 cols][33] / [4 gates][32][32]
 constexpr int RED_F4 = 256;           // argmax merge / word staging / sumexp group scratch (4 KB)
 __host__ __device__ inline size_t smem_bytes(int KC) {
   return 1024 /*align slack*/ + (size_t)KC * 16384 + (size_t)NSTAGE * CHUNK + XS_FLOATS * 4 +
-         RED_F4 * 16 + 12 * 32 * 4 + 16 * 4 + 16 * 8 + 64 + 512;
+         RED_F4 * 16 + SM_INTS * 4 + 16 * 8 + 64 + 512;
 }
 
 __device__ inline Smem carve(unsigned char* raw, int KC) {
@@ -528,15 +504,18 @@ __device__ inline Smem carve(unsigned char* raw, int KC) {
   s.red = reinterpret_cast<float4*>(s.xs + XS_FLOATS);
   int* ip = reinterpret_cast<int*>(s.red + RED_F4);
   s.label = ip;
-  s.flag = ip + 32;
-  s.tb = ip + 64;
-  s.ub = ip + 96;
-  s.cnt = ip + 128;
-  s.kdec = ip + 160;
-  s.vdec = reinterpret_cast<float*>(ip + 192);
-  s.ddec = ip + 224;
-  s.misc = ip + 256;  // 16 words
-  uint64_t* bp = reinterpret_cast<uint64_t*>(ip + 256 + 16);
+  s.flag = ip + MAXG * 32;
+  s.tb = ip + 2 * MAXG * 32;
+  s.ub = ip + 3 * MAXG * 32;
+  s.cnt = ip + 4 * MAXG * 32;
+  ip += 5 * MAXG * 32;
+  s.kdec = ip;
+  s.vdec = reinterpret_cast<float*>(ip + 32);
+  s.ddec = ip + 64;
+  s.misc = ip + 96;  // 16 words
+  s.grp = ip + 112;  // GS_N * MAXG words
+  static_assert((SM_INTS * 4) % 8 == 0, "mbarriers need 8-byte alignment");
+  uint64_t* bp = reinterpret_cast<uint64_t*>(ip + 112 + GS_N * MAXG);
   s.full = bp;
   s.empty = bp + NSTAGE;
   s.accf = bp + 2 * NSTAGE;
@@ -614,28 +593,66 @@ struct Epi : CfgFlags<SPEC> {
   const uint32_t tq;  // TMEM address of this warp's lane quadrant
   const int et, m, r0, role, layer, tile;
   const float wsc;
-  const int B, blank;
-  const bool tracer;
-  unsigned* const cnt;
-  int maxlen = 0, round = 0, p = 0, err = 0, acc_any = 0;
-  float ih[NR];  // R_0: table0[label] rows prefetched during the decision
-  long long s = 0, joint_evals = 0, pred_steps = 0, outer_iters = 0;
+  const int blank;
+  const bool c0;      // the layer-0 cell (I_0): table0[label] + hh0, no weights
+  const bool tracer;  // event-trace CTA (single-group decodes only)
+  // ---- the current item's group (set_group) ----
+  int g = 0, B = 0, row0 = 0;
+  unsigned* cnt = nullptr;  // this group's counters
+  int* label = nullptr;
+  int* flag = nullptr;
+  int* tb = nullptr;
+  int* ub = nullptr;
+  int* ecnt = nullptr;
+  int maxlen = 0, p = 0;
+  long long s = 0;
+  // ---- CTA-wide ----
+  int round = 0, err = 0, acc_any = 0;
+  float ih[NR];  // I_0: table0[label] rows gathered during the decision
+  long long joint_evals = 0, pred_steps = 0, outer_iters = 0;
   bool finish = false;
 
   __device__ Epi(const TParams& P_, const Smem& sm_, uint32_t tmem, int et_, int q, int role_, int layer_,
                  int tile_, float wsc_)
       : CfgFlags<SPEC>(P_), P(P_), sm(sm_), tq(tmem + ((uint32_t)(32 * q) << 16)), et(et_), m(32 * q + (et_ & 31)),
         r0(NR * (et_ >> 7)), role(role_),
-        layer(layer_), tile(tile_), wsc(wsc_), B(P_.B), blank(P_.V1 - 1), 
-        tracer(PPROF(P_) && (int)blockIdx.x == P_.prof_first[role_]), cnt(P_.cnt) {}
+        layer(layer_), tile(tile_), wsc(wsc_), blank(P_.V1 - 1), c0(role_ == ROLE_I && layer_ == 0),
+        tracer(PPROF(P_) && P_.ngrp == 1 && (int)blockIdx.x == P_.prof_first[role_]) {}
+
+  __device__ __forceinline__ int& gsc(int which) const { return sm.grp[which * MAXG + g]; }
+  __device__ __forceinline__ void set_group(int g_) {
+    g = g_;
+    row0 = P.gr0[g];
+    B = P.gr0[g + 1] - row0;
+    cnt = P.cnt + (size_t)g * NCOUNTERS * CSTRIDE;
+    label = sm.label + 32 * g;
+    flag = sm.flag + 32 * g;
+    tb = sm.tb + 32 * g;
+    ub = sm.ub + 32 * g;
+    ecnt = sm.cnt + 32 * g;
+    s = gsc(GS_STEP);
+    p = gsc(GS_PE);
+    maxlen = gsc(GS_MAXLEN);
+  }
+  // (every thread keeps the same copies; thread 0 writes them back)
+  __device__ __forceinline__ void save_group() {
+    if (et == 0) {
+      gsc(GS_STEP) = (int)s;
+      gsc(GS_PE) = p;
+    }
+  }
+  // per-thread state of the groups not in flight (global, this CTA's slice)
+  __device__ __forceinline__ float* gstate(int i) const {
+    return P.gst + (((size_t)g * P.G + blockIdx.x) * NSV + i) * NEPI + et;
+  }
 
   // per-CTA publish time of step s (all CTAs): prof[(NEV + cta) * PROF_WIN + s - PROF_S0]
   __device__ __forceinline__ void mark_pub() {
-    if (PPROF(P) && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN)
+    if (PPROF(P) && P.ngrp == 1 && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN)
       PPROF(P)[(size_t)(NEV + blockIdx.x) * PROF_WIN + (s - PROF_S0)] = gtimer();
   }
   // hand-off marks (globaltimer, cross-CTA): 40 P trunk published, 42 J words
-  // stored, 43 R0 words seen, 44 R0 h0 published, 46 I1 h1 published
+  // stored, 43 I_0 words seen, 44 I_0 h0 published, 46 I1 h1 published
   __device__ __forceinline__ void gmark(int ev) {
     if (tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN)
       PPROF(P)[(size_t)ev * PROF_WIN + (s - PROF_S0)] = gtimer();
@@ -680,10 +697,11 @@ struct Epi : CfgFlags<SPEC> {
         PPROF(P)[(size_t)(ev0 + 25 + k) * PROF_WIN + (s - PROF_S0)] = t[32 + k];
     }
   }
-  // one load+MMA round on this CTA's input at epoch e (-1 = exit)
+  // one load+MMA round on this CTA's input: group g, epoch e (-1 = exit)
   __device__ __forceinline__ void post(int e) {
     if (et == 0) {
       sm.misc[round & 1] = e;
+      sm.misc[6 + (round & 1)] = g;
       mbar_arrive(sm.cmd);
     }
     ++round;
@@ -701,7 +719,7 @@ struct Epi : CfgFlags<SPEC> {
       }
     }
     const int set = NACC == 1 ? 0 : (r & 1);
-    mbar_wait_sleep(&sm.accf[set], (uint32_t)(NACC == 1 ? (r & 1) : ((r >> 1) & 1)));
+    mbar_wait(&sm.accf[set], (uint32_t)(NACC == 1 ? (r & 1) : ((r >> 1) & 1)));
     tc_fence_after();
     const uint32_t a = tq + set * ACC_COLS + r0;
     {
@@ -722,10 +740,8 @@ struct Epi : CfgFlags<SPEC> {
     if (et == 0) spin_geq(cnt + (size_t)ci * CSTRIDE, target);
     epi_sync();
   }
-  // this CTA's global stores -> visible -> counter += n.  The release's
-  // MEMBAR.GPU makes the stores visible at L2 before the counter; the
-  // consumer's bulk copies read L2 only after observing the counter and its
-  // own fence.proxy.async (producer-side proxy fences cost ~600 cycles each).
+  // this CTA's global stores -> visible -> counter += n: the barrier orders
+  // every thread's stores before thread 0's release (cumulative at gpu scope)
   __device__ __forceinline__ void bump(int ci, int n = 1) {
     epi_sync();
     if (role == ROLE_P) mark(34);
@@ -734,21 +750,16 @@ struct Epi : CfgFlags<SPEC> {
   }
 
   // Publish activation chunks staged in shared memory (canonical layout) with
-  // TMA bulk stores: wait_group 0 guarantees the writes are complete, so the
-  // counter bump can be relaxed (a release's MEMBAR.GPU costs ~2000 cycles,
-  // this path ~800: scripts/mb_pub.cu).
-  //   full chunks: stage [n][CHUNK] -> gdst[n][CHUNK], counters ci..ci+n-1
-  __device__ __forceinline__ void publish_chunks(const unsigned char* stage, unsigned char* gdst, int n, int ci,
-                                                 int buf, int kc0, int par) {
+  // TMA tensor stores into this group's rows: wait_group 0 completes the
+  // writes, then the proxy fence + release (release_after_bulk) and the
+  // counter adds.  stage [n][CHUNK] -> chunks kc0 .. kc0+n-1, counters ci..
+  __device__ __forceinline__ void publish_chunks(const unsigned char* stage, int n, int ci, int buf, int kc0,
+                                                 int par) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     epi_sync();
     if (et == PUB_ET) {
-#if TMA_ACT
-      for (int c = 0; c < n; ++c) tma_st2(&P.stmap[buf], 64 * (kc0 + c), 64 * par, stage + (size_t)c * CHUNK);
-      (void)gdst;
-#else
-      for (int c = 0; c < n; ++c) bulk_s2g(gdst + (size_t)c * CHUNK, stage + (size_t)c * CHUNK, CHUNK);
-#endif
+      for (int c = 0; c < n; ++c)
+        tma_st2(&P.stmap[buf], 64 * (kc0 + c), 64 * (2 * g + par), stage + (size_t)c * CHUNK);
       bulk_commit_wait_all();
       release_after_bulk();
       for (int c = 0; c < n; ++c) publish_add(cnt + (size_t)(ci + c) * CSTRIDE);
@@ -757,19 +768,23 @@ struct Epi : CfgFlags<SPEC> {
 
   __device__ void init_rows() {
     if (et < 32) {
-      sm.label[et] = blank;
-      sm.tb[et] = 0;
-      sm.ub[et] = 0;
-      sm.cnt[et] = 0;
-      const int len = et < B ? __ldg(&P.out_len[et]) : 0;
-      sm.flag[et] = (et < B ? (fs ? (0 >= len) : !(0 < len)) : 1) | 2;  // every row runs P0
-      if (role == ROLE_E && et < B) P.counts[et] = 0;
+      label[et] = blank;
+      tb[et] = 0;
+      ub[et] = 0;
+      ecnt[et] = 0;
+      const int len = et < B ? __ldg(&P.out_len[row0 + et]) : 0;
+      flag[et] = (et < B ? (fs ? (0 >= len) : !(0 < len)) : 1) | 2;  // every row runs P0
+      if (role == ROLE_E && et < B) P.counts[row0 + et] = 0;
     }
+    maxlen = 0;
+    for (int b = 0; b < B; ++b) maxlen = max(maxlen, __ldg(&P.out_len[row0 + b]));
+    s = 0;
+    p = 0;
     if (et == 0) {
-      sm.misc[2] = 0;
-      sm.misc[3] = 0;
+      gsc(GS_T) = 0;
+      gsc(GS_SYM) = 0;
+      gsc(GS_MAXLEN) = maxlen;
     }
-    for (int b = 0; b < B; ++b) maxlen = max(maxlen, __ldg(&P.out_len[b]));
     epi_sync();
   }
 
@@ -790,9 +805,10 @@ struct Epi : CfgFlags<SPEC> {
     if (s >= NSLOT / 2 && s % (NSLOT / 2) == 0) {
       if (et < 32) {
         const unsigned target = (unsigned)(s - NSLOT / 2 + 1);
+        const unsigned* ack = P.ack + (size_t)g * P.G;
         for (;;) {
           unsigned mn = 0xffffffffu;
-          for (int c = et; c < P.G; c += 32) mn = min(mn, ld_relaxed(P.ack + c));
+          for (int c = et; c < P.G; c += 32) mn = min(mn, ld_relaxed(ack + c));
           if (__reduce_min_sync(0xffffffffu, mn) >= target) break;
         }
       }
@@ -803,6 +819,7 @@ struct Epi : CfgFlags<SPEC> {
     const int V1 = P.V1, VD = P.V1 + P.D;
     const int lane = et & 31, q = m >> 5, grp = et >> 7;
     const int col = 128 * tile + m;
+    unsigned long long* pwg = P.pw + (size_t)g * NSLOT * 2 * P.NJ * 32;
     // per-row argmax of the tile straight from registers: a warp reduce-scatter
     // (NR rows over 32 lanes), then the 4 lane-quadrant warps of the same rows
     // merge through smem in column order.  Ties keep the lowest column
@@ -873,18 +890,9 @@ struct Epi : CfgFlags<SPEC> {
         }
         // the tagged word goes out straight from the merging thread (no staging
         // barrier); tiles without duration columns publish no duration word
-        st_relaxed_u64(P.pw + (((size_t)slot * 2 + seg) * P.NJ + tile) * 32 + rr, pack_arg(bv, bi, tg));
+        st_relaxed_u64(pwg + (((size_t)slot * 2 + seg) * P.NJ + tile) * 32 + rr, pack_arg(bv, bi, tg));
         if (seg == 0) sm.vdec[rr] = bv;  // this tile's row max, for the sumexp pass
       }
-    }
-    if (PECHO(P) && tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) {
-      // exact J -> R_0 -> J round trip on this SM's clock: J bumps a probe word,
-      // R_0 tile 0 (spinning on it) echoes the step
-      const long long c0 = clock64();
-      st_relaxed_u64(PECHO(P) + 8, (unsigned long long)(s + 1));
-      while (ld_poll_u64(PECHO(P)) != (unsigned long long)(s + 1)) {
-      }
-      PPROF(P)[(size_t)37 * PROF_WIN + (s - PROF_S0)] = clock64() - c0;
     }
     mark(18);
     gmark(42);
@@ -896,7 +904,7 @@ struct Epi : CfgFlags<SPEC> {
     epi_sync();
     constexpr int NW = NEPI / 32, CPW = 128 / NW;  // epilogue warps, columns per warp
     const int r = et & 31, qq = et >> 5;
-    const int c0 = 128 * tile + CPW * qq;
+    const int cb = 128 * tile + CPW * qq;
     float* redf = reinterpret_cast<float*>(sm.red);  // [NW][32] (rd is done)
     // sumexp over the vocab columns relative to the tile's row max
     {
@@ -905,7 +913,7 @@ struct Epi : CfgFlags<SPEC> {
 #pragma unroll
       for (int c = 0; c < CPW; ++c) {
         const float x = xs[(CPW * qq + c) * 33 + r];
-        ev += (c0 + c < V1) ? __expf(x - M) : 0.0f;
+        ev += (cb + c < V1) ? __expf(x - M) : 0.0f;
       }
       redf[qq * 32 + r] = ev;
     }
@@ -914,7 +922,7 @@ struct Epi : CfgFlags<SPEC> {
       float S = 0.0f;
 #pragma unroll
       for (int k = 0; k < NW; ++k) S += redf[k * 32 + et];
-      P.ps[((size_t)slot * P.NJ + tile) * 32 + et] = make_float2(sm.vdec[et], S);
+      P.ps[(((size_t)g * NSLOT + slot) * P.NJ + tile) * 32 + et] = make_float2(sm.vdec[et], S);
     }
     epi_sync();
     if (et == 0) red_release_add(cnt + (size_t)cidx_part() * CSTRIDE, 1);
@@ -937,12 +945,7 @@ struct Epi : CfgFlags<SPEC> {
   // the row flags with ballots; ONE barrier then publishes the outcome.
   // The emitter also merges the (max, sumexp) partials for the score.
   __device__ void decide() {
-    if (role == ROLE_R && layer == 0) gmark(41);
-    if (PECHO(P) && role == ROLE_R && layer == 0 && tracer && et == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN) {
-      while (ld_poll_u64(PECHO(P) + 8) != (unsigned long long)(s + 1)) {
-      }
-      st_relaxed_u64(PECHO(P), (unsigned long long)(s + 1));
-    }
+    if (c0) gmark(41);
     if (et < 32) {
       const int b = et;
       const bool valid = b < B;
@@ -953,26 +956,11 @@ struct Epi : CfgFlags<SPEC> {
       long long lat1_out = 0;
       float best = 0.0f;
       if (valid) {
-        const unsigned long long* wv = P.pw + (((size_t)slot * 2 * P.NJ) * 32 + b) * PW_STRIDE;
-        const unsigned long long* wd = wv + (size_t)P.NJ * 32 * PW_STRIDE;
+        const unsigned long long* wv = P.pw + (size_t)g * NSLOT * 2 * P.NJ * 32 + ((size_t)slot * 2 * P.NJ) * 32 + b;
+        const unsigned long long* wd = wv + (size_t)P.NJ * 32;
         unsigned long long a[MAXNJ], d0 = 0ull, d1 = 0ull;
 #pragma unroll
         for (int t = 0; t < MAXNJ; ++t) a[t] = 0ull;
-        // every tile's word in flight at once; only R_0 consumes the decision
-        // on the critical path, the other roles back off
-        const bool lazy = !(role == ROLE_R && layer == 0);
-#if ECHO_GATE
-        // only R_0 (the critical consumer) polls the J words; the other roles
-        // wait for R_0 tile 0's echo of the step (a word that 55 CTAs poll),
-        // then read the words once: 75 CTAs polling the word lines for ~15 us
-        // before they are written delayed the writes by ~2 us
-        if (lazy) {
-          if (b == 0)
-            while (ld_relaxed(P.decided) < (unsigned)(s + 1)) {
-            }
-          __syncwarp(0xffffffffu >> (32 - B));
-        }
-#endif
         __syncwarp(0xffffffffu >> (32 - B));
         bool ok;
         const int nj = P.NJ;
@@ -981,26 +969,18 @@ struct Epi : CfgFlags<SPEC> {
         const int td0 = P.V1 / 128, td1 = (P.V1 + P.D - 1) / 128;
         int npoll = 0;
         long long lat1 = 0;
-        if (tracer && role == ROLE_R && layer == 0 && b == 0) {  // one strong load, timed
-          const long long c0 = clock64();
+        if (tracer && c0 && b == 0) {  // one strong load, timed
+          const long long cl0 = clock64();
           const unsigned long long w0 = ld_poll_u64(wv);
-          long long c1 = 0;
-          if (w0 != 0x123456789abcdefull) c1 = clock64();  // the branch waits for the load
-          lat1 = c1 - c0;
+          long long cl1 = 0;
+          if (w0 != 0x123456789abcdefull) cl1 = clock64();  // the branch waits for the load
+          lat1 = cl1 - cl0;
         }
-#if SPIN_ONE
-        // spin on one word (tile NJ-1, written last in column order by no one in
-        // particular) with a single load in flight, then read the rest once
-        // (warp-wide strong loads are serviced ~100 cycles apart: a 9-16 load
-        // batch per poll made each poll ~1 us; one load per poll is ~360 cycles)
-        while ((unsigned)(ld_poll_u64(wv + (nj - 1) * 32 * PW_STRIDE) >> 32 & 0xffu) != tg) ++npoll;
-        if (role == ROLE_R && layer == 0 && b == 0) mark(30);  // last tile's word seen
-#endif
-#if LAZY_BATCH_NS
-        // the CTAs off the critical path read the tile words after R_0 did:
-        // 75 CTAs reading the same 18 lines at once made R_0's read ~3x slower
-        if (lazy) __nanosleep(LAZY_BATCH_NS);
-#endif
+        // spin on one word (tile NJ-1) with a single load in flight, then read
+        // the rest once (warp-wide strong loads are serviced ~100 cycles apart:
+        // a 9-16 load batch per poll made each poll ~1 us; one load is ~360 cycles)
+        while ((unsigned)(ld_poll_u64(wv + (nj - 1) * 32) >> 32 & 0xffu) != tg) ++npoll;
+        if (c0 && b == 0) mark(30);  // last tile's word seen
         do {
           ++npoll;
           ok = true;
@@ -1009,10 +989,10 @@ struct Epi : CfgFlags<SPEC> {
           // (one ~300-cycle round trip each, ~2000 cycles per poll)
 #pragma unroll
           for (int t = 0; t < MAXNJ; ++t)
-            if (t < nj) a[t] = ld_poll_u64(wv + t * 32 * PW_STRIDE);
+            if (t < nj) a[t] = ld_poll_u64(wv + t * 32);
           if (hasd) {
-            d0 = ld_poll_u64(wd + td0 * 32 * PW_STRIDE);
-            d1 = ld_poll_u64(wd + td1 * 32 * PW_STRIDE);
+            d0 = ld_poll_u64(wd + td0 * 32);
+            d1 = ld_poll_u64(wd + td1 * 32);
           }
           // branch-free tag check: a short-circuit && compiled to one branch +
           // reconvergence block per tile (~1000 cycles for 16 tiles)
@@ -1024,9 +1004,8 @@ struct Epi : CfgFlags<SPEC> {
             bad |= (unsigned)(t < nj) & (unsigned)(ta != tg);
           }
           ok = bad == 0u;
-          if (!ok && lazy && LAZY_NS) __nanosleep(LAZY_NS);
         } while (!ok);
-        if (role == ROLE_R && layer == 0 && b == 0) mark(31);  // every tile's word seen
+        if (c0 && b == 0) mark(31);  // every tile's word seen
         npoll_out = npoll;
         lat1_out = lat1;
         best = -INFINITY;
@@ -1045,23 +1024,16 @@ struct Epi : CfgFlags<SPEC> {
         dd = hasd ? P.durations[di] : 0;
       }
       sm.kdec[b] = kk;
-#if ECHO_GATE
-      if (role == ROLE_R && layer == 0 && tile == 0 && b == 0)
-        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(P.decided), "r"((unsigned)(s + 1)) : "memory");
-#endif
-
-      if (role == ROLE_R && layer == 0 && tracer && b == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN)
+      if (c0 && tracer && b == 0 && s >= PROF_S0 && s < PROF_S0 + PROF_WIN)
         PPROF(P)[(size_t)39 * PROF_WIN + (s - PROF_S0)] = (unsigned long long)npoll_out,
         PPROF(P)[(size_t)38 * PROF_WIN + (s - PROF_S0)] = (unsigned long long)lat1_out;
-      if (role == ROLE_R && layer == 0) {
-        // hand the labels to the other 7 epilogue warps now: their table0
+      if (c0) {
+        // hand the labels to the other epilogue warps now: their table0
         // gathers for the layer-0 cell overlap the rules below; this warp's
-        // own gather (rows 0..15, labels of lanes 0..15) goes out first too
+        // own gather (rows r0.., labels of lanes r0..) goes out first too
         __syncwarp();
         asm volatile("barrier.cta.arrive.aligned 2, %0;" ::"n"(NEPI) : "memory");
-#if EARLY_GATHER
         gather_table0();
-#endif
         mark(22);
         gmark(43);
       }
@@ -1071,8 +1043,9 @@ struct Epi : CfgFlags<SPEC> {
         __syncwarp();
         if (valid) {
           float Mx = -INFINITY, Sx = 0.0f;
+          const float2* psg = P.ps + ((size_t)g * NSLOT + slot) * P.NJ * 32;
           for (int t = 0; t < P.NJ; ++t) {
-            const float2 pv = __ldcg(&P.ps[((size_t)slot * P.NJ + t) * 32 + b]);
+            const float2 pv = __ldcg(&psg[(size_t)t * 32 + b]);
             if (pv.x != -INFINITY) {
               const float nm = fmaxf(Mx, pv.x);
               Sx = (Sx == 0.0f ? 0.0f : Sx * __expf(Mx - nm)) + pv.y * __expf(pv.x - nm);
@@ -1083,49 +1056,50 @@ struct Epi : CfgFlags<SPEC> {
         }
       }
       // decision rules, lane per row (decoders.cpp:261-307 / 432-512)
-      const int t_fs = sm.misc[2];
-      int f = sm.flag[b] & ~2;
+      const int t_fs = gsc(GS_T);
+      int f = flag[b] & ~2;
       if (valid) {
         const int k = kk;
+        const int rg = row0 + b;  // batch row
         if (fs) {
           if (!(f & 1)) {
             if (k == blank) {
               f |= 1;
             } else {
-              const int nb = sm.cnt[b];
+              const int nb = ecnt[b];
               if (emitter && nb < P.cap) {
-                const size_t o = (size_t)b * P.cap + nb;
+                const size_t o = (size_t)rg * P.cap + nb;
                 P.tokens[o] = k;
                 P.frames[o] = t_fs;
                 P.scores[o] = v;
                 P.durs[o] = 0;
-                P.counts[b] = nb + 1;
+                P.counts[rg] = nb + 1;
               }
-              sm.cnt[b] = nb + 1;
-              sm.label[b] = k;
+              ecnt[b] = nb + 1;
+              label[b] = k;
               f |= 2;
             }
           }
         } else if (!(f & 1)) {
-          const int len = __ldg(&P.out_len[b]);
-          int t = sm.tb[b], u = sm.ub[b];
+          const int len = __ldg(&P.out_len[rg]);
+          int t = tb[b], u = ub[b];
           if (k == blank) {
             const int d = tdt ? dd : 1;
             t += d > 1 ? d : 1;
             u = 0;
           } else {
             const int d = tdt ? dd : 0;
-            const int nb = sm.cnt[b];
+            const int nb = ecnt[b];
             if (emitter && nb < P.cap) {
-              const size_t o = (size_t)b * P.cap + nb;
+              const size_t o = (size_t)rg * P.cap + nb;
               P.tokens[o] = k;
               P.frames[o] = t;
               P.scores[o] = v;
               P.durs[o] = d;
-              P.counts[b] = nb + 1;
+              P.counts[rg] = nb + 1;
             }
-            sm.cnt[b] = nb + 1;
-            sm.label[b] = k;
+            ecnt[b] = nb + 1;
+            label[b] = k;
             f |= 2;
             u += 1;
             if (d > 0) {
@@ -1136,8 +1110,8 @@ struct Epi : CfgFlags<SPEC> {
               u = 0;
             }
           }
-          sm.tb[b] = t;
-          sm.ub[b] = u;
+          tb[b] = t;
+          ub[b] = u;
           if (!(t < len)) f |= 1;
         }
       }
@@ -1146,109 +1120,128 @@ struct Epi : CfgFlags<SPEC> {
       const bool liveany = __ballot_sync(0xffffffffu, live_b) != 0;
       bool fin = false, frame_end = false;
       if (fs) {
-        int sym = sm.misc[3] + 1;
+        int sym = gsc(GS_SYM) + 1;
         int t = t_fs;
         if (!liveany || sym >= P.ms) {  // frame ends (decoders.cpp:297-313)
           frame_end = true;
           t += 1;
           sym = 0;
           if (t >= maxlen) fin = true;
-          if (valid) f = (f & 2) | (t >= __ldg(&P.out_len[b]) ? 1 : 0);
+          if (valid) f = (f & 2) | (t >= __ldg(&P.out_len[row0 + b]) ? 1 : 0);
         }
         __syncwarp();
         if (b == 0) {
-          sm.misc[3] = sym;
-          sm.misc[2] = t;
+          gsc(GS_SYM) = sym;
+          gsc(GS_T) = t;
         }
       } else {
         fin = !liveany;
       }
-      if (joint_evals + 1 > P.max_iters) fin = true;
-      sm.flag[b] = f;
+      if (s + 1 > P.max_iters) fin = true;  // runaway cap (engine.cpp:286-290), per group
+      flag[b] = f;
       if (b == 0) sm.misc[5] = (accany ? 1 : 0) | (fin ? 2 : 0) | (frame_end ? 4 : 0);
-      if (role == ROLE_R && layer == 0) mark(24);
-    } else if (role == ROLE_R && layer == 0) {
+      if (c0) mark(24);
+    } else if (c0) {
       asm volatile("barrier.cta.sync.aligned 2, %0;" ::"n"(NEPI) : "memory");
       mark2(35);
       gather_table0();
       mark2(36);
     }
     epi_sync();
-    if (role == ROLE_R && layer == 0) mark2(37);
-    if (!EARLY_GATHER && role == ROLE_R && layer == 0 && et < 32) gather_table0();
+    if (c0) mark2(37);
     const int o = sm.misc[5];
     acc_any = o & 1;
     finish = (o >> 1) & 1;
     if (o & 4) ++outer_iters;
     ++joint_evals;
-    if (joint_evals > P.max_iters) err = ERR_RUNAWAY;
-    mark(role == ROLE_J ? 3 : role == ROLE_R ? (layer == 0 ? 4 : 10) : role == ROLE_I ? 6 : role == ROLE_E ? 15 : 8);
+    if (s + 1 > P.max_iters) err = ERR_RUNAWAY;
+    mark(role == ROLE_J ? 3 : role == ROLE_R ? 10 : c0 ? 4 : role == ROLE_I ? 6 : role == ROLE_E ? 15 : 8);
   }
 
-  // ---- the decode skeleton: pred(te) after each accepting decision, idle(te) otherwise
-  template <typename Pred, typename Idle>
-  __device__ void run(Pred&& pred, Idle&& idle) {
-    init_rows();
-    pred(0LL);  // P0 = pred(blank, 0) for every row (decoders.cpp:414-430)
-    ++pred_steps;
-    int live = et < B ? !(sm.flag[et] & 1) : 0;
-    live = epi_or(live);
-    const bool running0 = fs ? (maxlen > 0) : (live != 0);
-    if (et < 32) sm.flag[et] &= ~2;
-    epi_sync();
-    bool running = running0;
-    while (running) {
-      if (role == ROLE_J) joint_round();
-      decide();
-      if (finish) break;
-      if (acc_any) {
-        ++p;
-        pred(s + 1);
-        ++pred_steps;
-        if (!fs) ++outer_iters;
-      } else {
-        idle(s + 1);
-      }
-      // this CTA is done with step s's words: ack (slot reuse, joint_round).
-      // The ack follows reads only (their values are consumed), so it needs
-      // no release; ~75 MEMBAR.GPU per step slowed every hand-off.
-      // (per-CTA word; the reads it covers were consumed before the barrier
-      // that precedes it, so it needs no release)
-      if (et == 0) st_relaxed_u32(P.ack + blockIdx.x, (unsigned)(s + 1));
-      ++s;
-      if (et < 32) sm.flag[et] &= ~2;
+  // ---- the decode skeleton.  Every group starts with P0 = pred(blank, 0)
+  // (decoders.cpp:414-430); then the live groups are visited round-robin, one
+  // decision per visit: pred(te) after an accepting decision, idle(te)
+  // otherwise.  load(mode) starts every visit: mode LD_INIT before a group's
+  // P0 (the role's per-thread state of the group := zero), LD_VISIT with one
+  // group, LD_MULTI with several (the state of the visited group moves from
+  // global memory into registers first); save() moves it back (several
+  // groups only).
+  template <typename Pred, typename Idle, typename Load, typename Save>
+  __device__ void run(Pred&& pred, Idle&& idle, Load&& load, Save&& save) {
+    const bool multi = P.ngrp > 1;
+    for (int gg = 0; gg < P.ngrp; ++gg) {
+      set_group(gg);
+      init_rows();
+      load(LD_INIT);
+      pred(0LL);
+      ++pred_steps;
+      int live = et < B ? !(flag[et] & 1) : 0;
+      live = epi_or(live);
+      const bool running0 = fs ? (maxlen > 0) : (live != 0);
+      if (et < 32) flag[et] &= ~2;
+      if (et == 0) gsc(GS_RUN) = running0 ? 1 : 0;
+      if (multi) save();
+      save_group();
       epi_sync();
+    }
+    for (;;) {
+      bool any = false;
+      for (int gg = 0; gg < P.ngrp; ++gg) {
+        if (!sm.grp[GS_RUN * MAXG + gg]) continue;
+        any = true;
+        set_group(gg);
+        load(multi ? LD_MULTI : LD_VISIT);
+        if (role == ROLE_J) joint_round();
+        decide();
+        if (finish) {
+          if (et == 0) gsc(GS_RUN) = 0;
+          epi_sync();
+          continue;
+        }
+        if (acc_any) {
+          ++p;
+          pred(s + 1);
+          ++pred_steps;
+          if (!fs) ++outer_iters;
+        } else {
+          idle(s + 1);
+        }
+        if (multi) save();
+        // this CTA is done with step s's words: ack (slot reuse, joint_round).
+        // A per-CTA word; the reads it covers were consumed before the barrier
+        // that precedes it, so it needs no release.
+        if (et == 0) st_relaxed_u32(P.ack + (size_t)g * P.G + blockIdx.x, (unsigned)(s + 1));
+        ++s;
+        if (et < 32) flag[et] &= ~2;
+        save_group();
+        epi_sync();
+      }
+      if (!any) break;
     }
   }
 
-  // ---- layer cells: pre-activations (gate row m, rows r0..r0+15) -> committed h.
+  // ---- layer cells: pre-activations (gate row m, rows r0..r0+NR-1) -> committed h.
   // LSTM tiles are unit-major (m = 4*unit + gate): a lane quad holds one unit's
   // i,f,g,o, so the gates meet through a per-warp smem transpose (__syncwarp,
   // no CTA barrier).  Lane (quad qd, slot g') then runs the cell for rows
   // r0 + 4j + g', j < NR / 4.
   __device__ __forceinline__ void cell_lstm(const float (&pre)[NR], int l, int pe, float (&c)[NR / 4],
                                             float (&h)[NR / 4]) {
-    const int lane = et & 31, g = lane & 3, qd = lane >> 2;
+    const int lane = et & 31, gt = lane & 3, qd = lane >> 2;
     float* xw = sm.xs + (et >> 5) * (NR * 33);  // this warp's [NR rows][33]
     // i, f, o: sigmoid; g: tanh(x) = 2 sigmoid(2x) - 1 (absolute error ~1e-7,
     // what the cell update c' = f c + i g needs; one code path per lane quad)
-    const float sc = g == 2 ? 2.0f : 1.0f;
+    const float sc = gt == 2 ? 2.0f : 1.0f;
 #pragma unroll
     for (int i = 0; i < NR; ++i) {
       const float a = sigm(sc * pre[i]);
-      xw[i * 33 + lane] = g == 2 ? 2.0f * a - 1.0f : a;
+      xw[i * 33 + lane] = gt == 2 ? 2.0f * a - 1.0f : a;
     }
     __syncwarp();
     const int u = 32 * tile + 8 * (m >> 5) + qd;
-#if TMA_ACT
     // a tile's 32 units: one 32 x 64 box, staged plain [64 rows][32] fp16
     __half* st16 = reinterpret_cast<__half*>(sm.red);
     const int ul = u - 32 * tile;
-#else
-    // a tile's 32 units are half a chunk (64-byte row segments): direct stores
-    // + release (64 separate 64-byte bulk stores cost more, scripts/mb_pub.cu)
-    unsigned char* ch = P.act[l] + ((size_t)(pe & 1) * P.act_kc[l] + (u >> 6)) * CHUNK;
-#endif
     // loads, arithmetic and stores in separate passes: the compiler cannot move
     // a later row's xw loads above an earlier row's st16 stores (both shared
     // memory), which serialised the NR / 4 per-row dependency chains
@@ -1256,47 +1249,39 @@ struct Epi : CfgFlags<SPEC> {
     bool cm[NR / 4];
 #pragma unroll
     for (int j = 0; j < NR / 4; ++j) {
-      const int i = 4 * j + g, r = r0 + i;
+      const int i = 4 * j + gt, r = r0 + i;
       gi[j] = xw[i * 33 + 4 * qd];
       gf[j] = xw[i * 33 + 4 * qd + 1];
       gg[j] = xw[i * 33 + 4 * qd + 2];
       go[j] = xw[i * 33 + 4 * qd + 3];
-      cm[j] = r < B && (sm.flag[r] & 2);
+      cm[j] = r < B && (flag[r] & 2);
     }
 #pragma unroll
     for (int j = 0; j < NR / 4; ++j) {
       const float cn = gf[j] * c[j] + gi[j] * gg[j];
       // tanh(c) = 2 sigm(2c) - 1 like the g gate (absolute error ~1e-7, what
       // h = o tanh(c) needs): no polynomial branch on the dependency chain
-      const float hn = u < P.H ? go[j] * (TANH_SIG ? fmaf(2.0f, sigm(2.0f * cn), -1.0f) : tanh_fast(cn)) : 0.0f;
+      const float hn = u < P.H ? go[j] * fmaf(2.0f, sigm(2.0f * cn), -1.0f) : 0.0f;
       c[j] = cm[j] ? cn : c[j];
       h[j] = cm[j] ? hn : h[j];
     }
 #pragma unroll
     for (int j = 0; j < NR / 4; ++j) {
-      const int r = r0 + 4 * j + g;
-#if TMA_ACT
+      const int r = r0 + 4 * j + gt;
       const __half hh = __float2half_rn(h[j]);
       st16[r * 32 + ul] = hh;
       st16[(32 + r) * 32 + ul] = __float2half_rn(h[j] - __half2float(hh));
-#else
-      store_split(ch, r, u & 63, h[j]);
-#endif
     }
     __syncwarp();
-    if (role == ROLE_R) mark(21);
-#if TMA_ACT
+    if (c0) mark(21);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     epi_sync();
     if (et == PUB_ET) {
-      tma_st2(&P.stmap[l], 32 * tile, 64 * (pe & 1), st16);
+      tma_st2(&P.stmap[l], 32 * tile, 64 * (2 * g + (pe & 1)), st16);
       bulk_commit_wait_all();
       release_after_bulk();
       publish_add(cnt + (size_t)cidx_act(l, (32 * tile) >> 6) * CSTRIDE);
     }
-#else
-    bump(cidx_act(l, (32 * tile) >> 6));
-#endif
   }
   // tanh RNN: one unit per row m (128 units per tile)
   __device__ __forceinline__ void cell_tanh(const float (&pre)[NR], int l, int pe, float (&h)[NR]) {
@@ -1308,13 +1293,12 @@ struct Epi : CfgFlags<SPEC> {
       for (int i = 0; i < NR; ++i) {
         const int r = r0 + i;
         const float hn = u < P.H ? tanh_fast(pre[i]) : 0.0f;
-        h[i] = (r < B && (sm.flag[r] & 2)) ? hn : h[i];
+        h[i] = (r < B && (flag[r] & 2)) ? hn : h[i];
         store_split(ch, r, u & 63, h[i]);
       }
     }
-    const int c0 = (128 * tile) >> 6;
-    publish_chunks(stage, P.act[l] + ((size_t)(pe & 1) * P.act_kc[l] + c0) * CHUNK, min(2, P.act_kc[l] - c0),
-                   cidx_act(l, c0), l, c0, pe & 1);
+    const int cb = (128 * tile) >> 6;
+    publish_chunks(stage, min(2, P.act_kc[l] - cb), cidx_act(l, cb), l, cb, pe & 1);
   }
 
   __device__ void run_role();
@@ -1324,8 +1308,10 @@ template <bool TR, int SPEC>
 __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
   const int unit = lstm ? 32 * tile + (m >> 2) : 128 * tile + m;  // LSTM tiles: m = 4*unit + gate
   const int gate = lstm ? (m & 3) : 0;
+  auto nop = [&]() {};
+  auto nopl = [&](int) {};
   if (role == ROLE_J || role == ROLE_E) {
-    run([&](long long) {}, [&](long long) {});
+    run([&](long long) {}, [&](long long) {}, nopl, nop);
   } else if (role == ROLE_P) {
     float gp[NR], fpv[NR];
 #pragma unroll
@@ -1333,15 +1319,15 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
     const int j = 128 * tile + m;
     // fp[b, t_b, j] for the next trunk, t from the latest decision
     auto prefetch = [&]() {
-      const int tfs = sm.misc[2];
+      const int tfs = gsc(GS_T);
 #pragma unroll
       for (int i = 0; i < NR; ++i) {
         // unconditional (clamped) loads so the warp does not stall here; rows
         // >= B / columns >= J are masked where the values are used
         const int r = min(r0 + i, B - 1);
-        int t = fs ? tfs : sm.tb[r];
+        int t = fs ? tfs : tb[r];
         t = t < 0 ? 0 : (t > P.T - 1 ? P.T - 1 : t);
-        fpv[i] = __ldg(&P.fp[((size_t)r * P.T + t) * P.Jp + min(j, P.Jp - 1)]);
+        fpv[i] = __ldg(&P.fp[((size_t)(row0 + r) * P.T + t) * P.Jp + min(j, P.Jp - 1)]);
       }
     };
     auto trunk = [&](long long te) {  // trunk(te) = relu(fp + gp) -> act[TRUNK]
@@ -1356,10 +1342,9 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
           store_split(ch, r, j & 63, x);
         }
       }
-      const int c0 = (128 * tile) >> 6;
+      const int cb = (128 * tile) >> 6;
       mark(33);
-      publish_chunks(stage, P.act[TRUNK] + ((size_t)(te & 1) * P.act_kc[TRUNK] + c0) * CHUNK,
-                     min(2, P.act_kc[TRUNK] - c0), cidx_act(TRUNK, c0), TRUNK, c0, (int)(te & 1));
+      publish_chunks(stage, min(2, P.act_kc[TRUNK] - cb), cidx_act(TRUNK, cb), TRUNK, cb, (int)(te & 1));
       gmark(40);
     };
     run(
@@ -1379,63 +1364,81 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
         [&](long long te) {
           prefetch();
           trunk(te);
+        },
+        [&](int mode) {
+#pragma unroll
+          for (int i = 0; i < NR; ++i) gp[i] = mode == LD_MULTI ? *gstate(i) : mode == LD_INIT ? 0.0f : gp[i];
+        },
+        [&]() {
+#pragma unroll
+          for (int i = 0; i < NR; ++i) *gstate(i) = gp[i];
         });
-  } else if (role == ROLE_R && layer > 0) {
+  } else if (role == ROLE_R) {
+    // hh_l(p+1) = h_l(p) @ W_hh_l -> global, for the layer-l cell of the next prediction
     run(
         [&](long long) {
           post(p);
           float v[NR];
           read_acc(round - 1, v);
-          float* hb = P.hh[layer] + ((size_t)((p + 1) & 1) * 64 + tile) * 32 * 128;
+          float* hb = P.hh[layer] + ((size_t)(2 * g + ((p + 1) & 1)) * 64 + tile) * 32 * 128;
 #pragma unroll
           for (int i = 0; i < NR; ++i) hb[(r0 + i) * 128 + m] = v[i];
           bump(cidx_hh(layer, tile));
           mark_pub();
         },
-        [&](long long) {});
+        [&](long long) {}, nopl, nop);
   } else {
-    // R_0 (layer-0 cell after the decision) or I_l (layer-l cell)
+    // I_0 (layer-0 cell: table0[label] + hh0) or I_l (W_ih_l MMA + hh_l)
     const float* bl = P.bias[layer];
     const float bias_m = unit < P.H ? __ldg(&bl[gate * P.H + unit]) : 0.0f;
-    const bool isr0 = role == ROLE_R;
-    float c4[NR / 4], h4[NR / 4], hr[NR];
+    float c4[NR / 4], h4[NR / 4], hr[NR], hx[NR];
+    int hx_ep = -1;  // I_0: prediction epoch whose hh0 is in hx
 #pragma unroll
     for (int j = 0; j < NR / 4; ++j) c4[j] = h4[j] = 0.0f;
 #pragma unroll
-    for (int j = 0; j < NR; ++j) hr[j] = 0.0f;
+    for (int j = 0; j < NR; ++j) hr[j] = hx[j] = 0.0f;
+    // hh_l(pe) (R_l's output) -> x; zero for P0
+    auto load_hh = [&](int pe, float (&x)[NR]) {
+      if (pe > 0) {
+        wait_counter(cidx_hh(layer, tile), (unsigned)pe);
+        const float* hb = P.hh[layer] + ((size_t)(2 * g + (pe & 1)) * 64 + tile) * 32 * 128;
+#pragma unroll
+        for (int i = 0; i < NR; ++i) x[i] = __ldcg(&hb[(r0 + i) * 128 + m]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < NR; ++i) x[i] = 0.0f;
+      }
+    };
+    // I_0: the next prediction's hh0 is ready long before the decision: fetch
+    // it at the start of the visit, before the word poll
+    auto prefetch_hh0 = [&]() {
+      if (c0 && hx_ep != p + 1) {
+        load_hh(p + 1, hx);
+        hx_ep = p + 1;
+      }
+    };
     run(
         [&](long long) {
           float v[NR], x[NR];
-          if (isr0) {
-            // gates0 = (table0[label] + hh0) + b   (App. B order); hh0 was
-            // accumulated after the previous step (TMEM), zero for P0
+          if (c0) {
+            // gates0 = (table0[label] + hh0) + b   (App. B order)
             if (p == 0) {  // P0: label blank for every row
 #pragma unroll
               for (int i = 0; i < NR; ++i)
                 ih[i] = r0 + i < B ? __ldg(&P.table0[(size_t)blank * P.GH + unit * P.Gg + gate]) : 0.0f;
             }
-#pragma unroll
-            for (int i = 0; i < NR; ++i) x[i] = (sm.flag[r0 + i] & 2) ? ih[i] : 0.0f;
-            if (p > 0) {
-              read_acc(round - 1, v);
-            } else {
-#pragma unroll
-              for (int i = 0; i < NR; ++i) v[i] = 0.0f;
+            if (hx_ep != p) {
+              load_hh(p, hx);
+              hx_ep = p;
             }
 #pragma unroll
-            for (int i = 0; i < NR; ++i) v[i] = (x[i] + v[i]) + bias_m;
+            for (int i = 0; i < NR; ++i) x[i] = (flag[r0 + i] & 2) ? ih[i] : 0.0f;
+#pragma unroll
+            for (int i = 0; i < NR; ++i) v[i] = (x[i] + hx[i]) + bias_m;
             mark(19);
           } else {
             post(p);
-            if (p > 0) {  // recurrent half from R_l, ready long before the input half
-              wait_counter(cidx_hh(layer, tile), (unsigned)p);
-              const float* hb = P.hh[layer] + ((size_t)(p & 1) * 64 + tile) * 32 * 128;
-#pragma unroll
-              for (int i = 0; i < NR; ++i) x[i] = __ldcg(&hb[(r0 + i) * 128 + m]);
-            } else {
-#pragma unroll
-              for (int i = 0; i < NR; ++i) x[i] = 0.0f;
-            }
+            load_hh(p, x);  // recurrent half from R_l, ready long before the input half
             read_acc(round - 1, v);
             mark(7);
             if (layer == 1) log_ld(48);
@@ -1446,19 +1449,46 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
           if (lstm) cell_lstm(v, layer, p, c4, h4);
           else cell_tanh(v, layer, p, hr);
           mark_pub();
-          gmark(isr0 ? 44 : 46);
-          if (isr0) {
-            mark(5);
-            post(p);  // hh0(p+1) = h0(p) @ W_hh0 into the other accumulator
-          } else {
-            mark(11);
-          }
+          gmark(c0 ? 44 : 46);
+          mark(c0 ? 5 : 11);
         },
-        [&](long long) {});
-    if (isr0) {  // drain the look-ahead hh0 round
-      float v[NR];
-      read_acc(round - 1, v);
-    }
+        [&](long long) {},
+        [&](int mode) {
+          if (mode == LD_INIT) {
+#pragma unroll
+            for (int j = 0; j < NR / 4; ++j) c4[j] = h4[j] = 0.0f;
+#pragma unroll
+            for (int j = 0; j < NR; ++j) hr[j] = 0.0f;
+            hx_ep = -1;
+            return;
+          }
+          if (mode == LD_MULTI) {
+            if (lstm) {
+#pragma unroll
+              for (int j = 0; j < NR / 4; ++j) {
+                c4[j] = *gstate(j);
+                h4[j] = *gstate(NR / 4 + j);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < NR; ++j) hr[j] = *gstate(j);
+            }
+            hx_ep = -1;
+          }
+          prefetch_hh0();
+        },
+        [&]() {
+          if (lstm) {
+#pragma unroll
+            for (int j = 0; j < NR / 4; ++j) {
+              *gstate(j) = c4[j];
+              *gstate(NR / 4 + j) = h4[j];
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < NR; ++j) *gstate(j) = hr[j];
+          }
+        });
   }
   post(-1);
   if (blockIdx.x == 0 && et == 0) {
@@ -1510,8 +1540,9 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
   const int4 rl = P.roles[blockIdx.x];
   const int role = rl.x, layer = rl.y, tile = rl.z;
   const float wsc = __int_as_float(rl.w);
-  const int in_buf = (role == ROLE_J || role == ROLE_E) ? TRUNK : role == ROLE_P ? P.L - 1 : role == ROLE_R ? layer : layer - 1;
-  const int KC = role == ROLE_E ? 0 : P.act_kc[in_buf];
+  const int in_buf = (role == ROLE_J || role == ROLE_E) ? TRUNK : role == ROLE_P ? P.L - 1 : role == ROLE_R ? layer
+                                                                                                      : max(layer - 1, 0);
+  const int KC = (role == ROLE_E || (role == ROLE_I && layer == 0)) ? 0 : P.act_kc[in_buf];  // no weights: E, I_0
   Smem sm = carve(smem_raw, KC);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const CfgFlags<SPEC> cf(P);
@@ -1572,7 +1603,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
     // the epilogue read the previous round's accumulator, so every earlier MMA
     // (and its smem read) has completed and the first NSTAGE chunks need no
     // empty-barrier wait.  eb bit s = uses of stage s so far (mod 2).
-    const unsigned* mycnt = P.cnt + (size_t)(cidx_act(in_buf, 0) + (lane < KC ? lane : 0)) * CSTRIDE;
+    const unsigned* mycnt0 = P.cnt + (size_t)(cidx_act(in_buf, 0) + (lane < KC ? lane : 0)) * CSTRIDE;
     const unsigned my_np = lane < KC ? (unsigned)P.nprod[in_buf][lane] : 0u;
     const CUtensorMap* lmap = &P.ldmap[in_buf];
     const bool stamp_ip = PPROF(P) && (role == ROLE_I || role == ROLE_P) && (int)blockIdx.x == P.prof_first[role];
@@ -1585,6 +1616,8 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
       mbar_wait(sm.cmd, r & 1);
       const int e = ((volatile int*)sm.misc)[r & 1];
       if (e < 0) break;
+      const int grp = ((volatile int*)sm.misc)[6 + (r & 1)];  // the round's row group
+      const unsigned* mycnt = mycnt0 + (size_t)grp * NCOUNTERS * CSTRIDE;
       const bool tr = trj && e >= PROF_S0 && e < PROF_S0 + PROF_WIN;
       const unsigned target = my_np * (unsigned)(e + 1);
       int next = 0, npoll = 0;
@@ -1618,7 +1651,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
             if (ctr) sm.dbg[kc] = clock64();
             if (elect_one()) {
               mbar_arrive_expect_tx(&sm.full[st], CHUNK);
-              tma_ld2_u(ring0 + st * CHUNK, lmap, 64 * kc, 64 * (e & 1), &sm.full[st]);
+              tma_ld2_u(ring0 + st * CHUNK, lmap, 64 * kc, 64 * (2 * grp + (e & 1)), &sm.full[st]);
             }
             __syncwarp();
           }

@@ -119,7 +119,7 @@ struct rnntg_decoder {
   // host-side work of the last decode (TimingReport.num_syncs / launches)
   int64_t n_syncs = 0, n_launches = 0, n_graph_launches = 0;
   // tensor executor above its per-kernel batch: balanced sub-batches of
-  // <= ptc::MAXB rows, each its own tensor-core decoder, run back to back on
+  // <= ptc::MAXB * ptc::MAXG rows, each its own tensor-core decoder, run back to back on
   // this decoder's stream (every K6 kernel takes most of the GPU's SMs)
   std::vector<rnntg_decoder*> subs;
   std::vector<int> sub_b0;
@@ -526,7 +526,8 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   const rnntg_dims& dd = m->dims;
   const bool lstm = M.cell == RNNTG_CELL_LSTM;
   const int H = M.H, J = M.J, V1 = M.V1, D = M.D, Hp = M.Hp, Jp = M.Jp, L = M.L;
-  if (d->B > ptc::MAXB) return fail(RNNTG_E_VALUE, "tensor-core executor supports batch <= 32");
+  if (d->B > ptc::MAXB * ptc::MAXG) return fail(RNNTG_E_VALUE, "tensor-core executor supports batch <= 256");
+  const int ngrp = (d->B + ptc::MAXB - 1) / ptc::MAXB;  // balanced row groups of <= 32 rows
   if (Hp > ptc::MAXKP || Jp > ptc::MAXKP)
     return fail(RNNTG_E_VALUE, "tensor-core executor supports hidden/joint <= 640");
   const int NJ = (V1 + D + 127) / 128, NP = (J + 127) / 128;
@@ -538,8 +539,7 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   for (int t = 0; t < NP; ++t) roles.push_back(make_int4(ptc::ROLE_P, 0, t, 0));
   for (int l = 0; l < L; ++l) {
     for (int t = 0; t < NG; ++t) roles.push_back(make_int4(ptc::ROLE_R, l, t, 0));
-    if (l > 0)
-      for (int t = 0; t < NG; ++t) roles.push_back(make_int4(ptc::ROLE_I, l, t, 0));
+    for (int t = 0; t < NG; ++t) roles.push_back(make_int4(ptc::ROLE_I, l, t, 0));  // I_0: the layer-0 cell
   }
   roles.push_back(make_int4(ptc::ROLE_E, 0, 0, 0));
   const int G = (int)roles.size();
@@ -570,7 +570,7 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   std::vector<float> row(ptc::MAXKP);
   for (int c = 0; c < G; ++c) {
     const int role = roles[c].x, l = roles[c].y, t = roles[c].z;
-    if (role == ptc::ROLE_E) {
+    if (role == ptc::ROLE_E || (role == ptc::ROLE_I && l == 0)) {  // no weights
       const float one = 1.0f;
       std::memcpy(&roles[c].w, &one, 4);
       continue;
@@ -653,6 +653,8 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   tp.GH = M.GH;
   tp.Gg = M.G;
   tp.max_iters = d->st.max_iters;
+  tp.ngrp = ngrp;
+  for (int g = 0; g <= ngrp; ++g) tp.gr0[g] = (int)((long long)d->B * g / ngrp);
   for (int i = 0; i < D; ++i) tp.durations[i] = dd.durations[i];
   int4* droles = nullptr;
   CK(upload(d->mem, &droles, roles));
@@ -674,7 +676,7 @@ rnntg_status setup_tc(rnntg_decoder* d) {
     if (b < L || b == ptc::TRUNK) {
       const int kc = (b == ptc::TRUNK ? Jp : Hp) / 64;
       tp.act_kc[b] = kc;
-      CK(d->mem.alloc(&tp.act[b], (size_t)2 * kc * ptc::CHUNK));
+      CK(d->mem.alloc(&tp.act[b], (size_t)ngrp * 2 * kc * ptc::CHUNK));
       for (int c = 0; c < kc; ++c) {
         int n = 0;
         if (b == ptc::TRUNK) {
@@ -696,7 +698,7 @@ rnntg_status setup_tc(rnntg_decoder* d) {
     for (int b = 0; b <= ptc::TRUNK; ++b) {
       if (!(b < L || b == ptc::TRUNK)) continue;
       const int Kp = tp.act_kc[b] * 64;
-      const cuuint64_t dims[2] = {(cuuint64_t)Kp, 128};
+      const cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)128 * ngrp};
       const cuuint64_t strides[1] = {(cuuint64_t)Kp * 2};
       const cuuint32_t estr[2] = {1, 1};
       const cuuint32_t lbox[2] = {64, 64};
@@ -712,16 +714,17 @@ rnntg_status setup_tc(rnntg_decoder* d) {
         return fail(RNNTG_E_CUDA, "activation store tensor map");
     }
   }
-  for (int l = 1; l < L; ++l) CK(d->mem.alloc(&tp.hh[l], (size_t)2 * 64 * 32 * 128));
-  d->tpw_bytes = (size_t)ptc::NSLOT * 2 * NJ * 32 * ptc::PW_STRIDE * sizeof(unsigned long long);
-  CK(d->mem.alloc(&tp.pw, (size_t)ptc::NSLOT * 2 * NJ * 32 * ptc::PW_STRIDE));
-  CK(d->mem.alloc(&tp.ps, (size_t)ptc::NSLOT * NJ * 32));
-  // counters, then the G per-CTA ack words: zeroed together before every launch
-  d->tcnt_bytes = ((size_t)ptc::NCOUNTERS * ptc::CSTRIDE + (size_t)G) * sizeof(unsigned);
-  CK(d->mem.alloc(&d->tcnt, (size_t)ptc::NCOUNTERS * ptc::CSTRIDE + (size_t)G));
+  for (int l = 0; l < L; ++l) CK(d->mem.alloc(&tp.hh[l], (size_t)ngrp * 2 * 64 * 32 * 128));
+  d->tpw_bytes = (size_t)ngrp * ptc::NSLOT * 2 * NJ * 32 * sizeof(unsigned long long);
+  CK(d->mem.alloc(&tp.pw, (size_t)ngrp * ptc::NSLOT * 2 * NJ * 32));
+  CK(d->mem.alloc(&tp.ps, (size_t)ngrp * ptc::NSLOT * NJ * 32));
+  // per group: counters, then the G per-CTA ack words: zeroed together before every launch
+  const size_t ncnt = (size_t)ngrp * ptc::NCOUNTERS * ptc::CSTRIDE;
+  d->tcnt_bytes = (ncnt + (size_t)ngrp * G) * sizeof(unsigned);
+  CK(d->mem.alloc(&d->tcnt, ncnt + (size_t)ngrp * G));
   tp.cnt = d->tcnt;
-  tp.ack = d->tcnt + (size_t)ptc::NCOUNTERS * ptc::CSTRIDE;
-  tp.decided = d->tcnt + (size_t)(ptc::NCOUNTERS - 1) * ptc::CSTRIDE;  // zeroed with the counters
+  tp.ack = d->tcnt + ncnt;
+  if (ngrp > 1) CK(d->mem.alloc(&tp.gst, (size_t)ngrp * G * ptc::NSV * ptc::NEPI));
   tp.tokens = d->st.tokens;
   tp.frames = d->st.frames;
   tp.scores = d->st.scores;
@@ -732,7 +735,6 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   for (int c = G - 1; c >= 0; --c) tp.prof_first[roles[c].x] = c;
   if (env_flag("RNNTG_PROF", false)) {
     CK(d->mem.alloc(&tp.prof, (size_t)(2 * ptc::NEV + G) * ptc::PROF_WIN));
-    if (env_flag("RNNTG_ECHO", false)) CK(d->mem.alloc(&tp.echo, 16));
   }
   return RNNTG_OK;
 }
@@ -1131,7 +1133,7 @@ rnntg_status rnntg_decoder_create(rnntg_model* m, int algo, int exec, int batch,
   if (exec < RNNTG_EXEC_GRAPH || exec > RNNTG_EXEC_HOSTLOOP)
     return fail(RNNTG_E_VALUE, "unknown exec mode");
   CK(cudaSetDevice(m->device));
-  if (exec == RNNTG_EXEC_TENSOR && batch > ptc::MAXB && m->dm.cell != RNNTG_CELL_SCRIPTED) {
+  if (exec == RNNTG_EXEC_TENSOR && batch > ptc::MAXB * ptc::MAXG && m->dm.cell != RNNTG_CELL_SCRIPTED) {
     // balanced sub-batches, one tensor-core decoder each, sharing one stream
     auto* d = new rnntg_decoder;
     d->m = m;
@@ -1140,7 +1142,7 @@ rnntg_status rnntg_decoder_create(rnntg_model* m, int algo, int exec, int batch,
     d->B = batch;
     d->T = max_frames;
     d->ms = max_symbols;
-    const int nsub = (batch + ptc::MAXB - 1) / ptc::MAXB;
+    const int nsub = (batch + ptc::MAXB * ptc::MAXG - 1) / (ptc::MAXB * ptc::MAXG);
     cudaError_t e = cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreate(&d->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&d->ev1);

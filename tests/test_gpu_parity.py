@@ -137,8 +137,8 @@ def test_lstm_golden(golden, idx, exec):
 
 @pytest.mark.parametrize("tdt", [False, True])
 def test_tensor_batch_above_kernel_limit(tdt):
-    """Tensor executor at B = 80: balanced sub-batches (27, 27, 26) of
-    tensor-core decoders run back to back; rows keep their order."""
+    """Tensor executor at B = 80: ONE kernel decoding three balanced row
+    groups (27, 27, 26) interleaved; rows keep their order."""
     _need_gpu()
     d = O.Dims(200, 64, 64, 96, 24, (0, 1, 2, 3, 4) if tdt else (), O.CELL_LSTM, 2)
     p = O.init_params(21, d)
@@ -274,4 +274,51 @@ def test_executors_agree_full_size(other, algo):
     assert same == B
     for a, b in zip(g, p):
         assert rel_err(a.scores, b.scores) < RTOL
+    m.close()
+
+
+@pytest.mark.parametrize("B", [33, 96, 256])
+@pytest.mark.parametrize("algo", [DecodeAlgo.FrameSync, DecodeAlgo.LabelLoop, DecodeAlgo.TdtLabelLoop],
+                         ids=lambda a: a.name)
+def test_tensor_row_groups(B, algo):
+    """Tensor executor beyond 32 rows in one kernel (ceil(B / 32) row groups,
+    every CTA visiting the live groups round-robin): ragged lengths (zeros,
+    short rows) so groups finish at different steps; against the oracle."""
+    _need_gpu()
+    tdt = algo == DecodeAlgo.TdtLabelLoop
+    d = O.Dims(150, 64, 64, 96, 24, (0, 1, 2, 3, 4) if tdt else (), O.CELL_LSTM, 2)
+    p = O.init_params(31, d)
+    T, ms = 14, 3
+    x = O.fill_uniform(32, -1.0, 1.0, (B, T, d.feature))
+    lens = np.array([0 if i % 29 == 3 else T - (7 * i) % 11 for i in range(B)], np.int32)
+    lens[-32:] = np.minimum(lens[-32:], 4)  # the last group finishes early
+    m = Model(to_model_dims(d), p)
+    cap = D.build_decode_graph(m, algo, B, T, ms, D.Exec.Tensor)
+    got = D.replay_decode(cap, x, lens)
+    again = D.replay_decode(cap, x, lens)
+    assert all(a == b for a, b in zip(got, again))
+    ref = O.decode_batch(d, p, x, lens, ms, tdt, record=True)
+    rep = compare_batch(got, ref, d.vocab, tdt, f"B{B}/{algo.name}")
+    st = cap.stats()
+    assert st["emitted"] == sum(len(h.tokens) for h in got)
+    print(f"\nB{B}/{algo.name}: {rep.exact}/{rep.utterances} exact, joint evals {st['joint_evals']}")
+    assert rep.ok, rep.failures[:5]
+    cap.close()
+    m.close()
+
+
+def test_tensor_row_groups_c2_dims():
+    """C2 dims (2x640 LSTM, V 1025) at B = 80, T = 6 on the single kernel."""
+    _need_gpu()
+    d = O.Dims(1024, 640, 640, 640, 1024, (), O.CELL_LSTM, 2)
+    p = O.init_params(1, d)
+    B, T, ms = 80, 6, 5
+    x = O.fill_uniform(2, -1.0, 1.0, (B, T, 1024))
+    lens = np.array([T - i % 3 for i in range(B)], np.int32)
+    m = Model(to_model_dims(d), p)
+    got = D.replay_decode(D.build_decode_graph(m, DecodeAlgo.FrameSync, B, T, ms, D.Exec.Tensor), x, lens)
+    ref = O.decode_batch(d, p, x, lens, ms, False, record=True)
+    rep = compare_batch(got, ref, d.vocab, False, "c2dims B80")
+    print(f"\nc2dims B80: {rep.exact}/{rep.utterances} exact, {rep.permitted} permitted")
+    assert rep.ok, rep.failures[:5]
     m.close()
