@@ -47,7 +47,7 @@ CONFIGS = {
     "c5": ("fs", 256, 500, 5, (), 2, 640, 640, 1024, 1024, "strong"),
 }
 ALGO_ID = {"fs": 0, "ll": 1, "tdt": 2}
-EXEC_ID = {"graph": 0, "persistent": 1, "tensor": 2, "hostloop": 3}
+EXEC_ID = {"graph": 0, "persistent": 1, "tensor": 2, "hostloop": 3, "graph_ffma": 4}
 ALGO_NAME = {"fs": "frame-looping", "ll": "label-looping", "tdt": "TDT label-looping"}
 METRIC = "decoded encoder frames/sec (Parakeet-1.1B dec, B=32); GPU idle %; µs/step"
 
@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--exec", default="tensor", choices=["tensor", "graph", "persistent", "hostloop"],
+    ap.add_argument("--exec", default="tensor", choices=["tensor", "graph", "persistent", "hostloop", "graph_ffma"],
                     help="tensor: persistent kernel on tcgen05 tensor cores (default, fastest; falls "
                          "back to persistent when the shape does not fit it), persistent: FFMA "
                          "persistent kernel, graph: conditional-WHILE CUDA graph, hostloop: the "
@@ -369,7 +369,7 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent):
 def measure_alt_exec(args, L_, model, cfg, xd, ld, Bl, T, frames_all):
     """Time the other executors on the same inputs."""
     return [measure_exec(other, L_, model, cfg, xd, ld, Bl, T, frames_all)
-            for other in ("tensor", "persistent", "graph", "hostloop") if other != args.exec]
+            for other in ("tensor", "persistent", "graph", "graph_ffma", "hostloop") if other != args.exec]
 
 
 def measure_exec(other, L_, model, cfg, xd, ld, Bl, T, frames_all):

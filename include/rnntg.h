@@ -60,12 +60,16 @@ typedef enum {
 
 /* How the loops run on the device. */
 typedef enum {
-  RNNTG_EXEC_GRAPH = 0,       /* CUDA graph, nested conditional WHILE nodes */
+  RNNTG_EXEC_GRAPH = 0,       /* CUDA graph, nested conditional WHILE nodes; loop bodies = the
+                                 tcgen05 step kernel (one decision per launch) when the model fits
+                                 it, else the FFMA step kernels of RNNTG_EXEC_GRAPH_FFMA */
   RNNTG_EXEC_PERSISTENT = 1,  /* one cooperative persistent kernel, in-kernel loops (FFMA) */
   RNNTG_EXEC_TENSOR = 2,      /* persistent kernel on tcgen05 tensor cores, role-specialised CTAs */
-  RNNTG_EXEC_HOSTLOOP = 3     /* sync-requiring baseline (greedy_decode_baseline, decoders.cpp:546-563):
+  RNNTG_EXEC_HOSTLOOP = 3,    /* sync-requiring baseline (greedy_decode_baseline, decoders.cpp:546-563):
                                  the graph's kernels driven by a host loop with a device->host flag
                                  read + synchronise per step; rnntg_launch blocks until done */
+  RNNTG_EXEC_GRAPH_FFMA = 4   /* CUDA graph with conditional WHILE nodes over the FFMA step kernels
+                                 (joint, per-layer prediction, pred_proj: 4 nodes per inner step) */
 } rnntg_exec;
 
 /* RnntDims (model.hpp:31-40) + the prediction-network cell.

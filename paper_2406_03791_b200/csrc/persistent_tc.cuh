@@ -171,7 +171,33 @@ struct TParams {
   Ctrl* ctrl;
   unsigned long long* prof;   // optional event trace [NEV][PROF_WIN] (first CTA of each role)
   int prof_first[NROLES];     // first CTA index per role (tracing CTAs)
+  // step launches (the CUDA-graph executor's loop body and the host loop):
+  // STEP_NONE = the whole decode in one launch; STEP_INIT = P0 of every group;
+  // STEP_ONE = one decision of every live group, then the loop flags
+  int step_mode;
+  int* ctl;                   // [G][CTL_INTS] each CTA's replicated control state between step launches
+  cudaGraphConditionalHandle h_outer, h_inner;
+  int use_cond;               // set the conditional handles (graph bodies)
+  unsigned long long* stamps;  // optional [G][16] globaltimer stamps of the last launch (RNNTG_STAMPS)
 };
+#ifndef STAMPS
+#define STAMPS 0  // compile the RNNTG_STAMPS launch stamps in (A/B builds: the checks cost in the hot loop)
+#endif
+// stamps[slot][cta][16], slot = (group 0's step at launch start) % 64
+__device__ __forceinline__ void stamp_at(const TParams& P, int slot, int i, unsigned long long t) {
+  if (STAMPS && P.stamps) P.stamps[((size_t)(slot & 63) * P.G + blockIdx.x) * 16 + i] = t;
+}
+__device__ __forceinline__ void stamp(const TParams& P, int slot, int i) {
+  if (STAMPS && P.stamps) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    stamp_at(P, slot, i, t);
+  }
+}
+enum { STEP_NONE = 0, STEP_INIT = 1, STEP_ONE = 2 };
+#ifndef STEP_JROT
+#define STEP_JROT 1  // step launches: J's joint at the end of a launch (for the next step)
+#endif
 constexpr int PROF_WIN = 64;  // traced joint steps [PROF_S0, PROF_S0 + PROF_WIN)
 constexpr int PROF_S0 = 100;
 constexpr int NEV = 136;  // 40..47: globaltimer hand-off marks; 48..53: I1/P load + MMA marks;
@@ -477,7 +503,8 @@ struct Smem {
   uint64_t* accf;       // [2]
   uint64_t* acce;       // [2]
   uint64_t* cmd;        // [1]
-  uint64_t* wbar;       // [1]
+  uint64_t* wbar;       // [1] W_lo (smem image) landed
+  uint64_t* wready;     // [1] every epilogue warp's share of the TMEM weights stored
   uint32_t* tslot;
   unsigned long long* dbg;  // [64] per-chunk trace stamps (RNNTG_PROF)
 };
@@ -485,6 +512,9 @@ enum { LD_INIT = 0, LD_VISIT, LD_MULTI };  // Epi::run's load modes
 // per-group scalars: FS frame t, FS symbols at t, step s, prediction epoch p, max(out_len), running
 enum { GS_T = 0, GS_SYM, GS_STEP, GS_PE, GS_MAXLEN, GS_RUN, GS_N };
 constexpr int SM_INTS = 5 * MAXG * 32 + 3 * 32 + 16 + GS_N * MAXG;  // 1440: 8-byte aligned end
+// a CTA's control state between step launches: the per-group row state and
+// scalars, then joint_evals / pred_steps / outer_iters (2 ints each), err
+constexpr int CTL_ROWS = 5 * MAXG * 32, CTL_INTS = CTL_ROWS + GS_N * MAXG + 8;
 
 constexpr int XS_FLOATS = 128 * 33;   // epilogue exchange: [128 cols][33] / [4 gates][32][32]
 constexpr int RED_F4 = 256;           // argmax merge / word staging / sumexp group scratch (4 KB)
@@ -522,8 +552,9 @@ __device__ inline Smem carve(unsigned char* raw, int KC) {
   s.acce = s.accf + 2;
   s.cmd = s.acce + 2;
   s.wbar = s.cmd + 1;
-  s.tslot = reinterpret_cast<uint32_t*>(s.wbar + 1);
-  s.dbg = reinterpret_cast<unsigned long long*>(s.wbar + 2);
+  s.wready = s.wbar + 1;
+  s.tslot = reinterpret_cast<uint32_t*>(s.wbar + 2);
+  s.dbg = reinterpret_cast<unsigned long long*>(s.wbar + 3);
   return s;
 }
 
@@ -583,6 +614,35 @@ struct CfgFlags<SPEC_GENERIC> {
   __device__ explicit CfgFlags(const TParams& P) : fs(P.algo == ALGO_FS), tdt(P.algo == ALGO_TDT), lstm(P.cell == 1) {}
 };
 
+// W_hi (and the first W_lo chunks) -> TMEM, each epilogue warp its share of
+// its lane quadrant's columns, then an arrival on wready for the MMA warp.
+template <int BATCH>
+__device__ __forceinline__ void load_tmem_weights(const uint32_t* lo, int KC, uint32_t tq, int et, uint64_t* wready) {
+  const int warp = 2 + (et >> 5), lane = et & 31, q = warp & 3, grp = (warp - 2) >> 2;
+  const int mm = 32 * q + lane;
+  const int ncol = (KC + nlo_chunks(KC)) * 32;  // W_hi pairs, then the TMEM-resident W_lo pairs
+  const int cbeg = grp * (ncol / WPQ), cend = (grp + 1) * (ncol / WPQ);
+  // BATCH columns' loads in flight per batch (a load + store per 8 columns put
+  // one L2 round trip per 8 columns on every step launch's start)
+  for (int c0 = cbeg; c0 < cend; c0 += BATCH) {
+    uint32_t r[BATCH];
+#pragma unroll
+    for (int j = 0; j < BATCH; ++j) r[j] = c0 + j < cend ? __ldg(lo + (size_t)(c0 + j) * 128 + mm) : 0u;
+#pragma unroll
+    for (int j = 0; j < BATCH; j += 8)
+      if (c0 + j < cend) {
+        uint32_t r8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r8[i] = r[j + i];
+        tmem_st8(tq + WLO_COL + c0 + j, r8);
+      }
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  tc_fence_before();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(wready);
+}
+
 template <bool TR, int SPEC>
 struct Epi : CfgFlags<SPEC> {
   using CfgFlags<SPEC>::fs;
@@ -595,6 +655,7 @@ struct Epi : CfgFlags<SPEC> {
   const float wsc;
   const int blank;
   const bool c0;      // the layer-0 cell (I_0): table0[label] + hh0, no weights
+  const bool words_prev;  // step launches with J rotated: step s's words / partials come from the previous launch
   const bool tracer;  // event-trace CTA (single-group decodes only)
   // ---- the current item's group (set_group) ----
   int g = 0, B = 0, row0 = 0;
@@ -610,13 +671,15 @@ struct Epi : CfgFlags<SPEC> {
   int round = 0, err = 0, acc_any = 0;
   float ih[NR];  // I_0: table0[label] rows gathered during the decision
   long long joint_evals = 0, pred_steps = 0, outer_iters = 0;
-  bool finish = false;
+  bool finish = false, frame_end = false;
+  unsigned long long t_entry = 0;  // kernel entry (globaltimer), for STAMPS builds
 
   __device__ Epi(const TParams& P_, const Smem& sm_, uint32_t tmem, int et_, int q, int role_, int layer_,
                  int tile_, float wsc_)
       : CfgFlags<SPEC>(P_), P(P_), sm(sm_), tq(tmem + ((uint32_t)(32 * q) << 16)), et(et_), m(32 * q + (et_ & 31)),
         r0(NR * (et_ >> 7)), role(role_),
         layer(layer_), tile(tile_), wsc(wsc_), blank(P_.V1 - 1), c0(role_ == ROLE_I && layer_ == 0),
+        words_prev(P_.step_mode == STEP_ONE && STEP_JROT),
         tracer(PPROF(P_) && P_.ngrp == 1 && (int)blockIdx.x == P_.prof_first[role_]) {}
 
   __device__ __forceinline__ int& gsc(int which) const { return sm.grp[which * MAXG + g]; }
@@ -696,6 +759,24 @@ struct Epi : CfgFlags<SPEC> {
       for (int k = 0; k < KC && k < 10; ++k)  // chunk landed (observer warp)
         PPROF(P)[(size_t)(ev0 + 25 + k) * PROF_WIN + (s - PROF_S0)] = t[32 + k];
     }
+  }
+  // W_hi (and the first W_lo chunks) -> TMEM, each epilogue warp its share of
+  // its lane quadrant's columns, then wready for the MMA warp.  Done lazily
+  // before the first round: with step launches a CTA's decision and the
+  // weight-free I_0 chain run before the weight traffic (the whole model,
+  // every launch) competes for L2.
+  bool wloaded = false;
+#ifndef WEAGER
+#define WEAGER 0  // A/B: step launches load the TMEM weights before their decision
+#endif
+#ifndef WBATCH
+#define WBATCH 16  // loads in flight per epilogue thread (32: register spills in the product kernels)
+#endif
+  __device__ __forceinline__ void load_weights() {
+    wloaded = true;
+    const int in_buf = role == ROLE_J ? TRUNK : role == ROLE_P ? P.L - 1 : role == ROLE_R ? layer : max(layer - 1, 0);
+    load_tmem_weights<WBATCH>(reinterpret_cast<const uint32_t*>(P.wimg + (size_t)blockIdx.x * P.wstride + P.wtoff),
+                      P.act_kc[in_buf], tq, et, sm.wready);
   }
   // one load+MMA round on this CTA's input: group g, epoch e (-1 = exit)
   __device__ __forceinline__ void post(int e) {
@@ -979,7 +1060,9 @@ struct Epi : CfgFlags<SPEC> {
         // spin on one word (tile NJ-1) with a single load in flight, then read
         // the rest once (warp-wide strong loads are serviced ~100 cycles apart:
         // a 9-16 load batch per poll made each poll ~1 us; one load is ~360 cycles)
-        while ((unsigned)(ld_poll_u64(wv + (nj - 1) * 32) >> 32 & 0xffu) != tg) ++npoll;
+        // (step launches: J wrote step s's words in the previous launch)
+        if (!words_prev)
+          while ((unsigned)(ld_poll_u64(wv + (nj - 1) * 32) >> 32 & 0xffu) != tg) ++npoll;
         if (c0 && b == 0) mark(30);  // last tile's word seen
         do {
           ++npoll;
@@ -1039,7 +1122,7 @@ struct Epi : CfgFlags<SPEC> {
       }
       float v = 0.0f;
       if (emitter) {
-        if (b == 0) spin_geq(cnt + (size_t)cidx_part() * CSTRIDE, (unsigned)P.NJ * (unsigned)(s + 1));
+        if (b == 0 && !words_prev) spin_geq(cnt + (size_t)cidx_part() * CSTRIDE, (unsigned)P.NJ * (unsigned)(s + 1));
         __syncwarp();
         if (valid) {
           float Mx = -INFINITY, Sx = 0.0f;
@@ -1152,6 +1235,7 @@ struct Epi : CfgFlags<SPEC> {
     const int o = sm.misc[5];
     acc_any = o & 1;
     finish = (o >> 1) & 1;
+    frame_end = (o >> 2) & 1;
     if (o & 4) ++outer_iters;
     ++joint_evals;
     if (s + 1 > P.max_iters) err = ERR_RUNAWAY;
@@ -1168,55 +1252,134 @@ struct Epi : CfgFlags<SPEC> {
   // groups only).
   template <typename Pred, typename Idle, typename Load, typename Save>
   __device__ void run(Pred&& pred, Idle&& idle, Load&& load, Save&& save) {
-    const bool multi = P.ngrp > 1;
-    for (int gg = 0; gg < P.ngrp; ++gg) {
-      set_group(gg);
-      init_rows();
-      load(LD_INIT);
-      pred(0LL);
-      ++pred_steps;
-      int live = et < B ? !(flag[et] & 1) : 0;
-      live = epi_or(live);
-      const bool running0 = fs ? (maxlen > 0) : (live != 0);
-      if (et < 32) flag[et] &= ~2;
-      if (et == 0) gsc(GS_RUN) = running0 ? 1 : 0;
-      if (multi) save();
-      save_group();
-      epi_sync();
-    }
-    for (;;) {
-      bool any = false;
+    const int mode = P.step_mode;
+    // with several groups or step launches, the per-thread state of a group
+    // lives in global memory between its visits
+    const bool multi = P.ngrp > 1 || mode != STEP_NONE;
+    int sslot = 0;
+    // the TMEM weights before the first round: at the start of a whole-decode
+    // or P0 launch; in a step launch after its first decision (the decision
+    // and the weight-free I_0 chain go first, before the weight traffic)
+    const bool has_w = !(role == ROLE_E || c0);
+    // the first MMAs after the decision (I_1 and R_0 on h0) load theirs before it
+    if (has_w && (WEAGER || (role == ROLE_I && layer == 1) || (role == ROLE_R && layer == 0))) load_weights();
+    if (mode == STEP_ONE) {
+      load_ctl();
+      sslot = sm.grp[GS_STEP * MAXG];
+      if (et == 0) {
+        stamp_at(P, sslot, 0, t_entry);
+        stamp(P, sslot, 2);
+      }
+    } else {
+      if (has_w && !wloaded) load_weights();
       for (int gg = 0; gg < P.ngrp; ++gg) {
-        if (!sm.grp[GS_RUN * MAXG + gg]) continue;
-        any = true;
         set_group(gg);
-        load(multi ? LD_MULTI : LD_VISIT);
-        if (role == ROLE_J) joint_round();
-        decide();
-        if (finish) {
-          if (et == 0) gsc(GS_RUN) = 0;
-          epi_sync();
-          continue;
-        }
-        if (acc_any) {
-          ++p;
-          pred(s + 1);
-          ++pred_steps;
-          if (!fs) ++outer_iters;
-        } else {
-          idle(s + 1);
-        }
-        if (multi) save();
-        // this CTA is done with step s's words: ack (slot reuse, joint_round).
-        // A per-CTA word; the reads it covers were consumed before the barrier
-        // that precedes it, so it needs no release.
-        if (et == 0) st_relaxed_u32(P.ack + (size_t)g * P.G + blockIdx.x, (unsigned)(s + 1));
-        ++s;
+        init_rows();
+        load(LD_INIT);
+        pred(0LL);
+        ++pred_steps;
+        int live = et < B ? !(flag[et] & 1) : 0;
+        live = epi_or(live);
+        const bool running0 = fs ? (maxlen > 0) : (live != 0);
         if (et < 32) flag[et] &= ~2;
+        if (et == 0) gsc(GS_RUN) = running0 ? 1 : 0;
+        if (multi) save();
+        if (role == ROLE_J && mode == STEP_INIT && running0 && STEP_JROT) joint_round();  // step 0's joint
         save_group();
         epi_sync();
       }
-      if (!any) break;
+    }
+    bool acc_round = false, fend_round = false;
+    if (mode != STEP_INIT) {
+      for (;;) {
+        bool any = false;
+        for (int gg = 0; gg < P.ngrp; ++gg) {
+          if (!sm.grp[GS_RUN * MAXG + gg]) continue;
+          any = true;
+          set_group(gg);
+          load(multi ? LD_MULTI : LD_VISIT);
+          if (et == 0 && gg == 0) stamp(P, sslot, 3);
+          // step launches run J at the END of a visit (the next step's joint,
+          // so J's weight load overlaps the decision + prediction chain)
+          if (role == ROLE_J && (mode == STEP_NONE || !STEP_JROT)) joint_round();
+          decide();
+          if (has_w && !wloaded) load_weights();
+          if (et == 0 && gg == 0) stamp(P, sslot, 4);
+          fend_round |= frame_end;
+          if (finish) {
+            if (et == 0) gsc(GS_RUN) = 0;
+            epi_sync();
+            continue;
+          }
+          acc_round |= acc_any != 0;
+          if (acc_any) {
+            ++p;
+            pred(s + 1);
+            ++pred_steps;
+            if (!fs) ++outer_iters;
+          } else {
+            idle(s + 1);
+          }
+          if (et == 0 && gg == 0) stamp(P, sslot, 5);
+          if (multi) save();
+          // this CTA is done with step s's words: ack (slot reuse, joint_round).
+          // A per-CTA word; the reads it covers were consumed before the barrier
+          // that precedes it, so it needs no release.
+          if (et == 0) st_relaxed_u32(P.ack + (size_t)g * P.G + blockIdx.x, (unsigned)(s + 1));
+          ++s;
+          if (et < 32) flag[et] &= ~2;
+          if (role == ROLE_J && mode == STEP_ONE && STEP_JROT) joint_round();  // step s + 1's joint
+          if (et == 0 && gg == 0) stamp(P, sslot, 6);
+          save_group();
+          epi_sync();
+        }
+        if (!any || mode == STEP_ONE) break;
+      }
+    }
+    if (mode != STEP_NONE) {
+      // step launches: keep the control state for the next launch, and set
+      // the loop flags (frame-looping: the inner WHILE runs a frame's
+      // symbols; label-looping: the inner WHILE skips blanks until a row
+      // accepts; the outer WHILE runs while any group is live)
+      save_ctl();
+      if (et == 0) stamp(P, sslot, 7);
+      if (blockIdx.x == 0 && et == 0) {
+        int run_any = 0;
+        for (int gg = 0; gg < P.ngrp; ++gg) run_any |= sm.grp[GS_RUN * MAXG + gg];
+        const bool inner = run_any && (fs ? !fend_round : !acc_round);
+        P.ctrl->any = run_any;
+        P.ctrl->abort = inner ? 1 : 0;  // host loop: the inner loop continues
+        if (P.use_cond) {
+          cudaGraphSetConditional(P.h_inner, inner ? 1u : 0u);
+          cudaGraphSetConditional(P.h_outer, run_any ? 1u : 0u);
+        }
+      }
+    }
+  }
+
+  // control state of this CTA <-> its global block (step launches)
+  __device__ void load_ctl() {
+    const int* c = P.ctl + (size_t)blockIdx.x * CTL_INTS;
+    for (int i = et; i < CTL_ROWS; i += NEPI) sm.label[i] = c[i];  // label, flag, tb, ub, cnt: contiguous
+    for (int i = et; i < GS_N * MAXG; i += NEPI) sm.grp[i] = c[CTL_ROWS + i];
+    const long long* cc = reinterpret_cast<const long long*>(c + CTL_ROWS + GS_N * MAXG);
+    joint_evals = cc[0];
+    pred_steps = cc[1];
+    outer_iters = cc[2];
+    err = c[CTL_ROWS + GS_N * MAXG + 6];
+    epi_sync();
+  }
+  __device__ void save_ctl() {
+    epi_sync();
+    int* c = P.ctl + (size_t)blockIdx.x * CTL_INTS;
+    for (int i = et; i < CTL_ROWS; i += NEPI) c[i] = sm.label[i];
+    for (int i = et; i < GS_N * MAXG; i += NEPI) c[CTL_ROWS + i] = sm.grp[i];
+    if (et == 0) {
+      long long* cc = reinterpret_cast<long long*>(c + CTL_ROWS + GS_N * MAXG);
+      cc[0] = joint_evals;
+      cc[1] = pred_steps;
+      cc[2] = outer_iters;
+      c[CTL_ROWS + GS_N * MAXG + 6] = err;
     }
   }
 
@@ -1400,7 +1563,8 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
     // hh_l(pe) (R_l's output) -> x; zero for P0
     auto load_hh = [&](int pe, float (&x)[NR]) {
       if (pe > 0) {
-        wait_counter(cidx_hh(layer, tile), (unsigned)pe);
+        // (step launches: R_l wrote hh_l(pe) in an earlier launch, ordered by the kernel boundary)
+        if (P.step_mode != STEP_ONE) wait_counter(cidx_hh(layer, tile), (unsigned)pe);
         const float* hb = P.hh[layer] + ((size_t)(2 * g + (pe & 1)) * 64 + tile) * 32 * 128;
 #pragma unroll
         for (int i = 0; i < NR; ++i) x[i] = __ldcg(&hb[(r0 + i) * 128 + m]);
@@ -1537,6 +1701,8 @@ __device__ __forceinline__ void mma_round(const TParams& P, const Smem& sm, uint
 template <bool TR, int SPEC>
 __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constant__ TParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned long long t_entry = 0;
+  if (STAMPS && threadIdx.x == 64) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
   const int4 rl = P.roles[blockIdx.x];
   const int role = rl.x, layer = rl.y, tile = rl.z;
   const float wsc = __int_as_float(rl.w);
@@ -1559,6 +1725,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
     }
     mbar_init(sm.cmd, 1);
     mbar_init(sm.wbar, 1);
+    mbar_init(sm.wready, NEPI / 32);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -1573,29 +1740,18 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
   const unsigned char* wimg = P.wimg + (size_t)blockIdx.x * P.wstride;
 
   // ---- resident weights: W_hi -> smem (bulk copies), W_lo -> TMEM ----
+#ifndef XP_NOWLO
+#define XP_NOWLO 0  // timing experiments only (wrong results): skip the smem weight copy
+#endif
+#ifndef XP_NOWHI
+#define XP_NOWHI 0  // timing experiments only: skip the TMEM weight load
+#endif
   if (tid == 0) {
-    const uint32_t bytes = (uint32_t)KC * 16384;
+    const uint32_t bytes = XP_NOWLO ? 0u : (uint32_t)KC * 16384;
     mbar_arrive_expect_tx(sm.wbar, bytes);
     for (uint32_t o = 0; o < bytes; o += 32768)
       bulk_g2s(sm.whi + o, wimg + o, bytes - o < 32768 ? bytes - o : 32768, sm.wbar);
   }
-  if (warp >= 2) {
-    const int q = warp & 3, grp = (warp - 2) >> 2;  // WPQ warps share a lane quadrant
-    const uint32_t* lo = reinterpret_cast<const uint32_t*>(wimg + P.wtoff);
-    const int m = 32 * q + lane;
-    const int ncol = (KC + nlo_chunks(KC)) * 32;  // W_hi pairs, then the TMEM-resident W_lo pairs
-    for (int c0 = grp * (ncol / WPQ); c0 < (grp + 1) * (ncol / WPQ); c0 += 8) {
-      uint32_t r[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = __ldg(lo + (size_t)(c0 + j) * 128 + m);
-      tmem_st8(tmem + ((uint32_t)(32 * q) << 16) + WLO_COL + c0, r);
-    }
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-  }
-  mbar_wait(sm.wbar, 0);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
 
   if (warp == 0) {
     // ================= producer (converged warp): stream input chunks into the ring =================
@@ -1672,6 +1828,11 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
       mbar_wait(sm.cmd, r & 1);
       const int e = ((volatile int*)sm.misc)[r & 1];
       if (e < 0) break;
+      if (r == 0) {  // the weights, before the first MMA
+        mbar_wait(sm.wbar, 0);    // W_lo smem image
+        mbar_wait(sm.wready, 0);  // TMEM weights (the epilogue's first post)
+        tc_fence_after();
+      }
       const int set = 0;
       if (r >= 1) mbar_wait(&sm.acce[0], (uint32_t)((r - 1) & 1));  // the epilogue read the last round
       tc_fence_after();
@@ -1693,6 +1854,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
   } else {
     // ================= epilogue + replicated control (128 threads) =================
     Epi<TR, SPEC> e(P, sm, tmem, tid - 64, warp & 3, role, layer, tile, wsc);
+    e.t_entry = t_entry;
     e.run_role();
   }
   tc_fence_before();

@@ -111,6 +111,10 @@ struct rnntg_decoder {
   size_t psmem = 0;
   // tensor-core persistent executor
   ptc::TParams tp{};
+  // graph / host-loop executors on the tensor-core step kernel: the init and
+  // one-step launch parameters (tp with step_mode STEP_INIT / STEP_ONE)
+  bool tc_steps = false;
+  ptc::TParams tp_step[2]{};
   size_t tsmem = 0;
   unsigned* tcnt = nullptr;
   size_t tcnt_bytes = 0, tpw_bytes = 0;
@@ -733,6 +737,7 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   tp.ctrl = d->st.ctrl;
   for (int r = 0; r < ptc::NROLES; ++r) tp.prof_first[r] = -1;
   for (int c = G - 1; c >= 0; --c) tp.prof_first[roles[c].x] = c;
+  if (env_flag("RNNTG_STAMPS", false)) CK(d->mem.alloc(&tp.stamps, (size_t)64 * G * 16));
   if (env_flag("RNNTG_PROF", false)) {
     CK(d->mem.alloc(&tp.prof, (size_t)(2 * ptc::NEV + G) * ptc::PROF_WIN));
   }
@@ -750,6 +755,97 @@ cudaError_t launch_tc(rnntg_decoder* d, cudaStream_t st) {
   const void* k = tc_kernel_for(d->tp.algo, d->tp.cell, d->tp.prof != nullptr);
   return cudaLaunchCooperativeKernel(k, dim3(d->tp.G), dim3(ptc::NTH), args,
                                      d->tsmem, st);
+}
+
+// ---------------------------------------------------------------- K6 step launches
+// The graph and host-loop executors run the tensor-core kernel one decision
+// per launch (STEP_ONE) after one P0 launch (STEP_INIT): the same role CTAs
+// and arithmetic as K6, with the replicated control state and the
+// per-thread cell / gp state kept in global memory between launches, and
+// the loop flags set from the device (cudaGraphSetConditional) or read back
+// by the host loop.
+rnntg_status setup_tc_steps(rnntg_decoder* d, bool use_cond) {
+  rnntg_status st = setup_tc(d);
+  if (st) return st;
+  ptc::TParams& tp = d->tp;
+  CK(d->mem.alloc(&tp.ctl, (size_t)tp.G * ptc::CTL_INTS));
+  if (!tp.gst) CK(d->mem.alloc(&tp.gst, (size_t)tp.ngrp * tp.G * ptc::NSV * ptc::NEPI));
+  for (int i = 0; i < 2; ++i) {
+    d->tp_step[i] = tp;
+    d->tp_step[i].step_mode = i == 0 ? ptc::STEP_INIT : ptc::STEP_ONE;
+    d->tp_step[i].use_cond = use_cond ? 1 : 0;
+  }
+  d->tc_steps = true;
+  return RNNTG_OK;
+}
+
+cudaError_t coop_node(cudaGraphNode_t n) {
+  // (RNNTG_GRAPH_COOP=0: plain kernel nodes -- every CTA is resident anyway,
+  // one per SM, G <= SMs, and the graph runs its nodes in order)
+  if (!env_flag("RNNTG_GRAPH_COOP", true)) return cudaSuccess;
+  cudaLaunchAttributeValue v{};
+  v.cooperative = 1;
+  return cudaGraphKernelNodeSetAttribute(n, cudaLaunchAttributeCooperative, &v);
+}
+
+cudaError_t memset_node(Builder& b, void* dst, size_t bytes) {
+  cudaMemsetParams p{};
+  p.dst = dst;
+  p.value = 0;
+  p.elementSize = 4;
+  p.width = bytes / 4;
+  p.height = 1;
+  cudaGraphNode_t n;
+  cudaError_t e = cudaGraphAddMemsetNode(&n, b.g, b.last ? &b.last : nullptr, b.last ? 1 : 0, &p);
+  if (e != cudaSuccess) return e;
+  b.last = n;
+  b.last_kernel = false;
+  return cudaSuccess;
+}
+
+// graph: counters/words reset -> K1 -> P0 launch ->
+//   WHILE any live { step ; WHILE inner { step } }
+// (frame-looping: the inner WHILE runs the rest of a frame's symbols;
+// label-looping: it runs the blank-skipping joint steps until a row accepts)
+cudaError_t build_graph_tc(rnntg_decoder* d) {
+  cudaError_t e;
+  if ((e = cudaGraphCreate(&d->graph, 0)) != cudaSuccess) return e;
+  cudaGraphConditionalHandle ho, hi;
+  if ((e = cudaGraphConditionalHandleCreate(&ho, d->graph, 0, 0)) != cudaSuccess) return e;
+  if ((e = cudaGraphConditionalHandleCreate(&hi, d->graph, 0, 0)) != cudaSuccess) return e;
+  for (int i = 0; i < 2; ++i) {
+    d->tp_step[i].h_outer = ho;
+    d->tp_step[i].h_inner = hi;
+  }
+  const void* k = tc_kernel_for(d->algo, d->m->dm.cell, false);
+  void* a_init[1] = {&d->tp_step[0]};
+  void* a_step[1] = {&d->tp_step[1]};
+  const dim3 grid(d->tp.G), block(ptc::NTH);
+  Builder root{d->graph};
+  root.pdl = false;  // the step kernel does not wait on griddepcontrol
+  if ((e = memset_node(root, d->tcnt, d->tcnt_bytes)) != cudaSuccess) return e;
+  if ((e = memset_node(root, d->tp.pw, d->tpw_bytes)) != cudaSuccess) return e;
+  if ((e = add_encproj(root, d)) != cudaSuccess) return e;
+  if ((e = root.kernel(k, grid, block, d->tsmem, a_init)) != cudaSuccess) return e;
+  if ((e = coop_node(root.last)) != cudaSuccess) return e;
+  cudaGraph_t outer_body, inner_body;
+  if ((e = root.while_node(ho, &outer_body)) != cudaSuccess) return e;
+  Builder ob{outer_body};
+  ob.pdl = false;
+  if ((e = ob.kernel(k, grid, block, d->tsmem, a_step)) != cudaSuccess) return e;
+  if ((e = coop_node(ob.last)) != cudaSuccess) return e;
+  if ((e = ob.while_node(hi, &inner_body)) != cudaSuccess) return e;
+  Builder ib{inner_body};
+  ib.pdl = false;
+  if ((e = ib.kernel(k, grid, block, d->tsmem, a_step)) != cudaSuccess) return e;
+  if ((e = coop_node(ib.last)) != cudaSuccess) return e;
+  return cudaGraphInstantiate(&d->gexec, d->graph, 0);
+}
+
+cudaError_t launch_tc_step(rnntg_decoder* d, int i) {
+  void* args[1] = {&d->tp_step[i]};
+  return cudaLaunchCooperativeKernel(tc_kernel_for(d->algo, d->m->dm.cell, false), dim3(d->tp.G), dim3(ptc::NTH),
+                                     args, d->tsmem, d->stream);
 }
 
 // ---------------------------------------------------------------- host loop
@@ -819,6 +915,33 @@ rnntg_status run_hostloop(rnntg_decoder* d) {
       CK(pred());  // acceptors' prediction step + round tail (sets `any`)
       CK(flags());
     }
+  }
+  return RNNTG_OK;
+}
+
+// The sync-requiring baseline on the tensor-core step kernel: the same
+// launches as the graph executor's loop bodies, issued by the host, with the
+// loop flags copied back and synchronised after every step.
+rnntg_status run_hostloop_tc(rnntg_decoder* d) {
+  cudaStream_t st = d->stream;
+  Ctrl* hc = d->hctrl;
+  auto flags = [&]() -> cudaError_t {
+    ++d->n_syncs;
+    cudaError_t e = cudaMemcpyAsync(hc, d->st.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(st);
+  };
+  CK(cudaMemsetAsync(d->tcnt, 0, d->tcnt_bytes, st));
+  CK(cudaMemsetAsync(d->tp.pw, 0, d->tpw_bytes, st));
+  CK(encproj_launch(d->enc, st));
+  CK(launch_tc_step(d, 0));  // P0
+  d->n_launches += 2;
+  CK(flags());
+  while (hc->any && !hc->err) {
+    do {  // inner: frame-looping -- the frame's symbols; label-looping -- blank skipping
+      CK(launch_tc_step(d, 1));
+      ++d->n_launches;
+      CK(flags());
+    } while (hc->any && hc->abort && !hc->err);
   }
   return RNNTG_OK;
 }
@@ -1130,7 +1253,7 @@ rnntg_status rnntg_decoder_create(rnntg_model* m, int algo, int exec, int batch,
   if (algo < 0 || algo > 2) return fail(RNNTG_E_VALUE, "unknown algo");
   if (algo == RNNTG_ALGO_TDT_LABEL_LOOP && m->dm.D == 0)
     return fail(RNNTG_E_STATE, "duration-head decoding needs a model with a duration head");
-  if (exec < RNNTG_EXEC_GRAPH || exec > RNNTG_EXEC_HOSTLOOP)
+  if (exec < RNNTG_EXEC_GRAPH || exec > RNNTG_EXEC_GRAPH_FFMA)
     return fail(RNNTG_E_VALUE, "unknown exec mode");
   CK(cudaSetDevice(m->device));
   if (exec == RNNTG_EXEC_TENSOR && batch > ptc::MAXB * ptc::MAXG && m->dm.cell != RNNTG_CELL_SCRIPTED) {
@@ -1186,14 +1309,20 @@ rnntg_status rnntg_decoder_create(rnntg_model* m, int algo, int exec, int batch,
         (e = cudaEventCreate(&d->ev1)) == cudaSuccess) {
       d->st.x = d->x_dev;
       d->st.out_len = d->len_dev;
-      if (m->dm.cell == RNNTG_CELL_SCRIPTED && exec != RNNTG_EXEC_GRAPH && exec != RNNTG_EXEC_HOSTLOOP)
+      if (m->dm.cell == RNNTG_CELL_SCRIPTED && exec != RNNTG_EXEC_GRAPH && exec != RNNTG_EXEC_HOSTLOOP &&
+          exec != RNNTG_EXEC_GRAPH_FFMA)
         st = fail(RNNTG_E_VALUE, "scripted models run on the graph or host-loop executor");
       else if (m->dm.cell != RNNTG_CELL_SCRIPTED &&
                !encproj_plan(d->enc, m->dm, d->x_dev, d->st.fp, batch * max_frames))
         st = fail(RNNTG_E_CUDA, "cannot encode TMA tensor maps for the encoder projection");
-      else if (exec == RNNTG_EXEC_GRAPH) e = build_graph(d);
+      else if (exec == RNNTG_EXEC_GRAPH || exec == RNNTG_EXEC_HOSTLOOP) {
+        // the tensor-core step kernel when the shape fits it; else the FFMA step kernels
+        const bool tc = m->dm.cell != RNNTG_CELL_SCRIPTED && env_flag("RNNTG_TC_STEPS", true) &&
+                        setup_tc_steps(d, exec == RNNTG_EXEC_GRAPH) == RNNTG_OK;
+        if (exec == RNNTG_EXEC_HOSTLOOP) e = cudaMallocHost(&d->hctrl, sizeof(Ctrl));
+        else e = tc ? build_graph_tc(d) : build_graph(d);
+      } else if (exec == RNNTG_EXEC_GRAPH_FFMA) e = build_graph(d);
       else if (exec == RNNTG_EXEC_TENSOR) st = setup_tc(d);
-      else if (exec == RNNTG_EXEC_HOSTLOOP) e = cudaMallocHost(&d->hctrl, sizeof(Ctrl));
       else st = setup_persistent(d);
     }
   }
@@ -1330,7 +1459,7 @@ rnntg_status rnntg_launch(rnntg_decoder* d) {
   CK(cudaEventRecord(d->ev0, d->stream));
   d->n_syncs = d->n_graph_launches = 0;
   d->n_launches = d->exec == RNNTG_EXEC_PERSISTENT || d->exec == RNNTG_EXEC_TENSOR ? 2 : 0;
-  if (d->exec == RNNTG_EXEC_GRAPH) d->n_launches = d->n_graph_launches = 1;
+  if (d->exec == RNNTG_EXEC_GRAPH || d->exec == RNNTG_EXEC_GRAPH_FFMA) d->n_launches = d->n_graph_launches = 1;
   if (d->exec == RNNTG_EXEC_PERSISTENT || d->exec == RNNTG_EXEC_TENSOR) {
     if (d->lexec) {
       CK(cudaGraphLaunch(d->lexec, d->stream));
@@ -1340,7 +1469,7 @@ rnntg_status rnntg_launch(rnntg_decoder* d) {
       CK(issue_persistent(d, d->stream));
     }
   } else if (d->exec == RNNTG_EXEC_HOSTLOOP) {
-    const rnntg_status st = run_hostloop(d);
+    const rnntg_status st = d->tc_steps ? run_hostloop_tc(d) : run_hostloop(d);
     if (st) return st;
   } else {
     CK(cudaGraphLaunch(d->gexec, d->stream));
@@ -1628,9 +1757,14 @@ rnntg_status rnntg_time_kernel(rnntg_decoder* d, int which, int reps, float* avg
 rnntg_status rnntg_debug_trace(rnntg_decoder* d, unsigned long long* out, int n) {
   if (!d || !out) return fail(RNNTG_E_VALUE, "bad arguments");
   if (!d->subs.empty()) return rnntg_debug_trace(d->subs[0], out, n);  // first sub-batch
+  CK(cudaStreamSynchronize(d->stream));
+  if (d->tp.stamps) {  // RNNTG_STAMPS=1 (STAMPS builds): [64 step slots][G][16] globaltimer stamps
+    const int tot = 64 * d->tp.G * 16;
+    CK(cudaMemcpy(out, d->tp.stamps, sizeof(unsigned long long) * std::min(n, tot), cudaMemcpyDeviceToHost));
+    return RNNTG_OK;
+  }
   if (d->exec != RNNTG_EXEC_TENSOR || !d->tp.prof)
     return fail(RNNTG_E_STATE, "tracing needs the tensor executor and RNNTG_PROF=1");
-  CK(cudaStreamSynchronize(d->stream));
   const int tot = (2 * ptc::NEV + d->tp.G) * ptc::PROF_WIN;
   CK(cudaMemcpy(out, d->tp.prof, sizeof(unsigned long long) * std::min(n, tot), cudaMemcpyDeviceToHost));
   return RNNTG_OK;

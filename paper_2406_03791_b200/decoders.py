@@ -36,10 +36,11 @@ class DecodeAlgo(enum.IntEnum):
 
 
 class Exec(enum.IntEnum):
-    Graph = 0        # CUDA graph with nested conditional WHILE nodes
+    Graph = 0        # CUDA graph with nested conditional WHILE nodes (tcgen05 step kernel bodies)
     Persistent = 1   # persistent kernel alternative (FFMA, shared-memory weights)
     Tensor = 2       # persistent kernel on tcgen05 tensor cores, role-specialised CTAs
     HostLoop = 3     # sync-requiring baseline: same kernels, host loop with a flag sync per step
+    GraphFFMA = 4    # CUDA graph over the FFMA step kernels (4 nodes per inner step)
 
 
 @dataclass

@@ -89,7 +89,7 @@ def test_oracle_reproduces_fixture_utterance(name):
 
 
 # ------------------------------------------------------------------ GPU parity
-EXECS = ["Tensor", "Graph", "Persistent", "HostLoop"]
+EXECS = ["Tensor", "Graph", "Persistent", "HostLoop", "GraphFFMA"]
 
 
 @pytest.mark.gpu

@@ -38,7 +38,7 @@ def golden():
         return json.load(fh)
 
 
-EXECS = [D.Exec.Graph, D.Exec.Persistent, D.Exec.Tensor, D.Exec.HostLoop]
+EXECS = [D.Exec.Graph, D.Exec.Persistent, D.Exec.Tensor, D.Exec.HostLoop, D.Exec.GraphFFMA]
 
 
 def run_case(seed, tdt, algo, report, exec=D.Exec.Graph):

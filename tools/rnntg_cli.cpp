@@ -216,6 +216,7 @@ rnntg_exec parse_exec(const std::string& s) {
   if (s == "persistent") return RNNTG_EXEC_PERSISTENT;
   if (s == "graph") return RNNTG_EXEC_GRAPH;
   if (s == "hostloop") return RNNTG_EXEC_HOSTLOOP;
+  if (s == "graph-ffma") return RNNTG_EXEC_GRAPH_FFMA;
   throw ValueError("exec must be tensor, persistent, graph or hostloop");
 }
 
