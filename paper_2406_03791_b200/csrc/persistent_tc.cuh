@@ -337,14 +337,18 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
 // MM_PROD / MM_CONS select the producer / consumer halves (A/B):
 //   MM_PROD 0 none (round 1: relied on L2 behaviour outside the model),
 //           1 fence.proxy.async.global + fence.acq_rel.gpu + relaxed adds,
-//           2 fence.proxy.async.global + red.release.gpu;
+//           2 fence.proxy.async.global + red.release.gpu,
+//           3 fence.acq_rel.gpu only,
+//           4 fence.proxy.async.global + fence.release.gpu + relaxed adds
+//             (MEMBAR.ALL.GPU alone; acq_rel adds ERRBAR, CGAERRBAR, CCTL.IVALL);
 //   MM_CONS 0 none, 1 relaxed spin + fence.acq_rel.gpu,
-//           2 acquire polls, 3 relaxed spin + one ld.acquire re-read.
+//           2 acquire polls, 3 relaxed spin + one ld.acquire re-read,
+//           4 relaxed spin + fence.acquire.gpu (CCTL.IVALL alone: no second L2 round trip).
 #ifndef MM_PROD
-#define MM_PROD 1
+#define MM_PROD 4
 #endif
 #ifndef MM_CONS
-#define MM_CONS 3
+#define MM_CONS 4
 #endif
 // one counter poll (the consumer's strong read)
 __device__ __forceinline__ unsigned ld_poll_cnt(const unsigned* p) {
@@ -356,6 +360,7 @@ __device__ __forceinline__ unsigned ld_poll_cnt(const unsigned* p) {
 // after a successful relaxed poll of p
 __device__ __forceinline__ void acquire_after(const unsigned* p) {
   if (MM_CONS == 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  if (MM_CONS == 4) asm volatile("fence.acquire.gpu;" ::: "memory");
   if (MM_CONS == 3) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -367,8 +372,15 @@ __device__ __forceinline__ void spin_geq(const unsigned* p, unsigned target) {
   }
   acquire_after(p);
 }
+// release pattern: fence.release.gpu (MEMBAR.ALL.GPU) + relaxed add; red.release
+// compiles to MEMBAR + ERRBAR + CGAERRBAR + RED
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  if (MM_PROD == 4) {
+    asm volatile("fence.release.gpu;" ::: "memory");
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  } else {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  }
 }
 __device__ __forceinline__ void fence_proxy_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -454,8 +466,9 @@ __device__ __forceinline__ void red_relaxed_add(unsigned* p, unsigned v) {
 // after bulk_commit_wait_all(): the completed bulk-store writes, ordered into
 // the generic proxy, then released at gpu scope before the counter adds
 __device__ __forceinline__ void release_after_bulk() {
-  if (MM_PROD == 1 || MM_PROD == 2) asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (MM_PROD == 1 || MM_PROD == 2 || MM_PROD == 4) asm volatile("fence.proxy.async.global;" ::: "memory");
   if (MM_PROD == 1 || MM_PROD == 3) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  if (MM_PROD == 4) asm volatile("fence.release.gpu;" ::: "memory");
 }
 #ifndef PUB_ET
 #define PUB_ET 0  // epilogue thread that issues the activation bulk stores + publish
@@ -1790,6 +1803,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
         // relaxed counter reads + a fence / acquire re-read (warp-synchronised:
         // any lane may issue the loads below): the acquire pattern
         if (MM_CONS == 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (MM_CONS == 4) asm volatile("fence.acquire.gpu;" ::: "memory");
         if (MM_CONS == 3) {
           if (lane >= next && lane < ready) acquire_after(mycnt);
           __syncwarp();
