@@ -260,15 +260,19 @@ def run_reference_arm(args, cfg, rank, world):
     print(json.dumps(out), flush=True)
 
 
-def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent):
+def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent, step_ms=None):
     """Dominant kernel's achieved bandwidth / FLOP rate, measured with CUDA
-    events on standalone launches of the decoder's own kernels."""
+    events on standalone launches of the decoder's own kernels (step_ms: the
+    tcgen05 step kernel's mean launch time from the CUPTI trace, for the graph
+    / host-loop executors)."""
     from paper_2406_03791_b200._lib import check
     algo, B, T, ms, durs, L, H, J, V, F, scaling = cfg
     kern = {}
     names = {0: "enc_proj"}
     if persistent:
         names[10] = "persistent"
+    elif step_ms is not None:
+        kern["ptc_step"] = step_ms
     else:
         names.update({1: "pred_layer0", 2: "pred_layer1", 8: "pred_proj", 9: "joint"})
     for w, n in names.items():
@@ -280,11 +284,10 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent):
     Hp = (H + 63) // 64 * 64
     Jp = (J + 63) // 64 * 64
     Bp = (Bl + 31) // 32 * 32
-    # the tensor executor runs B > 32 as ceil(B / 32) balanced sub-decodes back to
-    # back (one persistent launch each; stats are summed over them, and
-    # rnntg_time_kernel times one of them): count per launch at the sub-batch size
-    n_sub = (Bl + 31) // 32 if (persistent and args.exec == "tensor" and Bl > 32) else 1
-    Brow = Bl / n_sub
+    # the tensor executor decodes up to 256 rows in one kernel as <= 32-row
+    # groups (stats count group-steps); beyond 256 as sub-decodes back to back
+    n_sub = (Bl + 255) // 256 if (persistent and args.exec == "tensor" and Bl > 256) else 1
+    Brow = min(Bl, 32)
     V1 = V + 1
     V1p = (V1 + 15) // 16 * 16
     Dn = len(durs)
@@ -298,6 +301,7 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent):
         "joint": 4 * (Jp * V1p + 2 * Bp * Jp),
         "enc_proj": 4 * (Bl * T * F + F * Jp + Bl * T * Jp),
         "persistent": (st.pred_steps * pred_w + st.joint_evals * joint_w) / n_sub,
+        "ptc_step": (st.pred_steps * pred_w + st.joint_evals * joint_w) / max(st.joint_evals, 1),
     }
     pred_f = 2 * Brow * (4 * H * H * (2 * L - 1) + H * J)
     joint_f = 2 * Brow * J * (V1 + Dn)
@@ -305,10 +309,12 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent):
         "pred_layer1": 2 * Bl * 2 * H * 4 * H, "pred_layer0": 2 * Bl * H * 4 * H,
         "pred_proj": 2 * Bl * H * J, "joint": 2 * Bl * J * V1, "enc_proj": 2 * Bl * T * F * J,
         "persistent": (st.pred_steps * pred_f + st.joint_evals * joint_f) / n_sub,
+        "ptc_step": (st.pred_steps * pred_f + st.joint_evals * joint_f) / max(st.joint_evals, 1),
     }
     per_step_counts = {"enc_proj": 1, "pred_layer0": st.pred_steps,
                        "pred_layer1": st.pred_steps if L > 1 else 0,
-                       "pred_proj": st.pred_steps, "joint": st.joint_evals, "persistent": n_sub}
+                       "pred_proj": st.pred_steps, "joint": st.joint_evals, "persistent": n_sub,
+                       "ptc_step": st.joint_evals}
     share = {n: kern[n] * per_step_counts[n] / ms_per_step for n in kern}
     dom = max(share, key=share.get)
     peaks = {}
@@ -327,24 +333,27 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent):
     step_bytes = (st.pred_steps * pred_w + st.joint_evals * joint_w) / steps
     step_flops = (st.pred_steps * pred_f + st.joint_evals * joint_f) / steps
     t_step = ms_per_step * 1000.0 / steps
-    tensor = args.exec == "tensor"
+    tensor = args.exec in ("tensor", "graph", "hostloop")
     tc_peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1378.6)))
     # tensor executor: the fp32 GEMVs run as 3 fp16 tcgen05 products (hi.hi, hi.lo,
     # lo.hi), so the compute bound is 3x the FLOPs at the dense fp16 tensor peak;
     # the FFMA executors are bound by the FP32 CUDA-core peak
     t_flops = step_flops * 3 / (tc_peak * 1e6) if tensor else step_flops / (fp32_peak * 1e6)
     t_roof = max(step_bytes / (hbm_peak * 1e3), t_flops)
-    kname = {"persistent": "ptc_kernel" if tensor else "persistent_kernel"}.get(dom, dom)
+    kname = {"persistent": "ptc_kernel" if tensor else "persistent_kernel",
+             "ptc_step": "ptc_kernel (step launches)"}.get(dom, dom)
     extra = {}
     traffic = None
+    tsrc = next((f for f in ("r2_ncu_tensor_summary.json", "r1_ncu_tensor_summary.json")
+                 if os.path.exists(os.path.join(ROOT, "profiles", f))), None)
     try:  # dram read+write bytes per launch from the committed ncu --set full capture
-        for e in json.load(open(os.path.join(ROOT, "profiles", "r1_ncu_tensor_summary.json"))):
-            if tensor and kname in e.get("kernel", "") and Bl == 32 and T == 250:
+        for e in json.load(open(os.path.join(ROOT, "profiles", tsrc))):
+            if args.exec == "tensor" and "ptc_kernel" in e.get("kernel", "") and Bl == 32 and T == 250:
                 mb = lambda k: float(e[k].split()[0]) * {"Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9}[e[k].split()[1]]
                 traffic = mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")
     except Exception:
         traffic = None
-    if tensor and dom == "persistent":
+    if tensor and dom in ("persistent", "ptc_step"):
         tc_ach = 3 * flops_per[dom] / (kern[dom] / 1000.0) / 1e12
         extra["tensor"] = {"achieved_tflops": tc_ach, "peak_tflops": tc_peak, "frac": tc_ach / tc_peak,
                            "note": "3 fp16 tcgen05 products per fp32 MAC (hi/lo split) vs "
@@ -352,7 +361,7 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent):
                                    "smem/TMEM, so the hbm line is the equivalent streaming rate"}
     return {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": hbm_peak, "unit": "GB/s", **extra,
             "frac": ach / hbm_peak, "traffic": traffic,
-            "traffic_source": "profiles/r1_ncu_tensor_summary.json (ncu --set full, C2)" if traffic else None,
+            "traffic_source": f"profiles/{tsrc} (ncu --set full, C2)" if traffic else None,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)",
             "algorithmic_bytes_per_launch": bytes_per[dom],
             "avg_launch_us": kern[dom] * 1000.0,
@@ -405,6 +414,13 @@ def measure_idle(L_, dh, decode_ms=None):
     inflates launch gaps, so the traced span is reported separately."""
     from paper_2406_03791_b200._lib import check
     busy, span, nk = C.c_double(), C.c_double(), C.c_int64()
+    # one warm-up trace: the first CUPTI session of a process misses the kernels
+    # launched from conditional-node bodies of a graph
+    if L_.rnntg_trace_begin() != 0:
+        return None
+    check(L_.rnntg_launch(dh))
+    check(L_.rnntg_sync(dh))
+    check(L_.rnntg_trace_end(C.byref(busy), C.byref(span), C.byref(nk)))
     if L_.rnntg_trace_begin() != 0:
         return None
     check(L_.rnntg_launch(dh))
@@ -589,12 +605,20 @@ def main():
     per_rank_frames = Bl * T
     fs = algo == "fs"
     persistent = args.exec in ("persistent", "tensor")
+    # graph / host loop: the tcgen05 step kernel, one launch per decision
+    tc_steps = args.exec in ("graph", "hostloop")
     if persistent:
         launches_per_step = 2
+    elif tc_steps:
+        launches_per_step = 2 + st.joint_evals
     else:
         launches_per_step = 2 + st.pred_steps * (L + 1) + st.joint_evals + (st.outer_iters if fs else 0)
     hyps_dev = read_hyps(L_, dh, Bl)  # the timed decodes' hypotheses (device-resident inputs)
-    roofline, clk = roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent)
+    idle = measure_idle(L_, dh, ms_per_step)
+    step_ms = None
+    if tc_steps and idle and idle.get("kernels", 0) > 2:
+        step_ms = (idle["busy_ms"] - 0.0) / idle["kernels"]
+    roofline, clk = roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent, step_ms)
 
     # ---- e2e through the C ABI with host buffers ----
     e2e = None
@@ -678,7 +702,6 @@ def main():
                   file=sys.stderr)
 
     parity = check_parity(args, cfg, hyps_dev, b0, b1, rank, world, dist)
-    idle = measure_idle(L_, dh, ms_per_step)
     alt = None
     if not args.no_compare:
         alt = measure_alt_exec(args, L_, model, cfg, xd, ld, Bl, T, frames_all)
