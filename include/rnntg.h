@@ -196,6 +196,12 @@ rnntg_status rnntg_time_kernel(rnntg_decoder* d, int which, int reps, float* avg
 
 /* Tensor executor event trace (RNNTG_PROF=1): [16 events][64 steps] globaltimer ns. */
 rnntg_status rnntg_debug_trace(rnntg_decoder* d, unsigned long long* out, int n);
+/* Logit-level parity of the tensor-core executor (test_model.cpp:224-270
+ * analogue): runs one decode of the bound inputs with the J tiles' fp32
+ * logits of decision step `step` (group row order = batch order) copied to
+ * out[B][V1 + D] (vocab + blank, then the duration logits).  Rows that make
+ * no decision at that step keep 0.  Tensor executor, B <= 256 only. */
+rnntg_status rnntg_debug_logits(rnntg_decoder* d, int step, float* out);
 /* Persistent executor phase profile (CTA 0, ns per phase, accumulated since
  * the last call; needs RNNTG_PROF=1 at decoder creation). */
 rnntg_status rnntg_debug_profile(rnntg_decoder* d, unsigned long long* out16);

@@ -33,7 +33,7 @@ EXPORTS = [
     "rnntg_model_destroy", "rnntg_decoder_create", "rnntg_decoder_destroy",
     "rnntg_decoder_capacity", "rnntg_bind", "rnntg_bind_device", "rnntg_launch", "rnntg_sync",
     "rnntg_read", "rnntg_get_stats", "rnntg_decoder_stream", "rnntg_step_joint",
-    "rnntg_step_prediction", "rnntg_enc_proj", "rnntg_time_kernel", "rnntg_debug_profile", "rnntg_debug_trace", "rnntg_trace_begin", "rnntg_trace_end",
+    "rnntg_step_prediction", "rnntg_enc_proj", "rnntg_time_kernel", "rnntg_debug_profile", "rnntg_debug_trace", "rnntg_debug_logits", "rnntg_trace_begin", "rnntg_trace_end",
 ]
 
 _lib = None
@@ -69,6 +69,7 @@ def lib():
     L.rnntg_time_kernel.argtypes = [vp, C.c_int, C.c_int, P(C.c_float)]
     L.rnntg_debug_profile.argtypes = [vp, P(C.c_uint64)]
     L.rnntg_debug_trace.argtypes = [vp, P(C.c_uint64), C.c_int]
+    L.rnntg_debug_logits.argtypes = [vp, C.c_int, P(C.c_float)]
     L.rnntg_trace_end.argtypes = [P(C.c_double), P(C.c_double), P(C.c_int64)]
     _lib = L
     return L

@@ -179,6 +179,8 @@ struct TParams {
   cudaGraphConditionalHandle h_outer, h_inner;
   int use_cond;               // set the conditional handles (graph bodies)
   unsigned long long* stamps;  // optional [G][16] globaltimer stamps of the last launch (RNNTG_STAMPS)
+  float* dbg_logits;          // optional [B][V1 + D]: the J tiles' fp32 logits of decision step dbg_step
+  int dbg_step;               // (logit-level parity of the tensor-core executor, rnntg_debug_logits)
 };
 #ifndef STAMPS
 #define STAMPS 0  // compile the RNNTG_STAMPS launch stamps in (A/B builds: the checks cost in the hot loop)
@@ -686,6 +688,10 @@ struct Epi : CfgFlags<SPEC> {
   long long joint_evals = 0, pred_steps = 0, outer_iters = 0;
   bool finish = false, frame_end = false;
   unsigned long long t_entry = 0;  // kernel entry (globaltimer), for STAMPS builds
+  // STAMPS builds: per-phase clock64 sums of thread 0 -- 0 load, 1 J round,
+  // 2 decide, 3 pred/idle, 4 save/ack, 5 word wait (in decide), 6 acc wait (read_acc), 7 total
+  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  __device__ __forceinline__ long long clk() const { return STAMPS ? clock64() : 0; }
 
   __device__ Epi(const TParams& P_, const Smem& sm_, uint32_t tmem, int et_, int q, int role_, int layer_,
                  int tile_, float wsc_)
@@ -813,7 +819,9 @@ struct Epi : CfgFlags<SPEC> {
       }
     }
     const int set = NACC == 1 ? 0 : (r & 1);
+    const long long tw0 = clk();
     mbar_wait(&sm.accf[set], (uint32_t)(NACC == 1 ? (r & 1) : ((r >> 1) & 1)));
+    if (STAMPS) ph[6] += clk() - tw0;
     tc_fence_after();
     const uint32_t a = tq + set * ACC_COLS + r0;
     {
@@ -892,6 +900,12 @@ struct Epi : CfgFlags<SPEC> {
     mark(1);
     mark(16);
     const long long tacc = PPROF(P) ? clock64() : 0;
+    if (P.dbg_logits && s == P.dbg_step) {  // logit-parity dump (tests only)
+      const int colv = 128 * tile + m;
+      if (colv < P.V1 + P.D)
+        for (int i = 0; i < NR; ++i)
+          if (r0 + i < B) P.dbg_logits[(size_t)(row0 + r0 + i) * (P.V1 + P.D) + colv] = v[i];
+    }
     // slot reuse: steps s .. s + NSLOT/2 - 1 overwrite the slots of steps
     // s - NSLOT .. s - NSLOT/2 - 1, so EVERY CTA (not their sum: an off-path
     // role such as the emitter may lag) must have acked step s - NSLOT/2.
@@ -1073,6 +1087,7 @@ struct Epi : CfgFlags<SPEC> {
         // spin on one word (tile NJ-1) with a single load in flight, then read
         // the rest once (warp-wide strong loads are serviced ~100 cycles apart:
         // a 9-16 load batch per poll made each poll ~1 us; one load is ~360 cycles)
+        const long long tw0 = clk();
         // (step launches: J wrote step s's words in the previous launch)
         if (!words_prev)
           while ((unsigned)(ld_poll_u64(wv + (nj - 1) * 32) >> 32 & 0xffu) != tg) ++npoll;
@@ -1102,6 +1117,7 @@ struct Epi : CfgFlags<SPEC> {
           ok = bad == 0u;
         } while (!ok);
         if (c0 && b == 0) mark(31);  // every tile's word seen
+        if (STAMPS) ph[5] += clk() - tw0;
         npoll_out = npoll;
         lat1_out = lat1;
         best = -INFINITY;
@@ -1269,6 +1285,7 @@ struct Epi : CfgFlags<SPEC> {
     // with several groups or step launches, the per-thread state of a group
     // lives in global memory between its visits
     const bool multi = P.ngrp > 1 || mode != STEP_NONE;
+    ph[7] = clk();
     int sslot = 0;
     // the TMEM weights before the first round: at the start of a whole-decode
     // or P0 launch; in a step launch after its first decision (the decision
@@ -1310,12 +1327,16 @@ struct Epi : CfgFlags<SPEC> {
           if (!sm.grp[GS_RUN * MAXG + gg]) continue;
           any = true;
           set_group(gg);
+          long long tp0 = clk();
           load(multi ? LD_MULTI : LD_VISIT);
+          if (STAMPS) { const long long t = clk(); ph[0] += t - tp0; tp0 = t; }
           if (et == 0 && gg == 0) stamp(P, sslot, 3);
           // step launches run J at the END of a visit (the next step's joint,
           // so J's weight load overlaps the decision + prediction chain)
           if (role == ROLE_J && (mode == STEP_NONE || !STEP_JROT)) joint_round();
+          if (STAMPS) { const long long t = clk(); ph[1] += t - tp0; tp0 = t; }
           decide();
+          if (STAMPS) { const long long t = clk(); ph[2] += t - tp0; tp0 = t; }
           if (has_w && !wloaded) load_weights();
           if (et == 0 && gg == 0) stamp(P, sslot, 4);
           fend_round |= frame_end;
@@ -1334,6 +1355,7 @@ struct Epi : CfgFlags<SPEC> {
             idle(s + 1);
           }
           if (et == 0 && gg == 0) stamp(P, sslot, 5);
+          if (STAMPS) { const long long t = clk(); ph[3] += t - tp0; tp0 = t; }
           if (multi) save();
           // this CTA is done with step s's words: ack (slot reuse, joint_round).
           // A per-CTA word; the reads it covers were consumed before the barrier
@@ -1345,9 +1367,14 @@ struct Epi : CfgFlags<SPEC> {
           if (et == 0 && gg == 0) stamp(P, sslot, 6);
           save_group();
           epi_sync();
+          if (STAMPS) ph[4] += clk() - tp0;
         }
         if (!any || mode == STEP_ONE) break;
       }
+    }
+    if (STAMPS && mode == STEP_NONE && et == 0) {
+      ph[7] = clk() - ph[7];
+      for (int i = 0; i < 8; ++i) stamp_at(P, 63, 8 + i, (unsigned long long)ph[i]);
     }
     if (mode != STEP_NONE) {
       // step launches: keep the control state for the next launch, and set
@@ -1770,8 +1797,10 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
     // ================= producer (converged warp): stream input chunks into the ring =================
     // Stage of chunk kc is kc % NSTAGE every round: a round is posted only after
     // the epilogue read the previous round's accumulator, so every earlier MMA
-    // (and its smem read) has completed and the first NSTAGE chunks need no
-    // empty-barrier wait.  eb bit s = uses of stage s so far (mod 2).
+    // (and its smem read) has completed and the first NSTAGE chunks' empty-
+    // barrier waits return at once (they are still made, so every phase of
+    // every barrier is waited on: compute-sanitizer synccheck clean).
+    // eb bit s = uses of stage s so far (mod 2).
     const unsigned* mycnt0 = P.cnt + (size_t)(cidx_act(in_buf, 0) + (lane < KC ? lane : 0)) * CSTRIDE;
     const unsigned my_np = lane < KC ? (unsigned)P.nprod[in_buf][lane] : 0u;
     const CUtensorMap* lmap = &P.ldmap[in_buf];
@@ -1780,7 +1809,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
     const bool trj = PPROF(P) && role == ROLE_J && (int)blockIdx.x == P.prof_first[role] && lane == 0;
     unsigned long long* const prof = PPROF(P);
     const uint32_t ring0 = smem_u32(sm.ring);
-    uint32_t eb = 0;
+    uint32_t eb = 0, used = 0;
     for (int r = 0;; ++r) {
       mbar_wait(sm.cmd, r & 1);
       const int e = ((volatile int*)sm.misc)[r & 1];
@@ -1813,7 +1842,11 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
         for (int kc = 0; kc < MAXKC; ++kc) {
           if (kc >= next && kc < ready) {
             const int st = kc % NSTAGE;
-            if (kc >= NSTAGE) mbar_wait(&sm.empty[st], ((eb >> st) & 1u) ^ 1u);
+            // every phase of a stage's empty barrier is waited on once (the
+            // first NSTAGE chunks of a round find theirs complete: the round was
+            // posted after the epilogue read the previous round's accumulator)
+            if ((used >> st) & 1u) mbar_wait(&sm.empty[st], ((eb >> st) & 1u) ^ 1u);
+            used |= 1u << st;
             eb ^= 1u << st;
             if (tr && (kc == 0 || kc == KC - 1)) prof[(size_t)(kc ? 13 : 12) * PROF_WIN + (e - PROF_S0)] = gtimer();
             if ((kc == 0 || kc == KC - 1) && stamp_ip && lane == 0)
@@ -1830,6 +1863,9 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
       }
       if (ctr) sm.dbg[11] = npoll;
     }
+    // a step launch may end without an MMA round: the smem weight copy must
+    // still land before the CTA exits (no async write may outlive it)
+    mbar_wait(sm.wbar, 0);
   } else if (warp == 1) {
     // ================= MMA issuer (converged warp) =================
     const uint32_t whi0 = smem_u32(sm.whi), ring0 = smem_u32(sm.ring);

@@ -1770,6 +1770,27 @@ rnntg_status rnntg_debug_trace(rnntg_decoder* d, unsigned long long* out, int n)
   return RNNTG_OK;
 }
 
+rnntg_status rnntg_debug_logits(rnntg_decoder* d, int step, float* out) {
+  if (!d || !out || step < 0) return fail(RNNTG_E_VALUE, "bad arguments");
+  if (d->exec != RNNTG_EXEC_TENSOR || !d->subs.empty())
+    return fail(RNNTG_E_STATE, "logit dumps need the tensor executor (batch <= 256)");
+  if (!d->bound) return fail(RNNTG_E_STATE, "captured decoder is not initialized (no inputs bound)");
+  CK(cudaSetDevice(d->m->device));
+  const size_t n = (size_t)d->B * (d->tp.V1 + d->tp.D);
+  float* buf = nullptr;
+  CK(cudaMalloc(&buf, n * sizeof(float)));
+  cudaError_t e = cudaMemsetAsync(buf, 0, n * sizeof(float), d->stream);
+  d->tp.dbg_logits = buf;
+  d->tp.dbg_step = step;
+  if (e == cudaSuccess) e = issue_persistent(d, d->stream);  // direct launch: the captured one has no dump
+  d->tp.dbg_logits = nullptr;
+  if (e == cudaSuccess) e = cudaStreamSynchronize(d->stream);
+  if (e == cudaSuccess) e = cudaMemcpy(out, buf, n * sizeof(float), cudaMemcpyDeviceToHost);
+  cudaFree(buf);
+  if (e != cudaSuccess) return fail(RNNTG_E_CUDA, std::string("debug logits: ") + cudaGetErrorString(e));
+  return RNNTG_OK;
+}
+
 rnntg_status rnntg_debug_profile(rnntg_decoder* d, unsigned long long* out16) {
   if (!d || !out16) return fail(RNNTG_E_VALUE, "bad arguments");
   if (d->exec != RNNTG_EXEC_PERSISTENT || !d->pp.prof)

@@ -322,3 +322,53 @@ def test_tensor_row_groups_c2_dims():
     print(f"\nc2dims B80: {rep.exact}/{rep.utterances} exact, {rep.permitted} permitted")
     assert rep.ok, rep.failures[:5]
     m.close()
+
+
+@pytest.mark.parametrize("B,tdt,step", [(8, False, 0), (8, False, 7), (40, False, 7), (8, True, 0)])
+def test_tensor_logits_vs_oracle(B, tdt, step):
+    """Logit-level parity of the tcgen05 executor (test_model.cpp:224-270
+    analogue) at C2 dims: the J tiles' fp32 logits of decision step `step`,
+    turned into log-probabilities, against the oracle's joint on the same
+    prediction state (replayed from the decoded labels) within 1e-4 relative.
+    Random init emits a label at every step (T * ms per row), so at frame-
+    looping step s every row is at frame s // ms after s emissions."""
+    _need_gpu()
+    from paper_2406_03791_b200._lib import check, lib
+    durs = (0, 1, 2, 3, 4) if tdt else ()
+    d = O.Dims(1024, 640, 640, 640, 1024, durs, O.CELL_LSTM, 2)
+    p = O.init_params(1, d)
+    T, ms = 4, 5
+    x = O.fill_uniform(2, -1.0, 1.0, (B, T, 1024))
+    lens = np.full(B, T, np.int32)
+    m = Model(to_model_dims(d), p)
+    algo = DecodeAlgo.TdtLabelLoop if tdt else DecodeAlgo.FrameSync
+    cap = D.build_decode_graph(m, algo, B, T, ms, D.Exec.Tensor)
+    hyps = D.replay_decode(cap, x, lens)
+    V1, nD = d.vocab + 1, len(durs)
+    out = np.zeros((B, V1 + nD), np.float32)
+    check(lib().rnntg_debug_logits(cap.handle, step, out.ctypes.data_as(P._lib.C.POINTER(P._lib.C.c_float))))
+    # oracle state after `step` emissions (P0 = pred(blank, 0), then the labels)
+    st = O.prediction(d, p, np.full(B, d.vocab, np.int32), np.zeros((B, d.state_width), np.float32))
+    for k in range(step):
+        assert all(len(h.tokens) > k and h.frames[k] == k // ms for h in hyps)
+        st = O.prediction(d, p, np.array([h.tokens[k] for h in hyps], np.int32), st)
+    f = np.ascontiguousarray(x[:, step // ms, :])
+    logp_ref, dlogp_ref = O.joint(d, p, f, st)
+
+    def logsoftmax(v):
+        v = v.astype(np.float64)
+        mx = v.max(axis=1, keepdims=True)
+        return v - (mx + np.log(np.exp(v - mx).sum(axis=1, keepdims=True)))
+    logp = logsoftmax(out[:, :V1])
+    err = rel_err(logp, logp_ref)
+    print(f"\nB{B} tdt={tdt} step {step}: logp rel err {err:.2e}")
+    assert err < RTOL, err
+    # the emitted label is the argmax of these logits
+    if not tdt:
+        assert [int(np.argmax(out[b, :V1])) for b in range(B)] == [h.tokens[step] for h in hyps]
+    if tdt:
+        derr = rel_err(logsoftmax(out[:, V1:]), dlogp_ref)
+        print(f"  duration logp rel err {derr:.2e}")
+        assert derr < RTOL, derr
+    cap.close()
+    m.close()
