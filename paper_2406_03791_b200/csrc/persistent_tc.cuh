@@ -8,16 +8,18 @@
 //   role   weights (swap-AB: M = 128 output rows)   input        output
 //   J      [out_proj || dur_proj] cols 128t..        trunk(s)     per-row argmax words, (max, sumexp)
 //   P      pred_proj cols 128t..                     h_{L-1}(p)   gp -> trunk(s+1) = relu(fp + gp)
-//   R_l    W_hh_l gate rows (unit-major, 32 units)   h_l(p)       hh_l(p+1) -> global (for I_l)
-//   I_0    none (the layer-0 cell)                   table0[k] + hh_0(p)      cell -> h_0(p+1)
+//   R_0    W_hh0 gate rows (unit-major, 32 units)    table0[k] + hh0(p) (registers): the layer-0 cell
+//                                                    -> h_0(p+1); then h_0(p+1) @ W_hh0 -> hh0(p+2)
+//   R_l    W_hh_l gate rows, l >= 1                  h_l(p)       hh_l(p+1) -> global (for I_l);
+//                                                                 R_{L-1} tile 0 also merges the J
+//                                                                 partials: scores, hypotheses
 //   I_l    W_ih_l gate rows, l >= 1                  h_{l-1}(p)   (+ hh_l) cell -> h_l(p)
-//   E      none                                      J partials   lse, emitted score, hypotheses
 //
 // Row groups.  The batch is split into ngrp <= 8 groups of <= 32 rows; every
 // CTA serves every group, visiting the live groups round-robin one step
 // ("item") at a time.  The groups are independent decodes (model.hpp:89-91)
 // with their own buffers, counters and replicated control, so while one
-// group's step is in flight down the chain (J -> decision -> I_0 -> I_1 -> P),
+// group's step is in flight down the chain (J -> decision -> R_0 -> I_1 -> P),
 // the CTAs that are done with it work on the next group's step.
 //
 // Arithmetic.  Every GEMV is D[128 x 32 rows] = W[128 x K] . A^T on the
@@ -41,7 +43,8 @@
 // Control state (labels, cursors, masks, frame counters) is replicated in
 // every CTA: each CTA merges the J tiles' argmax words for every row and
 // applies the same decision rules (decoders.cpp:261-307, 432-512), so no
-// decision broadcast is needed.  The emitter CTA writes the hypotheses.
+// decision broadcast is needed.  R_{L-1} tile 0 (off the per-step chain)
+// writes the hypotheses.
 //
 // Warp roles inside a CTA: warp 0 = TMA producer, warp 1 = MMA issuer
 // (elect.sync inside a converged warp: issuing from a divergent lane costs
@@ -75,7 +78,8 @@ constexpr int MAXNJ = MAXNJ_CFG;       // joint tiles (V+1+D <= 2048)
 constexpr int CHUNK = 8192;      // [64 rows][64 k] fp16, SWIZZLE_128B
 constexpr int MAXB = 32;         // rows per group (one MMA N slice: 32 hi + 32 lo activation rows)
 constexpr int MAXG = 8;          // row groups per kernel: batch <= 256
-constexpr int NSV = 8;           // per-thread state floats saved per group (P: gp[NR]; cells: c, h)
+constexpr int MAXI = 2;          // instances per kernel
+constexpr int NSV = 16;          // per-thread state floats saved per group (P: gp; cells: c, h; R_0: + hh0)
 constexpr int MAXKP = 640;       // K <= 640: W_lo (K/2 TMEM columns) + 2 x 96 accumulator columns
 constexpr int MAXKC = MAXKP / 64;
 constexpr int TRUNK = MAXL;      // activation buffer ids: h_0..h_{L-1}, trunk
@@ -86,7 +90,8 @@ constexpr int MAXBUF = MAXL + 1;
 constexpr int NSLOT = NSLOT_CFG;  // joint-partial ring depth (ack checked every NSLOT/2 steps)
 constexpr int CSTRIDE = 32;      // u32 words between counters (one 128-byte line each)
 
-// I with layer 0 is the layer-0 cell (no weights: table0[label] + hh0 from R_0)
+// (ROLE_E, a weightless emitter CTA, and I_0, a weightless layer-0 cell, are
+// no longer assigned: J tile 0 emits, R_0 runs the layer-0 cell)
 enum Role { ROLE_J = 0, ROLE_P = 1, ROLE_R = 2, ROLE_I = 3, ROLE_E = 4 };  // E: emitter (no weights)
 constexpr int NROLES = 5;
 #ifndef TANH_SIG
@@ -178,6 +183,12 @@ struct TParams {
   int* ctl;                   // [G][CTL_INTS] each CTA's replicated control state between step launches
   cudaGraphConditionalHandle h_outer, h_inner;
   int use_cond;               // set the conditional handles (graph bodies)
+  int split0;                 // 1: layer-0 cell on its own CTAs (I_0) + an emitter CTA (E); 0: merged into R_0
+  // instances: independent CTA sets, each decoding its own row groups
+  // (roles[c].y >> 8 = instance); groups [ig0[i], ig0[i+1]), CTAs [ic0[i], ic0[i+1])
+  int ninst;
+  int ig0[MAXI + 1];
+  int ic0[MAXI + 1];
   unsigned long long* stamps;  // optional [G][16] globaltimer stamps of the last launch (RNNTG_STAMPS)
   float* dbg_logits;          // optional [B][V1 + D]: the J tiles' fp32 logits of decision step dbg_step
   int dbg_step;               // (logit-level parity of the tensor-core executor, rnntg_debug_logits)
@@ -197,6 +208,9 @@ __device__ __forceinline__ void stamp(const TParams& P, int slot, int i) {
   }
 }
 enum { STEP_NONE = 0, STEP_INIT = 1, STEP_ONE = 2 };
+#ifndef FORCE_SPLIT0
+#define FORCE_SPLIT0 0  // A/B: compile the merged-R_0 paths out
+#endif
 #ifndef STEP_JROT
 #define STEP_JROT 1  // step launches: J's joint at the end of a launch (for the next step)
 #endif
@@ -666,10 +680,14 @@ struct Epi : CfgFlags<SPEC> {
   const TParams& P;
   const Smem& sm;
   const uint32_t tq;  // TMEM address of this warp's lane quadrant
-  const int et, m, r0, role, layer, tile;
+  const int et, m, r0, role, layer, tile, inst;
   const float wsc;
   const int blank;
-  const bool c0;      // the layer-0 cell (I_0): table0[label] + hh0, no weights
+  const bool c0;      // runs the layer-0 cell (table0[label] + hh0 + b): I_0 (split0) or R_0
+  const bool r0m;     // R_0 merged with the cell: then h_0 @ W_hh0 -> hh0 of the next prediction in registers
+  // the emitter (merges the J partials: scores, hypotheses): R_{L-1} tile 0,
+  // a CTA off the per-step chain (J tile 0 for one-layer models)
+  const bool is_emitter;
   const bool words_prev;  // step launches with J rotated: step s's words / partials come from the previous launch
   const bool tracer;  // event-trace CTA (single-group decodes only)
   // ---- the current item's group (set_group) ----
@@ -694,10 +712,13 @@ struct Epi : CfgFlags<SPEC> {
   __device__ __forceinline__ long long clk() const { return STAMPS ? clock64() : 0; }
 
   __device__ Epi(const TParams& P_, const Smem& sm_, uint32_t tmem, int et_, int q, int role_, int layer_,
-                 int tile_, float wsc_)
+                 int tile_, int inst_, float wsc_)
       : CfgFlags<SPEC>(P_), P(P_), sm(sm_), tq(tmem + ((uint32_t)(32 * q) << 16)), et(et_), m(32 * q + (et_ & 31)),
         r0(NR * (et_ >> 7)), role(role_),
-        layer(layer_), tile(tile_), wsc(wsc_), blank(P_.V1 - 1), c0(role_ == ROLE_I && layer_ == 0),
+        layer(layer_), tile(tile_), inst(inst_), wsc(wsc_), blank(P_.V1 - 1), c0((FORCE_SPLIT0 || P_.split0) ? (role_ == ROLE_I && layer_ == 0) : (role_ == ROLE_R && layer_ == 0)),
+        r0m(!FORCE_SPLIT0 && !P_.split0 && role_ == ROLE_R && layer_ == 0),
+        is_emitter(P_.split0 ? role_ == ROLE_E
+                   : P_.L > 1 ? (role_ == ROLE_R && layer_ == P_.L - 1 && tile_ == 0) : (role_ == ROLE_J && tile_ == 0)),
         words_prev(P_.step_mode == STEP_ONE && STEP_JROT),
         tracer(PPROF(P_) && P_.ngrp == 1 && (int)blockIdx.x == P_.prof_first[role_]) {}
 
@@ -876,7 +897,7 @@ struct Epi : CfgFlags<SPEC> {
       ecnt[et] = 0;
       const int len = et < B ? __ldg(&P.out_len[row0 + et]) : 0;
       flag[et] = (et < B ? (fs ? (0 >= len) : !(0 < len)) : 1) | 2;  // every row runs P0
-      if (role == ROLE_E && et < B) P.counts[row0 + et] = 0;
+      if (is_emitter && et < B) P.counts[row0 + et] = 0;
     }
     maxlen = 0;
     for (int b = 0; b < B; ++b) maxlen = max(maxlen, __ldg(&P.out_len[row0 + b]));
@@ -916,7 +937,7 @@ struct Epi : CfgFlags<SPEC> {
         const unsigned* ack = P.ack + (size_t)g * P.G;
         for (;;) {
           unsigned mn = 0xffffffffu;
-          for (int c = et; c < P.G; c += 32) mn = min(mn, ld_relaxed(ack + c));
+          for (int c = P.ic0[inst] + et; c < P.ic0[inst + 1]; c += 32) mn = min(mn, ld_relaxed(ack + c));
           if (__reduce_min_sync(0xffffffffu, mn) >= target) break;
         }
       }
@@ -1059,7 +1080,7 @@ struct Epi : CfgFlags<SPEC> {
       const bool valid = b < B;
       const int slot = (int)(s % NSLOT);
       const unsigned tg = step_tag(s);
-      const bool emitter = role == ROLE_E;
+      const bool emitter = is_emitter;
       int kk = blank, dd = 0, npoll_out = 0;
       long long lat1_out = 0;
       float best = 0.0f;
@@ -1289,10 +1310,10 @@ struct Epi : CfgFlags<SPEC> {
     int sslot = 0;
     // the TMEM weights before the first round: at the start of a whole-decode
     // or P0 launch; in a step launch after its first decision (the decision
-    // and the weight-free I_0 chain go first, before the weight traffic)
-    const bool has_w = !(role == ROLE_E || c0);
-    // the first MMAs after the decision (I_1 and R_0 on h0) load theirs before it
-    if (has_w && (WEAGER || (role == ROLE_I && layer == 1) || (role == ROLE_R && layer == 0))) load_weights();
+    // and R_0's weight-free layer-0 cell go first, before the weight traffic),
+    // except I_1, the first MMA after the decision, which loads before it
+    const bool has_w = role != ROLE_E && !(role == ROLE_I && layer == 0);
+    if (has_w && (WEAGER || (role == ROLE_I && layer == 1) || (role == ROLE_R && layer == 0 && !r0m))) load_weights();
     if (mode == STEP_ONE) {
       load_ctl();
       sslot = sm.grp[GS_STEP * MAXG];
@@ -1302,7 +1323,7 @@ struct Epi : CfgFlags<SPEC> {
       }
     } else {
       if (has_w && !wloaded) load_weights();
-      for (int gg = 0; gg < P.ngrp; ++gg) {
+      for (int gg = P.ig0[inst]; gg < P.ig0[inst + 1]; ++gg) {
         set_group(gg);
         init_rows();
         load(LD_INIT);
@@ -1323,7 +1344,7 @@ struct Epi : CfgFlags<SPEC> {
     if (mode != STEP_INIT) {
       for (;;) {
         bool any = false;
-        for (int gg = 0; gg < P.ngrp; ++gg) {
+        for (int gg = P.ig0[inst]; gg < P.ig0[inst + 1]; ++gg) {
           if (!sm.grp[GS_RUN * MAXG + gg]) continue;
           any = true;
           set_group(gg);
@@ -1337,7 +1358,7 @@ struct Epi : CfgFlags<SPEC> {
           if (STAMPS) { const long long t = clk(); ph[1] += t - tp0; tp0 = t; }
           decide();
           if (STAMPS) { const long long t = clk(); ph[2] += t - tp0; tp0 = t; }
-          if (has_w && !wloaded) load_weights();
+          if (has_w && !wloaded && !r0m) load_weights();  // (merged R_0: after its cell, in pred)
           if (et == 0 && gg == 0) stamp(P, sslot, 4);
           fend_round |= frame_end;
           if (finish) {
@@ -1576,7 +1597,7 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
 #pragma unroll
           for (int i = 0; i < NR; ++i) *gstate(i) = gp[i];
         });
-  } else if (role == ROLE_R) {
+  } else if (role == ROLE_R && !r0m) {
     // hh_l(p+1) = h_l(p) @ W_hh_l -> global, for the layer-l cell of the next prediction
     run(
         [&](long long) {
@@ -1591,16 +1612,17 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
         },
         [&](long long) {}, nopl, nop);
   } else {
-    // I_0 (layer-0 cell: table0[label] + hh0) or I_l (W_ih_l MMA + hh_l)
+    // R_0: the layer-0 cell (table0[label] + hh0 + b), then the next
+    // prediction's hh0 = h0 @ W_hh0 into registers (hx); I_l: the W_ih_l MMA
+    // plus hh_l from R_l
     const float* bl = P.bias[layer];
     const float bias_m = unit < P.H ? __ldg(&bl[gate * P.H + unit]) : 0.0f;
     float c4[NR / 4], h4[NR / 4], hr[NR], hx[NR];
-    int hx_ep = -1;  // I_0: prediction epoch whose hh0 is in hx
 #pragma unroll
     for (int j = 0; j < NR / 4; ++j) c4[j] = h4[j] = 0.0f;
 #pragma unroll
     for (int j = 0; j < NR; ++j) hr[j] = hx[j] = 0.0f;
-    // hh_l(pe) (R_l's output) -> x; zero for P0
+    // hh_l(pe) (R_l's output, l >= 1) -> x; zero for P0
     auto load_hh = [&](int pe, float (&x)[NR]) {
       if (pe > 0) {
         // (step launches: R_l wrote hh_l(pe) in an earlier launch, ordered by the kernel boundary)
@@ -1613,27 +1635,40 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
         for (int i = 0; i < NR; ++i) x[i] = 0.0f;
       }
     };
-    // I_0: the next prediction's hh0 is ready long before the decision: fetch
-    // it at the start of the visit, before the word poll
-    auto prefetch_hh0 = [&]() {
-      if (c0 && hx_ep != p + 1) {
-        load_hh(p + 1, hx);
-        hx_ep = p + 1;
+    const int hxo = lstm ? NR / 2 : NR;  // gst slot of hx (after the cell state)
+    int hx_ep = -1;  // I_0 (split0): prediction epoch whose hh0 (from R_0, global) is in hx
+    // R_0's hh0 MMA is read lazily: at the group's next use or when the next
+    // round needs the accumulator (its group's registers / global state)
+    int pend_r = -1, pend_g = 0;
+    auto flush = [&]() {
+      if (!r0m || pend_r < 0) return;
+      float v[NR];
+      read_acc(pend_r, v);
+      if (pend_g == g) {
+#pragma unroll
+        for (int i = 0; i < NR; ++i) hx[i] = v[i];
       }
+      if (P.ngrp > 1 || P.step_mode != STEP_NONE) {  // the group's state in global memory
+        float* gs = P.gst + (((size_t)pend_g * P.G + blockIdx.x) * NSV + hxo) * NEPI + et;
+#pragma unroll
+        for (int i = 0; i < NR; ++i) gs[(size_t)i * NEPI] = v[i];
+      }
+      pend_r = -1;
     };
     run(
         [&](long long) {
           float v[NR], x[NR];
           if (c0) {
+            flush();  // (normally done at the visit's start)
+            if (!r0m && hx_ep != p) {  // I_0: hh0(p) from R_0 (P0: zeros)
+              load_hh(p, hx);
+              hx_ep = p;
+            }
             // gates0 = (table0[label] + hh0) + b   (App. B order)
             if (p == 0) {  // P0: label blank for every row
 #pragma unroll
               for (int i = 0; i < NR; ++i)
                 ih[i] = r0 + i < B ? __ldg(&P.table0[(size_t)blank * P.GH + unit * P.Gg + gate]) : 0.0f;
-            }
-            if (hx_ep != p) {
-              load_hh(p, hx);
-              hx_ep = p;
             }
 #pragma unroll
             for (int i = 0; i < NR; ++i) x[i] = (flag[r0 + i] & 2) ? ih[i] : 0.0f;
@@ -1655,18 +1690,25 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
           mark_pub();
           gmark(c0 ? 44 : 46);
           mark(c0 ? 5 : 11);
+          if (r0m) {
+            // hh0 of the next prediction (h0(p) @ W_hh0): the MMA runs while the
+            // rest of the step goes down the chain (and this CTA moves on)
+            if (!wloaded) load_weights();
+            post(p);
+            pend_r = round - 1;
+            pend_g = g;
+          }
         },
-        [&](long long) {},
+        [&](long long) {
+          if (r0m) flush();
+        },
         [&](int mode) {
           if (mode == LD_INIT) {
 #pragma unroll
             for (int j = 0; j < NR / 4; ++j) c4[j] = h4[j] = 0.0f;
 #pragma unroll
-            for (int j = 0; j < NR; ++j) hr[j] = 0.0f;
-            hx_ep = -1;
-            return;
-          }
-          if (mode == LD_MULTI) {
+            for (int j = 0; j < NR; ++j) hr[j] = hx[j] = 0.0f;
+          } else if (mode == LD_MULTI) {
             if (lstm) {
 #pragma unroll
               for (int j = 0; j < NR / 4; ++j) {
@@ -1677,9 +1719,21 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
 #pragma unroll
               for (int j = 0; j < NR; ++j) hr[j] = *gstate(j);
             }
+            if (r0m) {
+#pragma unroll
+              for (int j = 0; j < NR; ++j) hx[j] = *gstate(hxo + j);
+            }
             hx_ep = -1;
           }
-          prefetch_hh0();
+          if (mode == LD_INIT) hx_ep = -1;
+          // merged R_0: the look-ahead hh0 MMA finished long ago; read it before
+          // the decision so the layer-0 cell does not wait on the accumulator.
+          // I_0: the next prediction's hh0 is ready long before the decision.
+          if (r0m && mode != LD_INIT) flush();
+          if (c0 && !r0m && mode != LD_INIT && hx_ep != p + 1) {
+            load_hh(p + 1, hx);
+            hx_ep = p + 1;
+          }
         },
         [&]() {
           if (lstm) {
@@ -1692,10 +1746,22 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
 #pragma unroll
             for (int j = 0; j < NR; ++j) *gstate(j) = hr[j];
           }
+          if (r0m && pend_r < 0) {  // (a pending hh0 is stored by its flush)
+#pragma unroll
+            for (int j = 0; j < NR; ++j) *gstate(hxo + j) = hx[j];
+          }
         });
+    flush();  // merged R_0: the last look-ahead round
   }
   post(-1);
-  if (blockIdx.x == 0 && et == 0) {
+  if (P.ninst > 1 && (int)blockIdx.x == P.ic0[inst] && et == 0) {  // instance totals (Ctrl zeroed at launch)
+    Ctrl* c = P.ctrl;
+    atomicAdd(reinterpret_cast<unsigned long long*>(&c->joint_evals), (unsigned long long)joint_evals);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&c->pred_steps), (unsigned long long)pred_steps);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&c->outer_iters), (unsigned long long)outer_iters);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&c->iters), (unsigned long long)joint_evals);
+    atomicMax(&c->err, err);
+  } else if (P.ninst <= 1 && blockIdx.x == 0 && et == 0) {
     Ctrl* c = P.ctrl;
     c->joint_evals = joint_evals;
     c->pred_steps = pred_steps;
@@ -1744,7 +1810,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
   unsigned long long t_entry = 0;
   if (STAMPS && threadIdx.x == 64) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
   const int4 rl = P.roles[blockIdx.x];
-  const int role = rl.x, layer = rl.y, tile = rl.z;
+  const int role = rl.x, layer = rl.y & 0xff, inst = rl.y >> 8, tile = rl.z;
   const float wsc = __int_as_float(rl.w);
   const int in_buf = (role == ROLE_J || role == ROLE_E) ? TRUNK : role == ROLE_P ? P.L - 1 : role == ROLE_R ? layer
                                                                                                       : max(layer - 1, 0);
@@ -1903,7 +1969,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
     }
   } else {
     // ================= epilogue + replicated control (128 threads) =================
-    Epi<TR, SPEC> e(P, sm, tmem, tid - 64, warp & 3, role, layer, tile, wsc);
+    Epi<TR, SPEC> e(P, sm, tmem, tid - 64, warp & 3, role, layer, tile, inst, wsc);
     e.t_entry = t_entry;
     e.run_role();
   }

@@ -524,7 +524,7 @@ float h2f(uint16_t h) {
 
 // Tensor-core persistent executor: role assignment (one 128-row weight tile
 // per CTA), fp16 hi/lo weight images, activation / counter buffers.
-rnntg_status setup_tc(rnntg_decoder* d) {
+rnntg_status setup_tc(rnntg_decoder* d, bool allow_inst = true) {
   rnntg_model* m = d->m;
   const DevModel& M = m->dm;
   const rnntg_dims& dd = m->dims;
@@ -538,18 +538,32 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   const int NG = lstm ? (H + 31) / 32 : (H + 127) / 128;
   if (NJ > ptc::MAXNJ) return fail(RNNTG_E_VALUE, "tensor-core executor: vocab + durations <= 2048");
   if (NG > 64) return fail(RNNTG_E_VALUE, "tensor-core executor: too many gate tiles");
-  std::vector<int4> roles;
-  for (int t = 0; t < NJ; ++t) roles.push_back(make_int4(ptc::ROLE_J, 0, t, 0));
-  for (int t = 0; t < NP; ++t) roles.push_back(make_int4(ptc::ROLE_P, 0, t, 0));
-  for (int l = 0; l < L; ++l) {
-    for (int t = 0; t < NG; ++t) roles.push_back(make_int4(ptc::ROLE_R, l, t, 0));
-    for (int t = 0; t < NG; ++t) roles.push_back(make_int4(ptc::ROLE_I, l, t, 0));  // I_0: the layer-0 cell
-  }
-  roles.push_back(make_int4(ptc::ROLE_E, 0, 0, 0));
-  const int G = (int)roles.size();
   int nsm = 0, optin = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
+  // split0: the layer-0 cell on its own (weightless) I_0 CTAs and the
+  // hypotheses on an emitter CTA (E) -- the shortest per-step chain; else the
+  // cell merged into R_0 and the emitter into R_{L-1} tile 0 (fewer CTAs).
+  // Two row groups or more and room for two merged CTA sets: two instances,
+  // each decoding half of the groups on its own SMs.
+  const int g_merged = NJ + NP + NG * (2 * L - 1);
+  const int ninst = allow_inst && ngrp >= 2 && 2 * g_merged <= nsm && !env_flag("RNNTG_ONE_INST", false) ? 2 : 1;
+  const int split0 = ninst > 1 || env_flag("RNNTG_MERGE0", false) ? 0 : 1;
+  std::vector<int4> roles;
+  int ic0[ptc::MAXI + 1] = {0, 0, 0};
+  for (int i = 0; i < ninst; ++i) {
+    ic0[i] = (int)roles.size();
+    for (int t = 0; t < NJ; ++t) roles.push_back(make_int4(ptc::ROLE_J, i << 8, t, 0));
+    for (int t = 0; t < NP; ++t) roles.push_back(make_int4(ptc::ROLE_P, i << 8, t, 0));
+    for (int l = 0; l < L; ++l) {
+      for (int t = 0; t < NG; ++t) roles.push_back(make_int4(ptc::ROLE_R, l | (i << 8), t, 0));
+      if (l > 0 || split0)
+        for (int t = 0; t < NG; ++t) roles.push_back(make_int4(ptc::ROLE_I, l | (i << 8), t, 0));
+    }
+    if (split0) roles.push_back(make_int4(ptc::ROLE_E, i << 8, 0, 0));
+  }
+  ic0[ninst] = (int)roles.size();
+  const int G = (int)roles.size();
   if (G > nsm) return fail(RNNTG_E_VALUE, "tensor-core executor needs one SM per weight tile");
   const int KCmax = std::max(Hp, Jp) / 64;
   d->tsmem = ptc::smem_bytes(KCmax);
@@ -573,7 +587,7 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   std::vector<unsigned char> img((size_t)G * wstride, 0);
   std::vector<float> row(ptc::MAXKP);
   for (int c = 0; c < G; ++c) {
-    const int role = roles[c].x, l = roles[c].y, t = roles[c].z;
+    const int role = roles[c].x, l = roles[c].y & 0xff, t = roles[c].z;
     if (role == ptc::ROLE_E || (role == ptc::ROLE_I && l == 0)) {  // no weights
       const float one = 1.0f;
       std::memcpy(&roles[c].w, &one, 4);
@@ -658,6 +672,12 @@ rnntg_status setup_tc(rnntg_decoder* d) {
   tp.Gg = M.G;
   tp.max_iters = d->st.max_iters;
   tp.ngrp = ngrp;
+  tp.split0 = split0;
+  tp.ninst = ninst;
+  for (int i = 0; i <= ninst; ++i) {
+    tp.ic0[i] = ic0[i];
+    tp.ig0[i] = ngrp * i / ninst;  // the instances' row groups
+  }
   for (int g = 0; g <= ngrp; ++g) tp.gr0[g] = (int)((long long)d->B * g / ngrp);
   for (int i = 0; i < D; ++i) tp.durations[i] = dd.durations[i];
   int4* droles = nullptr;
@@ -750,6 +770,8 @@ cudaError_t launch_tc(rnntg_decoder* d, cudaStream_t st) {
   // tagged argmax words carry step tags: clear them so a stale word from the
   // previous decode can never validate
   if ((e = cudaMemsetAsync(d->tp.pw, 0, d->tpw_bytes, st)) != cudaSuccess) return e;
+  // instances add their totals into the control block
+  if (d->tp.ninst > 1 && (e = cudaMemsetAsync(d->st.ctrl, 0, sizeof(Ctrl), st)) != cudaSuccess) return e;
   void* args[1] = {&d->tp};
   // the traced instantiation only when the event trace is on (RNNTG_PROF)
   const void* k = tc_kernel_for(d->tp.algo, d->tp.cell, d->tp.prof != nullptr);
@@ -765,7 +787,7 @@ cudaError_t launch_tc(rnntg_decoder* d, cudaStream_t st) {
 // the loop flags set from the device (cudaGraphSetConditional) or read back
 // by the host loop.
 rnntg_status setup_tc_steps(rnntg_decoder* d, bool use_cond) {
-  rnntg_status st = setup_tc(d);
+  rnntg_status st = setup_tc(d, false);  // (one instance: the loop flags read one CTA's state)
   if (st) return st;
   ptc::TParams& tp = d->tp;
   CK(d->mem.alloc(&tp.ctl, (size_t)tp.G * ptc::CTL_INTS));

@@ -13,13 +13,13 @@ x = synth.encoder_outputs(2, B, T, 1024); lens = np.full(B, T, np.int32)
 cap = D.build_decode_graph(m, DecodeAlgo.FrameSync, B, T, 5, D.Exec.Tensor)
 for _ in range(2): D.replay_decode(cap, x, lens)
 st = cap.stats()
-G = 95
+G = int(os.environ.get("Q_G", "74"))
 buf = (C.c_uint64 * (64 * G * 16))()
 check(L.rnntg_debug_trace(cap.handle, buf, 64 * G * 16))
 a = np.frombuffer(buf, np.uint64).reshape(64, G, 16).astype(np.int64)[63, :, 8:16].astype(np.float64)
 print(f"B={B} T={T}: {st['gpu_ms']:.2f} ms, {1000*st['gpu_ms']/st['joint_evals']:.2f} us per group-step")
 names = ["load", "J", "decide", "pred", "save", "(wordwait)", "(accwait)"]
-roles = [("J", 0, 9), ("P", 9, 14), ("R0", 14, 34), ("I0", 34, 54), ("R1", 54, 74), ("I1", 74, 94), ("E", 94, 95)]
+roles = [("J", 0, 9), ("P", 9, 14), ("R0", 14, 34), ("R1", 34, 54), ("I1", 54, 74)]
 print("role  " + " ".join(f"{n:>10s}" for n in names))
 for r, lo, hi in roles:
     tot = a[lo:hi, 7].mean()

@@ -14,7 +14,7 @@ x = synth.encoder_outputs(2, 32, T, 1024); lens = np.full(32, T, np.int32)
 for exn in sys.argv[1:] or ["HostLoop", "Graph"]:
     cap = D.build_decode_graph(m, DecodeAlgo.FrameSync, 32, T, 5, D.Exec[exn])
     for _ in range(2): D.replay_decode(cap, x, lens)
-    G = 95
+    G = int(os.environ.get("Q_G", "74"))
     buf = (C.c_uint64 * (64 * G * 16))()
     check(L.rnntg_debug_trace(cap.handle, buf, 64 * G * 16))
     a = np.frombuffer(buf, np.uint64).reshape(64, G, 16).astype(np.int64)
@@ -30,7 +30,7 @@ for exn in sys.argv[1:] or ["HostLoop", "Graph"]:
           f"gap median {np.median(gaps):.2f} us (min {np.min(gaps):.2f})")
     k = order[32]
     t0 = a[k, :, 0].min()
-    roles = [("J", 0, 9), ("P", 9, 14), ("R0", 14, 34), ("I0", 34, 54), ("R1", 54, 74), ("I1", 74, 94), ("E", 94, 95)]
+    roles = [("J", 0, 9), ("P", 9, 14), ("R0", 14, 34), ("R1", 34, 54), ("I1", 54, 74)]
     names = ["entry", "-", "run", "load", "decide", "pred", "jtail", "end"]
     print("  role " + " ".join(f"{n:>12s}" for n in names))
     for r, lo, hi in roles:
