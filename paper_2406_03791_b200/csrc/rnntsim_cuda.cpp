@@ -8,8 +8,11 @@
 #include <chrono>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <tuple>
 
 #include "rnntsim/errors.hpp"
 
@@ -19,37 +22,55 @@ namespace {
 
 rnntg_exec g_exec = RNNTG_EXEC_TENSOR;
 std::mutex g_mu;
+// A device model is shared by the cache entry and every decoder built on it
+// (rnntg_decoder keeps a raw pointer): it is destroyed with the last owner.
+using ModelRef = std::shared_ptr<rnntg_model>;
+ModelRef own(rnntg_model* m) { return ModelRef(m, [](rnntg_model* p) { rnntg_model_destroy(p); }); }
 // Device copies keyed by model object; an entry is reused only while the
 // object at that address still exports the same weights (a new model may be
-// constructed at a freed address), checked by a sampled fingerprint.
+// constructed at a freed address), checked by a hash of every weight.
 struct Entry {
-  rnntg_model* m = nullptr;
+  ModelRef m;
   uint64_t fp = 0;
 };
 std::map<const DecoderModel*, Entry> g_models;
 std::map<const Engine*, int64_t> g_joint_evals;
 
+// every weight, four 64-bit multiply-xorshift lanes (~4 ms for the 8.9 M
+// parameters of the Parakeet-shaped decoder)
 uint64_t fingerprint(const rnntg_dims& d, const std::vector<const float*>& w) {
-  uint64_t h = 1469598103934665603ull;
-  auto mix = [&h](uint64_t v) {
-    h ^= v;
-    h *= 1099511628211ull;
-  };
   const int64_t V1 = d.vocab + 1, H = d.hidden, E = d.embed, J = d.joint, F = d.feature;
   const int64_t G = d.cell == RNNTG_CELL_LSTM ? 4 * H : H;
   std::vector<int64_t> n = {V1 * E};
   for (int l = 0; l < d.layers; ++l) n.insert(n.end(), {(l ? H : E) * G, H * G, G});
   n.insert(n.end(), {F * J, H * J, J * V1});
   if (d.num_durations) n.push_back(J * d.num_durations);
-  mix(static_cast<uint64_t>(d.vocab) | (static_cast<uint64_t>(d.hidden) << 20) |
-      (static_cast<uint64_t>(d.cell) << 40) | (static_cast<uint64_t>(d.num_durations) << 48));
-  for (size_t i = 0; i < w.size() && i < n.size(); ++i)
-    for (int64_t e = 0; e < n[i]; e += 97) {
-      uint32_t u;
-      std::memcpy(&u, &w[i][e], 4);
-      mix(u);
+  auto mix = [](uint64_t h, uint64_t v) {
+    h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    h *= 0xbf58476d1ce4e5b9ull;
+    return h ^ (h >> 31);
+  };
+  uint64_t lane[4] = {0x243f6a8885a308d3ull, 0x13198a2e03707344ull, 0xa4093822299f31d0ull, 0x082efa98ec4e6c89ull};
+  lane[0] = mix(lane[0], static_cast<uint64_t>(d.vocab) | (static_cast<uint64_t>(d.hidden) << 20) |
+                             (static_cast<uint64_t>(d.cell) << 40) | (static_cast<uint64_t>(d.num_durations) << 48));
+  for (size_t i = 0; i < w.size() && i < n.size(); ++i) {
+    const unsigned char* b = reinterpret_cast<const unsigned char*>(w[i]);
+    const size_t bytes = static_cast<size_t>(n[i]) * 4;
+    size_t o = 0;
+    for (; o + 32 <= bytes; o += 32)
+      for (int k = 0; k < 4; ++k) {
+        uint64_t v;
+        std::memcpy(&v, b + o + 8 * k, 8);
+        lane[k] = mix(lane[k], v);
+      }
+    for (; o < bytes; o += 4) {
+      uint32_t v;
+      std::memcpy(&v, b + o, 4);
+      lane[0] = mix(lane[0], v);
     }
-  return h;
+    lane[1] = mix(lane[1], bytes);
+  }
+  return mix(mix(lane[0], lane[1]), mix(lane[2], lane[3]));
 }
 
 [[noreturn]] void raise(rnntg_status s) {
@@ -142,7 +163,7 @@ ScriptedTables scripted_tables(const ScriptedModel& sm) {
   return st;
 }
 
-rnntg_model* upload(const DecoderModel& model) {
+ModelRef upload(const DecoderModel& model) {
   std::lock_guard<std::mutex> lk(g_mu);
   rnntg_dims d{};
   std::vector<const float*> w;
@@ -152,15 +173,14 @@ rnntg_model* upload(const DecoderModel& model) {
     auto it = g_models.find(&model);
     if (it != g_models.end()) {
       if (it->second.fp == fp) return it->second.m;
-      rnntg_model_destroy(it->second.m);
-      g_models.erase(it);
+      g_models.erase(it);  // live decoders keep their own reference
     }
     const int nd = static_cast<int>(st.durs.size());
     rnntg_model* m = nullptr;
     check(rnntg_model_create_scripted(0, st.V, st.B, st.T, st.U, st.lab.data(), st.fs.data(), st.arr.data(), nd,
                                       nd ? st.durs.data() : nullptr, nd ? st.dv.data() : nullptr, &m));
-    g_models[&model] = Entry{m, fp};
-    return m;
+    g_models[&model] = Entry{own(m), fp};
+    return g_models[&model].m;
   }
   if (const auto* nm = dynamic_cast<const NeuralModel*>(&model)) {
     const RnntParams& p = nm->params();
@@ -187,13 +207,12 @@ rnntg_model* upload(const DecoderModel& model) {
   auto it = g_models.find(&model);
   if (it != g_models.end()) {
     if (it->second.fp == fp) return it->second.m;
-    rnntg_model_destroy(it->second.m);
-    g_models.erase(it);
+    g_models.erase(it);  // live decoders keep their own reference
   }
   rnntg_model* m = nullptr;
   check(rnntg_model_create(0, &d, w.data(), static_cast<int>(w.size()), &m));
-  g_models[&model] = Entry{m, fp};
-  return m;
+  g_models[&model] = Entry{own(m), fp};
+  return g_models[&model].m;
 }
 
 // bind_decode_inputs' validation (decoders.cpp:124-142) on reference Tensors.
@@ -211,17 +230,21 @@ void validate(const Tensor& x, const Tensor& out_len, int batch, int frames, int
 }
 
 struct Handle {
+  ModelRef model;  // keeps the device model alive while the decoder exists
   rnntg_decoder* d = nullptr;
   Engine* engine = nullptr;
   int batch = 0;
   ~Handle() {
-    if (d) rnntg_decoder_destroy(d);
+    if (d) rnntg_decoder_destroy(d);  // before `model` is released
   }
 };
 
 // replay_decode_timed: the decoder whose inputs this thread bound last, and
 // the decode region (CUPTI window + host clock) opened right before its launch
 thread_local Handle* t_bound = nullptr;
+// the engine of the eager call in progress (a cached decoder may have been
+// built under another engine; decode_joint_evals reports per engine)
+thread_local Engine* t_engine = nullptr;
 thread_local bool t_timed = false;
 thread_local std::chrono::steady_clock::time_point t_launch0;
 
@@ -232,9 +255,9 @@ Hypotheses read(Handle& h) {
   check(rnntg_read(h.d, cnt.data(), tok.data(), frm.data(), sc.data(), nullptr, cap));
   rnntg_stats st{};
   check(rnntg_get_stats(h.d, &st));
-  if (h.engine) {
+  if (Engine* e = t_engine ? t_engine : h.engine) {
     std::lock_guard<std::mutex> lk(g_mu);
-    g_joint_evals[h.engine] = st.joint_evals;
+    g_joint_evals[e] = st.joint_evals;
   }
   // read_emissions (decoders.cpp:97-122): total_score summed in double
   Hypotheses out(static_cast<size_t>(B));
@@ -251,12 +274,43 @@ Hypotheses read(Handle& h) {
   return out;
 }
 
+// The eager entry points reuse a captured decoder per (thread, device model,
+// algorithm, shape, executor): building one repacks and uploads the weight
+// images and captures the launch graph.  Per thread, because engines (and so
+// concurrent decodes) are per thread (engine.hpp:136-138).
+using DecKey = std::tuple<std::thread::id, const rnntg_model*, int, int, int, int, int>;
+std::map<DecKey, std::shared_ptr<CapturedDecoder>> g_decoders;
+constexpr size_t kMaxCachedDecoders = 32;
+
 Hypotheses eager(Engine& engine, const DecoderModel& model, DecodeAlgo algo, const Tensor& x,
                  const Tensor& out_len, int max_symbols) {
   if (x.rank() != 3) throw DimensionError("features must be rank 3 [batch, frames, features]");
-  CapturedDecoder cap = cuda::build_decode_graph(engine, model, algo, static_cast<int>(x.dim(0)),
-                                                 static_cast<int>(x.dim(1)), max_symbols);
-  return cuda::replay_decode(cap, x, out_len);
+  const int B = static_cast<int>(x.dim(0)), T = static_cast<int>(x.dim(1));
+  const ModelRef m = upload(model);
+  const DecKey key{std::this_thread::get_id(), m.get(), static_cast<int>(algo), B, T, max_symbols,
+                   static_cast<int>(g_exec)};
+  std::shared_ptr<CapturedDecoder> cap;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_decoders.find(key);
+    if (it != g_decoders.end()) cap = it->second;
+  }
+  if (!cap) {
+    cap = std::make_shared<CapturedDecoder>(cuda::build_decode_graph(engine, model, algo, B, T, max_symbols));
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_decoders.size() >= kMaxCachedDecoders) g_decoders.clear();
+    g_decoders[key] = cap;
+  }
+  cap->engine = &engine;
+  t_engine = &engine;
+  try {
+    Hypotheses out = cuda::replay_decode(*cap, x, out_len);
+    t_engine = nullptr;
+    return out;
+  } catch (...) {
+    t_engine = nullptr;
+    throw;
+  }
 }
 
 }  // namespace
@@ -270,8 +324,10 @@ CapturedDecoder build_decode_graph(Engine& engine, const DecoderModel& model, De
   if (max_symbols < 1) throw ValueError("max_symbols must be >= 1");
   if (algo == DecodeAlgo::TdtLabelLoop && !model.has_duration_head())
     throw StateError("duration-head decoding needs a model with a duration head");
-  rnntg_model* m = upload(model);
+  const ModelRef mref = upload(model);
+  rnntg_model* m = mref.get();
   auto h = std::make_shared<Handle>();
+  h->model = mref;
   h->engine = &engine;
   h->batch = batch;
   const int a = algo == DecodeAlgo::FrameSync ? RNNTG_ALGO_FRAME_SYNC
@@ -372,7 +428,7 @@ int64_t decode_joint_evals(const Engine& engine) {
 
 void release_models() {
   std::lock_guard<std::mutex> lk(g_mu);
-  for (auto& kv : g_models) rnntg_model_destroy(kv.second.m);
+  g_decoders.clear();  // cached decoders (live CapturedDecoders keep their own references)
   g_models.clear();
 }
 
