@@ -1061,7 +1061,9 @@ struct Epi : CfgFlags<SPEC> {
   // table0[label] rows of this thread's gate row for the next layer-0 cell
   // (issued early; consumed only in the cell, so the loads stay in flight)
   __device__ __forceinline__ void gather_table0() {
-    const int unit = lstm ? 32 * tile + (m >> 2) : 128 * tile + m, gate = lstm ? (m & 3) : 0;
+    // (units past Hp exist only in the last tile and are masked in the cell;
+    // clamped so the last table row's gather stays inside the table)
+    const int unit = min(lstm ? 32 * tile + (m >> 2) : 128 * tile + m, P.Hp - 1), gate = lstm ? (m & 3) : 0;
     // unconditional loads (rows >= B carry the blank label, a valid row): a
     // predicated load compiles to load + select and the warp stalls on it
 #pragma unroll
@@ -1668,7 +1670,7 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
             if (p == 0) {  // P0: label blank for every row
 #pragma unroll
               for (int i = 0; i < NR; ++i)
-                ih[i] = r0 + i < B ? __ldg(&P.table0[(size_t)blank * P.GH + unit * P.Gg + gate]) : 0.0f;
+                ih[i] = r0 + i < B ? __ldg(&P.table0[(size_t)blank * P.GH + min(unit, P.Hp - 1) * P.Gg + gate]) : 0.0f;
             }
 #pragma unroll
             for (int i = 0; i < NR; ++i) x[i] = (flag[r0 + i] & 2) ? ih[i] : 0.0f;

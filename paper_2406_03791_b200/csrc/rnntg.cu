@@ -102,6 +102,7 @@ struct rnntg_decoder {
   float* x_dev = nullptr;  // [B*T][Fp] pitched, zero-padded features
   EncPlan enc;             // K1 tensor maps over x_dev -> st.fp
   int* len_dev = nullptr;
+  int* len_bad = nullptr;  // set on the device when bound device lengths lie outside [0, T]
   // kernel-node argument storage (copied into the nodes at creation)
   DevModel arg_m{};
   DevState arg_s{};
@@ -1326,6 +1327,7 @@ rnntg_status rnntg_decoder_create(rnntg_model* m, int algo, int exec, int batch,
   if (!st) {
     if ((e = d->mem.alloc(&d->x_dev, (size_t)batch * max_frames * m->dm.Fp)) == cudaSuccess &&
         (e = d->mem.alloc(&d->len_dev, (size_t)batch)) == cudaSuccess &&
+        (e = d->mem.alloc(&d->len_bad, (size_t)1)) == cudaSuccess &&
         (e = cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking)) == cudaSuccess &&
         (e = cudaEventCreate(&d->ev0)) == cudaSuccess &&
         (e = cudaEventCreate(&d->ev1)) == cudaSuccess) {
@@ -1408,16 +1410,25 @@ rnntg_status rnntg_bind(rnntg_decoder* d, const float* x, const int32_t* out_len
   return RNNTG_OK;
 }
 
+// Device-resident lengths are validated on the device, in stream order (no
+// host round trip per bind): an entry outside [0, T] (decoders.cpp:136-140)
+// is clamped so the decode stays in bounds, flagged, and reported as
+// DimensionError by the next rnntg_sync / rnntg_read.
+__global__ void check_lengths_kernel(int* len, int B, int T, int* bad) {
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    const int v = len[b];
+    if (v < 0 || v > T) {
+      len[b] = v < 0 ? 0 : T;
+      atomicExch(bad, 1);
+    }
+  }
+}
+
 rnntg_status rnntg_bind_device(rnntg_decoder* d, const float* x_dev, const int32_t* len_dev) {
   if (!d) return fail(RNNTG_E_STATE, "decoder is null");
   if (!x_dev || !len_dev) return fail(RNNTG_E_DIMENSION, "null input");
   CK(cudaSetDevice(d->m->device));
-  std::vector<int32_t> lens(d->B);
-  CK(cudaMemcpyAsync(lens.data(), len_dev, sizeof(int32_t) * d->B, cudaMemcpyDeviceToHost,
-                     d->stream));
-  CK(cudaStreamSynchronize(d->stream));
-  rnntg_status st = check_lengths(d, lens.data());
-  if (st) return st;
+  rnntg_status st = RNNTG_OK;
   const size_t F = d->m->dm.F, Fp = d->m->dm.Fp;
   if (!d->subs.empty()) {
     for (size_t i = 0; i < d->subs.size(); ++i)
@@ -1431,6 +1442,8 @@ rnntg_status rnntg_bind_device(rnntg_decoder* d, const float* x_dev, const int32
                        (size_t)d->B * d->T, cudaMemcpyDeviceToDevice, d->stream));
   CK(cudaMemcpyAsync(d->len_dev, len_dev, sizeof(int32_t) * d->B, cudaMemcpyDeviceToDevice,
                      d->stream));
+  check_lengths_kernel<<<1, 256, 0, d->stream>>>(d->len_dev, d->B, d->T, d->len_bad);
+  CK(cudaGetLastError());
   d->bound = true;
   return RNNTG_OK;
 }
@@ -1511,6 +1524,14 @@ rnntg_status rnntg_sync(rnntg_decoder* d) {
     if (st) return st;
   }
   if (!d->subs.empty()) return RNNTG_OK;
+  if (d->len_bad) {  // device-bound lengths out of range (rnntg_bind_device)
+    int bad = 0;
+    CK(cudaMemcpy(&bad, d->len_bad, sizeof(int), cudaMemcpyDeviceToHost));
+    if (bad) {
+      CK(cudaMemset(d->len_bad, 0, sizeof(int)));
+      return fail(RNNTG_E_DIMENSION, "out_len entries must lie in [0, frames]");
+    }
+  }
   if (d->launched) {
     int err = 0;
     CK(cudaMemcpy(&err, &d->st.ctrl->err, sizeof(int), cudaMemcpyDeviceToHost));

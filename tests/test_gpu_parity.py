@@ -372,3 +372,32 @@ def test_tensor_logits_vs_oracle(B, tdt, step):
         assert derr < RTOL, derr
     cap.close()
     m.close()
+
+
+def test_bind_device_lengths_checked_on_device():
+    """rnntg_bind_device validates device-resident lengths without a host round
+    trip (decoders.cpp:136-140): an out-of-range entry surfaces as
+    DimensionError at the next sync, the decoder stays usable afterwards."""
+    _need_gpu()
+    import torch
+    from paper_2406_03791_b200 import errors
+    from paper_2406_03791_b200._lib import check, lib
+    d = O.Dims(29, 32, 32, 24, 16, (), O.CELL_LSTM, 2)
+    p = O.init_params(1, d)
+    B, T = 4, 8
+    x = O.fill_uniform(2, -1.0, 1.0, (B, T, d.feature))
+    m = Model(to_model_dims(d), p)
+    cap = D.build_decode_graph(m, DecodeAlgo.FrameSync, B, T, 3, D.Exec.Tensor)
+    L = lib()
+    xd = torch.from_numpy(x).cuda()
+    bad = torch.tensor([8, 9, 3, 0], dtype=torch.int32).cuda()
+    check(L.rnntg_bind_device(cap.handle, P._lib.C.c_void_p(xd.data_ptr()), P._lib.C.c_void_p(bad.data_ptr())))
+    check(L.rnntg_launch(cap.handle))
+    with pytest.raises(errors.DimensionError):
+        check(L.rnntg_sync(cap.handle))
+    good = np.array([8, 5, 3, 0], np.int32)
+    got = D.replay_decode(cap, x, good)
+    rep = compare_batch(got, O.decode_batch(d, p, x, good, 3, False, record=True), d.vocab, False, "after")
+    assert rep.ok, rep.failures
+    cap.close()
+    m.close()
