@@ -376,9 +376,23 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent, step
 
 
 def measure_alt_exec(args, L_, model, cfg, xd, ld, Bl, T, frames_all):
-    """Time the other executors on the same inputs."""
-    return [measure_exec(other, L_, model, cfg, xd, ld, Bl, T, frames_all)
-            for other in ("tensor", "persistent", "graph", "graph_ffma", "hostloop") if other != args.exec]
+    """Time the other executors on the same inputs (graph_k1: the graph with
+    one decision per kernel-node launch, RNNTG_GRAPH_STEPS=1)."""
+    out = []
+    for other in ("tensor", "persistent", "graph", "graph_k1", "graph_ffma", "hostloop"):
+        if other == args.exec:
+            continue
+        if other == "graph_k1":
+            os.environ["RNNTG_GRAPH_STEPS"] = "1"
+            try:
+                r = measure_exec("graph", L_, model, cfg, xd, ld, Bl, T, frames_all)
+            finally:
+                os.environ.pop("RNNTG_GRAPH_STEPS", None)
+            r["exec"] = "graph_k1"
+            out.append(r)
+        else:
+            out.append(measure_exec(other, L_, model, cfg, xd, ld, Bl, T, frames_all))
+    return out
 
 
 def measure_exec(other, L_, model, cfg, xd, ld, Bl, T, frames_all):

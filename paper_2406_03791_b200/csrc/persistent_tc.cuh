@@ -183,6 +183,7 @@ struct TParams {
   int* ctl;                   // [G][CTL_INTS] each CTA's replicated control state between step launches
   cudaGraphConditionalHandle h_outer, h_inner;
   int use_cond;               // set the conditional handles (graph bodies)
+  int steps_per_launch;       // STEP_ONE: decisions per live group per launch (the loop body unrolled)
   int split0;                 // 1: layer-0 cell on its own CTAs (I_0) + an emitter CTA (E); 0: merged into R_0
   // instances: independent CTA sets, each decoding its own row groups
   // (roles[c].y >> 8 = instance); groups [ig0[i], ig0[i+1]), CTAs [ic0[i], ic0[i+1])
@@ -688,7 +689,10 @@ struct Epi : CfgFlags<SPEC> {
   // the emitter (merges the J partials: scores, hypotheses): R_{L-1} tile 0,
   // a CTA off the per-step chain (J tile 0 for one-layer models)
   const bool is_emitter;
-  const bool words_prev;  // step launches with J rotated: step s's words / partials come from the previous launch
+  // step launches, a group's first visit of the launch: its words / partials
+  // (J rotated) and hh_l come from earlier launches (ordered by the kernel
+  // boundary), so those waits are skipped; later visits in the same launch wait
+  bool words_prev = false;
   const bool tracer;  // event-trace CTA (single-group decodes only)
   // ---- the current item's group (set_group) ----
   int g = 0, B = 0, row0 = 0;
@@ -719,7 +723,7 @@ struct Epi : CfgFlags<SPEC> {
         r0m(!FORCE_SPLIT0 && !P_.split0 && role_ == ROLE_R && layer_ == 0),
         is_emitter(P_.split0 ? role_ == ROLE_E
                    : P_.L > 1 ? (role_ == ROLE_R && layer_ == P_.L - 1 && tile_ == 0) : (role_ == ROLE_J && tile_ == 0)),
-        words_prev(P_.step_mode == STEP_ONE && STEP_JROT),
+
         tracer(PPROF(P_) && P_.ngrp == 1 && (int)blockIdx.x == P_.prof_first[role_]) {}
 
   __device__ __forceinline__ int& gsc(int which) const { return sm.grp[which * MAXG + g]; }
@@ -1344,16 +1348,19 @@ struct Epi : CfgFlags<SPEC> {
     }
     bool acc_round = false, fend_round = false;
     if (mode != STEP_INIT) {
-      for (;;) {
+      for (int rnd = 0;; ++rnd) {
         bool any = false;
         for (int gg = P.ig0[inst]; gg < P.ig0[inst + 1]; ++gg) {
           if (!sm.grp[GS_RUN * MAXG + gg]) continue;
           any = true;
           set_group(gg);
+          words_prev = mode == STEP_ONE && STEP_JROT && rnd == 0;
+          if (STAMPS && mode == STEP_NONE) sslot = (int)s;  // whole-decode launches: one slot per step
           long long tp0 = clk();
           load(multi ? LD_MULTI : LD_VISIT);
           if (STAMPS) { const long long t = clk(); ph[0] += t - tp0; tp0 = t; }
           if (et == 0 && gg == 0) stamp(P, sslot, 3);
+          if (STAMPS && role == ROLE_J && et == 0 && gg == 0) stamp(P, sslot, 1);  // (J: before its joint)
           // step launches run J at the END of a visit (the next step's joint,
           // so J's weight load overlaps the decision + prediction chain)
           if (role == ROLE_J && (mode == STEP_NONE || !STEP_JROT)) joint_round();
@@ -1392,7 +1399,7 @@ struct Epi : CfgFlags<SPEC> {
           epi_sync();
           if (STAMPS) ph[4] += clk() - tp0;
         }
-        if (!any || mode == STEP_ONE) break;
+        if (!any || (mode == STEP_ONE && rnd + 1 >= P.steps_per_launch)) break;
       }
     }
     if (STAMPS && mode == STEP_NONE && et == 0) {
@@ -1628,7 +1635,7 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
     auto load_hh = [&](int pe, float (&x)[NR]) {
       if (pe > 0) {
         // (step launches: R_l wrote hh_l(pe) in an earlier launch, ordered by the kernel boundary)
-        if (P.step_mode != STEP_ONE) wait_counter(cidx_hh(layer, tile), (unsigned)pe);
+        if (!words_prev) wait_counter(cidx_hh(layer, tile), (unsigned)pe);
         const float* hb = P.hh[layer] + ((size_t)(2 * g + (pe & 1)) * 64 + tile) * 32 * 128;
 #pragma unroll
         for (int i = 0; i < NR; ++i) x[i] = __ldcg(&hb[(r0 + i) * 128 + m]);
