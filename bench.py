@@ -565,6 +565,11 @@ def main():
     dims = ModelDims(V, H, H, J, F, durs, "lstm", L)
     model = Model.from_seed(dims, 1, device=local, blank_bias=args.blank_bias)
     L_ = lib()
+    # CUPTI first: kernels in the conditional bodies of a graph instantiated
+    # before the first activity session are missing from its records
+    _b, _s, _n = C.c_double(), C.c_double(), C.c_int64()
+    if L_.rnntg_trace_begin() == 0:
+        L_.rnntg_trace_end(C.byref(_b), C.byref(_s), C.byref(_n))
     dh = C.c_void_p()
     rc = L_.rnntg_decoder_create(model.handle, ALGO_ID[algo], EXEC_ID[args.exec], Bl, T, ms,
                                  C.byref(dh))

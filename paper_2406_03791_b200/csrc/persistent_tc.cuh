@@ -1306,8 +1306,24 @@ struct Epi : CfgFlags<SPEC> {
   // group, LD_MULTI with several (the state of the visited group moves from
   // global memory into registers first); save() moves it back (several
   // groups only).
-  template <typename Pred, typename Idle, typename Load, typename Save>
-  __device__ void run(Pred&& pred, Idle&& idle, Load&& load, Save&& save) {
+  // the next live group of this instance after the current one (round-robin order)
+  __device__ __forceinline__ int next_live() const {
+    const int n = P.ig0[inst + 1] - P.ig0[inst];
+    for (int k = 1; k <= n; ++k) {
+      const int gg = P.ig0[inst] + (g - P.ig0[inst] + k) % n;
+      if (sm.grp[GS_RUN * MAXG + gg]) return gg;
+    }
+    return g;
+  }
+  // lag: with several live groups, P and the pure R roles leave their MMA
+  // running and finish the previous group's epilogue on their next visit,
+  // after its decision (fin), so the visit does not span the upstream chain
+  // (not in the P0 pass: no visit in between would finish the lagged epilogue)
+  bool in_init = false;
+  __device__ __forceinline__ bool lag_ok() const { return P.step_mode == STEP_NONE && !in_init && next_live() != g; }
+
+  template <typename Pred, typename Idle, typename Load, typename Save, typename Fin>
+  __device__ void run(Pred&& pred, Idle&& idle, Load&& load, Save&& save, Fin&& fin) {
     const int mode = P.step_mode;
     // with several groups or step launches, the per-thread state of a group
     // lives in global memory between its visits
@@ -1320,6 +1336,10 @@ struct Epi : CfgFlags<SPEC> {
     // except I_1, the first MMA after the decision, which loads before it
     const bool has_w = role != ROLE_E && !(role == ROLE_I && layer == 0);
     if (has_w && (WEAGER || (role == ROLE_I && layer == 1) || (role == ROLE_R && layer == 0 && !r0m))) load_weights();
+    if (mode != STEP_ONE) {  // (shared memory is not zeroed at launch: no stale running flags)
+      for (int i = et; i < GS_N * MAXG; i += NEPI) sm.grp[i] = 0;
+      epi_sync();
+    }
     if (mode == STEP_ONE) {
       load_ctl();
       sslot = sm.grp[GS_STEP * MAXG];
@@ -1329,6 +1349,7 @@ struct Epi : CfgFlags<SPEC> {
       }
     } else {
       if (has_w && !wloaded) load_weights();
+      in_init = true;
       for (int gg = P.ig0[inst]; gg < P.ig0[inst + 1]; ++gg) {
         set_group(gg);
         init_rows();
@@ -1345,6 +1366,7 @@ struct Epi : CfgFlags<SPEC> {
         save_group();
         epi_sync();
       }
+      in_init = false;
     }
     bool acc_round = false, fend_round = false;
     if (mode != STEP_INIT) {
@@ -1366,6 +1388,7 @@ struct Epi : CfgFlags<SPEC> {
           if (role == ROLE_J && (mode == STEP_NONE || !STEP_JROT)) joint_round();
           if (STAMPS) { const long long t = clk(); ph[1] += t - tp0; tp0 = t; }
           decide();
+          fin();  // a lagged epilogue of the previous visit
           if (STAMPS) { const long long t = clk(); ph[2] += t - tp0; tp0 = t; }
           if (has_w && !wloaded && !r0m) load_weights();  // (merged R_0: after its cell, in pred)
           if (et == 0 && gg == 0) stamp(P, sslot, 4);
@@ -1402,6 +1425,7 @@ struct Epi : CfgFlags<SPEC> {
         if (!any || (mode == STEP_ONE && rnd + 1 >= P.steps_per_launch)) break;
       }
     }
+    fin();
     if (STAMPS && mode == STEP_NONE && et == 0) {
       ph[7] = clk() - ph[7];
       for (int i = 0; i < 8; ++i) stamp_at(P, 63, 8 + i, (unsigned long long)ph[i]);
@@ -1544,7 +1568,7 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
   auto nop = [&]() {};
   auto nopl = [&](int) {};
   if (role == ROLE_J || role == ROLE_E) {
-    run([&](long long) {}, [&](long long) {}, nopl, nop);
+    run([&](long long) {}, [&](long long) {}, nopl, nop, nop);
   } else if (role == ROLE_P) {
     float gp[NR], fpv[NR];
 #pragma unroll
@@ -1563,7 +1587,7 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
         fpv[i] = __ldg(&P.fp[((size_t)(row0 + r) * P.T + t) * P.Jp + min(j, P.Jp - 1)]);
       }
     };
-    auto trunk = [&](long long te) {  // trunk(te) = relu(fp + gp) -> act[TRUNK]
+    auto trunk = [&](long long te, const float (&gpa)[NR]) {  // trunk(te) = relu(fp + gp) -> act[TRUNK]
       mark(32);
       unsigned char* stage = reinterpret_cast<unsigned char*>(sm.xs);  // [2][CHUNK] staging
       if (j < P.Jp) {
@@ -1571,7 +1595,7 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
 #pragma unroll
         for (int i = 0; i < NR; ++i) {
           const int r = r0 + i;
-          const float x = (r < B && j < P.J) ? fmaxf(fpv[i] + gp[i], 0.0f) : 0.0f;
+          const float x = (r < B && j < P.J) ? fmaxf(fpv[i] + gpa[i], 0.0f) : 0.0f;
           store_split(ch, r, j & 63, x);
         }
       }
@@ -1580,9 +1604,31 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
       publish_chunks(stage, min(2, P.act_kc[TRUNK] - cb), cidx_act(TRUNK, cb), TRUNK, cb, (int)(te & 1));
       gmark(40);
     };
+    // a lagged pred (several live groups): its trunk finished on the next visit
+    int pend_r = -1, pend_g = 0;
+    long long pend_te = 0;
+    auto finish_pending = [&]() {
+      if (pend_r < 0) return;
+      const int gcur = g;
+      set_group(pend_g);  // (the current group's decision left its s / p untouched)
+      float v[NR];
+      prefetch();
+      read_acc(pend_r, v);
+      trunk(pend_te, v);
+#pragma unroll
+      for (int i = 0; i < NR; ++i) *gstate(i) = v[i];  // the group's gp
+      pend_r = -1;
+      set_group(gcur);
+    };
     run(
         [&](long long te) {
           post(p);
+          if (lag_ok()) {
+            pend_r = round - 1;
+            pend_g = g;
+            pend_te = te;
+            return;
+          }
           prefetch();
           float v[NR];
           read_acc(round - 1, v);
@@ -1590,13 +1636,13 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
           log_ld(51);
 #pragma unroll
           for (int i = 0; i < NR; ++i) gp[i] = v[i];
-          trunk(te);
+          trunk(te, gp);
           mark(14);
           mark_pub();
         },
         [&](long long te) {
           prefetch();
-          trunk(te);
+          trunk(te, gp);
         },
         [&](int mode) {
 #pragma unroll
@@ -1605,21 +1651,39 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
         [&]() {
 #pragma unroll
           for (int i = 0; i < NR; ++i) *gstate(i) = gp[i];
-        });
+        },
+        finish_pending);
   } else if (role == ROLE_R && !r0m) {
-    // hh_l(p+1) = h_l(p) @ W_hh_l -> global, for the layer-l cell of the next prediction
+    // hh_l(p+1) = h_l(p) @ W_hh_l -> global, for the layer-l cell of the next
+    // prediction; lagged to the next visit while other groups are live
+    int pend_r = -1, pend_g = 0, pend_p = 0;
+    auto store_hh = [&](int r, int gq, int pq) {
+      float v[NR];
+      read_acc(r, v);
+      float* hb = P.hh[layer] + ((size_t)(2 * gq + ((pq + 1) & 1)) * 64 + tile) * 32 * 128;
+#pragma unroll
+      for (int i = 0; i < NR; ++i) hb[(r0 + i) * 128 + m] = v[i];
+      epi_sync();  // every thread's stores, then thread 0's release
+      if (et == 0) red_release_add(P.cnt + (size_t)gq * NCOUNTERS * CSTRIDE + (size_t)cidx_hh(layer, tile) * CSTRIDE, 1);
+    };
     run(
         [&](long long) {
           post(p);
-          float v[NR];
-          read_acc(round - 1, v);
-          float* hb = P.hh[layer] + ((size_t)(2 * g + ((p + 1) & 1)) * 64 + tile) * 32 * 128;
-#pragma unroll
-          for (int i = 0; i < NR; ++i) hb[(r0 + i) * 128 + m] = v[i];
-          bump(cidx_hh(layer, tile));
+          if (lag_ok()) {
+            pend_r = round - 1;
+            pend_g = g;
+            pend_p = p;
+            return;
+          }
+          store_hh(round - 1, g, p);
           mark_pub();
         },
-        [&](long long) {}, nopl, nop);
+        [&](long long) {}, nopl, nop,
+        [&]() {
+          if (pend_r < 0) return;
+          store_hh(pend_r, pend_g, pend_p);
+          pend_r = -1;
+        });
   } else {
     // R_0: the layer-0 cell (table0[label] + hh0 + b), then the next
     // prediction's hh0 = h0 @ W_hh0 into registers (hx); I_l: the W_ih_l MMA
@@ -1759,7 +1823,8 @@ __device__ __forceinline__ void Epi<TR, SPEC>::run_role() {
 #pragma unroll
             for (int j = 0; j < NR; ++j) *gstate(hxo + j) = hx[j];
           }
-        });
+        },
+        nop);
     flush();  // merged R_0: the last look-ahead round
   }
   post(-1);
