@@ -288,6 +288,10 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent, step
     # groups (stats count group-steps); beyond 256 as sub-decodes back to back
     n_sub = (Bl + 255) // 256 if (persistent and args.exec == "tensor" and Bl > 256) else 1
     Brow = min(Bl, 32)
+    # the stats count group-steps (<= 32 rows each); the weights of a step are
+    # read once for all ceil(B / 32) groups (on chip), so per launch the
+    # algorithmic weight bytes are those of the batch steps = group-steps / groups
+    ngrp = max(1, -(-Bl // 32)) if Bl <= 256 else 8
     V1 = V + 1
     V1p = (V1 + 15) // 16 * 16
     Dn = len(durs)
@@ -300,7 +304,7 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent, step
         "pred_proj": 4 * (Hp * Jp + Bp * Hp + Bp * Jp),
         "joint": 4 * (Jp * V1p + 2 * Bp * Jp),
         "enc_proj": 4 * (Bl * T * F + F * Jp + Bl * T * Jp),
-        "persistent": (st.pred_steps * pred_w + st.joint_evals * joint_w) / n_sub,
+        "persistent": (st.pred_steps * pred_w + st.joint_evals * joint_w) / n_sub / ngrp,
         "ptc_step": (st.pred_steps * pred_w + st.joint_evals * joint_w) / max(st.joint_evals, 1),
     }
     pred_f = 2 * Brow * (4 * H * H * (2 * L - 1) + H * J)

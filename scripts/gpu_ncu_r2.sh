@@ -9,8 +9,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   > gpurun_out/r2_launches_c2.log 2>&1; echo "launches rc=$?"
 RNNTG_LAUNCH_GRAPH=0 T=100 timeout 900 ncu --set full --import-source on --clock-control none -k regex:ptc_kernel -c 1 \
   -o gpurun_out/r2_ncu_tc -f python scripts/prof_kernels_exec.py tensor > gpurun_out/r2_ncu_tc.log 2>&1; echo "tc rc=$?"
-T=20 timeout 900 ncu --set full --import-source on --clock-control none --graph-profiling node -k regex:ptc_kernel -s 30 -c 1 \
-  -o gpurun_out/r2_ncu_step -f python scripts/prof_kernels_exec.py graph > gpurun_out/r2_ncu_step.log 2>&1; echo "step rc=$?"
+# the graph executor's body kernel (step launches), launched by the host loop
+# (ncu does not profile kernels in conditional-node bodies)
+T=20 timeout 900 ncu --set full --import-source on --clock-control none -k regex:ptc_kernel -s 30 -c 1 \
+  -o gpurun_out/r2_ncu_step -f python scripts/prof_kernels_exec.py hostloop > gpurun_out/r2_ncu_step.log 2>&1; echo "step rc=$?"
 T=250 timeout 900 ncu --set full --import-source on --clock-control none -k regex:encproj -c 1 \
   -o gpurun_out/r2_ncu_k1 -f python scripts/prof_kernels_exec.py tensor > gpurun_out/r2_ncu_k1.log 2>&1; echo "k1 rc=$?"
 ls -la gpurun_out/*.ncu-rep

@@ -10,7 +10,7 @@ import numpy as np  # noqa: E402
 from paper_2406_03791_b200 import Model, ModelDims, synth  # noqa: E402
 from paper_2406_03791_b200._lib import check, lib  # noqa: E402
 
-ex = {"graph": 0, "persistent": 1, "tensor": 2}[sys.argv[1] if len(sys.argv) > 1 else "graph"]
+ex = {"graph": 0, "persistent": 1, "tensor": 2, "hostloop": 3}[sys.argv[1] if len(sys.argv) > 1 else "graph"]
 B, T = 32, int(os.environ.get("T", 250))
 dims = ModelDims(1024, 640, 640, 640, 1024, (), "lstm", 2)
 m = Model.from_seed(dims, 1)
