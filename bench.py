@@ -334,7 +334,7 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent, step
     fp32_ach = flops_per[dom] / (kern[dom] / 1000.0) / 1e12
     # per inner step roofline (north star): max(weight bytes / HBM, FLOPs / FP32 peak)
     steps = max(st.joint_evals, 1)
-    step_bytes = (st.pred_steps * pred_w + st.joint_evals * joint_w) / steps
+    step_bytes = (st.pred_steps * pred_w + st.joint_evals * joint_w) / steps / ngrp  # (weights shared by the groups)
     step_flops = (st.pred_steps * pred_f + st.joint_evals * joint_f) / steps
     t_step = ms_per_step * 1000.0 / steps
     tensor = args.exec in ("tensor", "graph", "hostloop")
