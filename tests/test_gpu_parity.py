@@ -401,3 +401,32 @@ def test_bind_device_lengths_checked_on_device():
     assert rep.ok, rep.failures
     cap.close()
     m.close()
+
+
+@pytest.mark.parametrize("steps", [1, 3])
+@pytest.mark.parametrize("algo", [DecodeAlgo.FrameSync, DecodeAlgo.LabelLoop, DecodeAlgo.TdtLabelLoop],
+                         ids=lambda a: a.name)
+def test_graph_decisions_per_launch(steps, algo):
+    """The graph executor's WHILE body with 1 and 3 decisions per kernel-node
+    launch (RNNTG_GRAPH_STEPS; default 2 is covered by the other suites), one
+    and two row groups, against the oracle."""
+    _need_gpu()
+    tdt = algo == DecodeAlgo.TdtLabelLoop
+    d = O.Dims(150, 64, 64, 96, 24, (0, 1, 2, 3, 4) if tdt else (), O.CELL_LSTM, 2)
+    p = O.init_params(51, d)
+    T, ms = 12, 3
+    os.environ["RNNTG_GRAPH_STEPS"] = str(steps)
+    try:
+        for B in (7, 45):
+            x = O.fill_uniform(52, -1.0, 1.0, (B, T, d.feature))
+            lens = np.array([T - (5 * i) % 7 for i in range(B)], np.int32)
+            m = Model(to_model_dims(d), p)
+            cap = D.build_decode_graph(m, algo, B, T, ms, D.Exec.Graph)
+            got = D.replay_decode(cap, x, lens)
+            rep = compare_batch(got, O.decode_batch(d, p, x, lens, ms, tdt, record=True), d.vocab, tdt,
+                                f"K{steps}/B{B}")
+            assert rep.ok, rep.failures[:5]
+            cap.close()
+            m.close()
+    finally:
+        os.environ.pop("RNNTG_GRAPH_STEPS", None)
