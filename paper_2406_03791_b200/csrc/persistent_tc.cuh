@@ -110,10 +110,14 @@ constexpr int NROLES = 5;
 // branch between the two forms inside the unrolled loop cost ~2 us/step, so the
 // MMA warp dispatches once per round to a body templated on the chunk count.
 constexpr bool SWAP_HILO = true;  // W_hi in TMEM, W_lo (mostly) in smem: the packing convention
-constexpr int ACC_COLS = 96;      // [x_hi | x_lo | lo.x_hi] (one set)
+#ifndef ACC64
+#define ACC64 1  // W_lo.A_hi accumulates into the A_hi columns of W_hi.[A_hi | A_lo]: 64-column accumulator
+#endif
+constexpr int ACC_COLS = ACC64 ? 64 : 96;  // [hi.x_hi (+ lo.x_hi) | hi.x_lo] (| lo.x_hi)
 constexpr int NACC = 1;           // accumulator sets (two measured 0.05 us/step slower)
 constexpr int WLO_COL = NACC * ACC_COLS;  // first TMEM weight column
-constexpr int MAXNLO = (512 - WLO_COL) / 32 / 2;  // 6: bound of nlo_chunks over KC
+constexpr int MAXNLO = (512 - WLO_COL) / 32 / 2;  // 7 (ACC64) / 6: bound of nlo_chunks over KC
+static_assert(MAXNLO <= 7, "mma_round dispatch covers nlo 0..6 and MAXNLO");
 #ifndef NLO_MAX
 #define NLO_MAX MAXNLO  // A/B knob: cap on the TMEM-resident W_lo chunks
 #endif
@@ -241,16 +245,17 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
 // and the MMA warp's issue rate paced the phases (A/B -0.23 us/step).  first:
 // the chunk starts the tile (its MMAs overwrite D1 / D2).
 __device__ __forceinline__ void mma_chunk_ts2(uint32_t d1, uint32_t d2, uint32_t ahi, uint64_t alo, uint64_t b,
-                                              uint32_t first, uint32_t id64, uint32_t id32, uint64_t* bar) {
+                                              uint32_t first, uint32_t id64, uint32_t id32, uint64_t* bar,
+                                              uint32_t first2) {
   asm volatile(
-      "{\n\t.reg .pred p, t, e;\n\t.reg .b32 h1, h2, h3;\n\t.reg .b64 l1, l2, l3, b1, b2, b3;\n\t"
-      "setp.eq.b32 p, %5, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+      "{\n\t.reg .pred p, q, t, e;\n\t.reg .b32 h1, h2, h3;\n\t.reg .b64 l1, l2, l3, b1, b2, b3;\n\t"
+      "setp.eq.b32 p, %5, 0;\n\tsetp.eq.b32 q, %9, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
       "add.u32 h1, %2, 8;\n\tadd.u32 h2, %2, 16;\n\tadd.u32 h3, %2, 24;\n\t"
       "add.u64 l1, %3, 2;\n\tadd.u64 l2, %3, 4;\n\tadd.u64 l3, %3, 6;\n\t"
       "add.u64 b1, %4, 2;\n\tadd.u64 b2, %4, 4;\n\tadd.u64 b3, %4, 6;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %4, %6, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], %3, %4, %7, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], %3, %4, %7, q;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h1], b1, %6, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%1], l1, b1, %7, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h2], b2, %6, t;\n\t"
@@ -258,21 +263,22 @@ __device__ __forceinline__ void mma_chunk_ts2(uint32_t d1, uint32_t d2, uint32_t
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h3], b3, %6, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%1], l3, b3, %7, t;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n\t}" ::"r"(d1),
-      "r"(d2), "r"(ahi), "l"(alo), "l"(b), "r"(first), "r"(id64), "r"(id32), "r"(smem_u32(bar))
+      "r"(d2), "r"(ahi), "l"(alo), "l"(b), "r"(first), "r"(id64), "r"(id32), "r"(smem_u32(bar)), "r"(first2)
       : "memory");
 }
 // TS x TS chunk with the W_lo product in its own columns d2 (A_lo from TMEM)
 __device__ __forceinline__ void mma_chunk_tt2(uint32_t d1, uint32_t d2, uint32_t ahi, uint32_t alo, uint64_t b,
-                                              uint32_t first, uint32_t id64, uint32_t id32, uint64_t* bar) {
+                                              uint32_t first, uint32_t id64, uint32_t id32, uint64_t* bar,
+                                              uint32_t first2) {
   asm volatile(
-      "{\n\t.reg .pred p, t, e;\n\t.reg .b32 h1, h2, h3, l1, l2, l3;\n\t.reg .b64 b1, b2, b3;\n\t"
-      "setp.eq.b32 p, %5, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+      "{\n\t.reg .pred p, q, t, e;\n\t.reg .b32 h1, h2, h3, l1, l2, l3;\n\t.reg .b64 b1, b2, b3;\n\t"
+      "setp.eq.b32 p, %5, 0;\n\tsetp.eq.b32 q, %9, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
       "add.u32 h1, %2, 8;\n\tadd.u32 h2, %2, 16;\n\tadd.u32 h3, %2, 24;\n\t"
       "add.u32 l1, %3, 8;\n\tadd.u32 l2, %3, 16;\n\tadd.u32 l3, %3, 24;\n\t"
       "add.u64 b1, %4, 2;\n\tadd.u64 b2, %4, 4;\n\tadd.u64 b3, %4, 6;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %4, %6, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], [%3], %4, %7, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], [%3], %4, %7, q;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h1], b1, %6, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%1], [l1], b1, %7, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h2], b2, %6, t;\n\t"
@@ -280,7 +286,7 @@ __device__ __forceinline__ void mma_chunk_tt2(uint32_t d1, uint32_t d2, uint32_t
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h3], b3, %6, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%1], [l3], b3, %7, t;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n\t}" ::"r"(d1),
-      "r"(d2), "r"(ahi), "r"(alo), "l"(b), "r"(first), "r"(id64), "r"(id32), "r"(smem_u32(bar))
+      "r"(d2), "r"(ahi), "r"(alo), "l"(b), "r"(first), "r"(id64), "r"(id32), "r"(smem_u32(bar)), "r"(first2)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -850,14 +856,21 @@ struct Epi : CfgFlags<SPEC> {
     tc_fence_after();
     const uint32_t a = tq + set * ACC_COLS + r0;
     {
-      uint32_t x0[NR], x1[NR], x2[NR];
+      uint32_t x0[NR], x1[NR];
       tmem_ldn(a, x0);
       tmem_ldn(a + 32, x1);
-      tmem_ldn(a + 64, x2);
-      tmem_wait_ld();
+      if (ACC64) {
+        tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < NR; ++i)
-        v[i] = (__uint_as_float(x0[i]) + (__uint_as_float(x1[i]) + __uint_as_float(x2[i]))) * wsc;
+        for (int i = 0; i < NR; ++i) v[i] = (__uint_as_float(x0[i]) + __uint_as_float(x1[i])) * wsc;
+      } else {
+        uint32_t x2[NR];
+        tmem_ldn(a + 64, x2);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < NR; ++i)
+          v[i] = (__uint_as_float(x0[i]) + (__uint_as_float(x1[i]) + __uint_as_float(x2[i]))) * wsc;
+      }
     }
     tc_fence_before();
     __syncwarp();
@@ -1853,7 +1866,8 @@ template <int NLO, bool TR>
 __device__ __forceinline__ void mma_round(const TParams& P, const Smem& sm, uint32_t& fb, int KC, uint32_t tmem,
                                           uint32_t whi0, uint32_t ring0, bool ctr, bool tr, int e) {
   constexpr uint32_t ID64 = idesc_f16(128, 64), ID32 = idesc_f16(128, 32);
-  const uint32_t d1 = tmem, d2 = tmem + 64;
+  const uint32_t d1 = tmem, d2 = ACC64 ? tmem : tmem + 64;
+  const uint32_t f2 = ACC64 ? 0u : 1u;  // (ACC64: the W_lo product always accumulates)
 #pragma unroll  // (a rolled loop measured 0.45 us/step slower)
   for (int kc = 0; kc < MAXKC; ++kc) {
     if (kc < KC) {
@@ -1866,10 +1880,10 @@ __device__ __forceinline__ void mma_round(const TParams& P, const Smem& sm, uint
       const uint64_t bd = sdesc_sw128(ring0 + st * CHUNK);
       if (kc < NLO)
         mma_chunk_tt2(d1, d2, tmem + WLO_COL + kc * 32, tmem + WLO_COL + (KC + kc) * 32, bd, kc == 0, ID64, ID32,
-                      &sm.empty[st]);
+                      &sm.empty[st], f2 & (kc == 0));
       else
         mma_chunk_ts2(d1, d2, tmem + WLO_COL + kc * 32, sdesc_sw128(whi0 + kc * 16384), bd, kc == 0, ID64, ID32,
-                      &sm.empty[st]);
+                      &sm.empty[st], f2 & (kc == 0));
     }
   }
 }
@@ -2034,6 +2048,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
         case 3: mma_round<3, TR>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
         case 4: mma_round<4, TR>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
         case 5: mma_round<5, TR>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
+        case 6: mma_round<6, TR>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
         default: mma_round<MAXNLO, TR>(P, sm, fb, KC, tmem, whi0, ring0, ctr, tr, e); break;
       }
       mma_commit(&sm.accf[set]);

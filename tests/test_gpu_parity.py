@@ -158,7 +158,7 @@ def test_tensor_batch_above_kernel_limit(tdt):
     m.close()
 
 
-@pytest.mark.parametrize("H,J,tdt", [(96, 200, False), (320, 640, True), (640, 192, False)])
+@pytest.mark.parametrize("H,J,tdt", [(96, 200, False), (320, 640, True), (640, 192, False), (384, 448, True)])
 def test_tensor_mixed_chunk_counts(H, J, tdt):
     """Tensor executor with hidden and joint widths padding to different chunk
     counts (the per-CTA weight image is laid out for the larger one; W_lo is
