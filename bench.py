@@ -231,7 +231,7 @@ def run_reference_arm(args, cfg, rank, world):
     threads = min(nproc, B)
     ref_algo = {"fs": "sync_free", "ll": "label_loop", "tdt": "tdt"}[algo]
     x, _ = make_inputs(cfg, 0, threads)
-    secs_per_step = max(1.0, min(20.0, 120.0 / max(args.steps + args.warmup, 1)))
+    secs_per_step = max(0.2, min(20.0, args.cpu_seconds, 120.0 / max(args.steps + args.warmup, 1)))
     _, s2 = m.decode(ref_algo, np.ascontiguousarray(x[:, :2]), np.full(threads, 2, np.int32), ms, threads)
     Ts = int(max(2, min(T, 2 * secs_per_step / max(s2, 1e-3))))
     xs = np.ascontiguousarray(x[:, :Ts])
@@ -632,8 +632,9 @@ def main():
     tc_steps = args.exec in ("graph", "hostloop")
     if persistent:
         launches_per_step = 2
-    elif tc_steps:
-        launches_per_step = 2 + st.joint_evals
+    elif tc_steps:  # K1 + P0 + one launch per (up to RNNTG_GRAPH_STEPS) decisions
+        k = int(os.environ.get("RNNTG_GRAPH_STEPS", "2")) if args.exec == "graph" else 1
+        launches_per_step = 2 + -(-st.joint_evals // max(k, 1))
     else:
         launches_per_step = 2 + st.pred_steps * (L + 1) + st.joint_evals + (st.outer_iters if fs else 0)
     hyps_dev = read_hyps(L_, dh, Bl)  # the timed decodes' hypotheses (device-resident inputs)
