@@ -213,12 +213,6 @@ __device__ __forceinline__ void stamp(const TParams& P, int slot, int i) {
   }
 }
 enum { STEP_NONE = 0, STEP_INIT = 1, STEP_ONE = 2 };
-#ifndef FORCE_SPLIT0
-#define FORCE_SPLIT0 0  // A/B: compile the merged-R_0 paths out
-#endif
-#ifndef STEP_JROT
-#define STEP_JROT 1  // step launches: J's joint at the end of a launch (for the next step)
-#endif
 constexpr int PROF_WIN = 64;  // traced joint steps [PROF_S0, PROF_S0 + PROF_WIN)
 constexpr int PROF_S0 = 100;
 constexpr int NEV = 136;  // 40..47: globaltimer hand-off marks; 48..53: I1/P load + MMA marks;
@@ -725,8 +719,8 @@ struct Epi : CfgFlags<SPEC> {
                  int tile_, int inst_, float wsc_)
       : CfgFlags<SPEC>(P_), P(P_), sm(sm_), tq(tmem + ((uint32_t)(32 * q) << 16)), et(et_), m(32 * q + (et_ & 31)),
         r0(NR * (et_ >> 7)), role(role_),
-        layer(layer_), tile(tile_), inst(inst_), wsc(wsc_), blank(P_.V1 - 1), c0((FORCE_SPLIT0 || P_.split0) ? (role_ == ROLE_I && layer_ == 0) : (role_ == ROLE_R && layer_ == 0)),
-        r0m(!FORCE_SPLIT0 && !P_.split0 && role_ == ROLE_R && layer_ == 0),
+        layer(layer_), tile(tile_), inst(inst_), wsc(wsc_), blank(P_.V1 - 1), c0(P_.split0 ? (role_ == ROLE_I && layer_ == 0) : (role_ == ROLE_R && layer_ == 0)),
+        r0m(!P_.split0 && role_ == ROLE_R && layer_ == 0),
         is_emitter(P_.split0 ? role_ == ROLE_E
                    : P_.L > 1 ? (role_ == ROLE_R && layer_ == P_.L - 1 && tile_ == 0) : (role_ == ROLE_J && tile_ == 0)),
 
@@ -1375,7 +1369,7 @@ struct Epi : CfgFlags<SPEC> {
         if (et < 32) flag[et] &= ~2;
         if (et == 0) gsc(GS_RUN) = running0 ? 1 : 0;
         if (multi) save();
-        if (role == ROLE_J && mode == STEP_INIT && running0 && STEP_JROT) joint_round();  // step 0's joint
+        if (role == ROLE_J && mode == STEP_INIT && running0) joint_round();  // step 0's joint
         save_group();
         epi_sync();
       }
@@ -1389,7 +1383,7 @@ struct Epi : CfgFlags<SPEC> {
           if (!sm.grp[GS_RUN * MAXG + gg]) continue;
           any = true;
           set_group(gg);
-          words_prev = mode == STEP_ONE && STEP_JROT && rnd == 0;
+          words_prev = mode == STEP_ONE && rnd == 0;
           if (STAMPS && mode == STEP_NONE) sslot = (int)s;  // whole-decode launches: one slot per step
           long long tp0 = clk();
           load(multi ? LD_MULTI : LD_VISIT);
@@ -1398,7 +1392,7 @@ struct Epi : CfgFlags<SPEC> {
           if (STAMPS && role == ROLE_J && et == 0 && gg == 0) stamp(P, sslot, 1);  // (J: before its joint)
           // step launches run J at the END of a visit (the next step's joint,
           // so J's weight load overlaps the decision + prediction chain)
-          if (role == ROLE_J && (mode == STEP_NONE || !STEP_JROT)) joint_round();
+          if (role == ROLE_J && mode == STEP_NONE) joint_round();
           if (STAMPS) { const long long t = clk(); ph[1] += t - tp0; tp0 = t; }
           decide();
           fin();  // a lagged epilogue of the previous visit
@@ -1429,7 +1423,7 @@ struct Epi : CfgFlags<SPEC> {
           if (et == 0) st_relaxed_u32(P.ack + (size_t)g * P.G + blockIdx.x, (unsigned)(s + 1));
           ++s;
           if (et < 32) flag[et] &= ~2;
-          if (role == ROLE_J && mode == STEP_ONE && STEP_JROT) joint_round();  // step s + 1's joint
+          if (role == ROLE_J && mode == STEP_ONE) joint_round();  // step s + 1's joint
           if (et == 0 && gg == 0) stamp(P, sslot, 6);
           save_group();
           epi_sync();
