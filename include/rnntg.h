@@ -153,7 +153,10 @@ int rnntg_decoder_capacity(const rnntg_decoder* d);
  * (float32) and out_len[B] (int32 in [0,T]) from HOST memory (async; pinned
  * memory makes it truly asynchronous). */
 rnntg_status rnntg_bind(rnntg_decoder* d, const float* x, const int32_t* out_len);
-/* Same, from DEVICE pointers already resident on the decoder's device. */
+/* Same, from DEVICE pointers already resident on the decoder's device.  The
+ * lengths are checked on the device in stream order (no host round trip): an
+ * entry outside [0, T] is clamped for the decode and reported as
+ * RNNTG_E_DIMENSION by the next rnntg_sync / rnntg_read. */
 rnntg_status rnntg_bind_device(rnntg_decoder* d, const float* x_dev,
                                const int32_t* out_len_dev);
 /* One graph launch (replay_decode's single host launch, decoders.cpp:629-639). */
