@@ -797,12 +797,13 @@ rnntg_status setup_tc_steps(rnntg_decoder* d, bool use_cond) {
     d->tp_step[i] = tp;
     d->tp_step[i].step_mode = i == 0 ? ptc::STEP_INIT : ptc::STEP_ONE;
     d->tp_step[i].use_cond = use_cond ? 1 : 0;
-    // graph bodies run up to RNNTG_GRAPH_STEPS (default 2) decisions per
-    // launch -- the WHILE body unrolled, halving the per-launch weight reload
-    // and the conditional-node relaunch per decision; the sync-requiring host
-    // loop stays at one decision (and one flag read-back) per launch
+    // graph bodies run up to RNNTG_GRAPH_STEPS (default 3) decisions per
+    // launch -- the WHILE body unrolled, amortising the per-launch weight
+    // reload and the conditional-node relaunch (~5 us) over the decisions;
+    // the sync-requiring host loop stays at one decision (and one flag
+    // read-back) per launch
     const char* gs = getenv("RNNTG_GRAPH_STEPS");
-    d->tp_step[i].steps_per_launch = use_cond ? std::max(1, gs ? atoi(gs) : 2) : 1;
+    d->tp_step[i].steps_per_launch = use_cond ? std::max(1, gs ? atoi(gs) : 3) : 1;
   }
   d->tc_steps = true;
   return RNNTG_OK;
