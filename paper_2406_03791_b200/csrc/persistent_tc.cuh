@@ -188,6 +188,7 @@ struct TParams {
   cudaGraphConditionalHandle h_outer, h_inner;
   int use_cond;               // set the conditional handles (graph bodies)
   int steps_per_launch;       // STEP_ONE: decisions per live group per launch (the loop body unrolled)
+  int pdl;                    // step launches as programmatic dependents: weights before griddepcontrol.wait
   int split0;                 // 1: layer-0 cell on its own CTAs (I_0) + an emitter CTA (E); 0: merged into R_0
   // instances: independent CTA sets, each decoding its own row groups
   // (roles[c].y >> 8 = instance); groups [ig0[i], ig0[i+1]), CTAs [ic0[i], ic0[i+1])
@@ -487,6 +488,9 @@ __device__ __forceinline__ void release_after_bulk() {
   if (MM_PROD == 1 || MM_PROD == 3) asm volatile("fence.acq_rel.gpu;" ::: "memory");
   if (MM_PROD == 4) asm volatile("fence.release.gpu;" ::: "memory");
 }
+#ifndef PUB_DIRECT
+#define PUB_DIRECT 1  // activation hand-offs: plain stores + release (0: TMA store + wait_group + release)
+#endif
 #ifndef PUB_ET
 #define PUB_ET 0  // epilogue thread that issues the activation bulk stores + publish
 #endif
@@ -889,6 +893,25 @@ struct Epi : CfgFlags<SPEC> {
   // counter adds.  stage [n][CHUNK] -> chunks kc0 .. kc0+n-1, counters ci..
   __device__ __forceinline__ void publish_chunks(const unsigned char* stage, int n, int ci, int buf, int kc0,
                                                  int par) {
+    if (PUB_DIRECT) {
+      // plain 16-byte stores from the staged chunks (smem swizzle undone),
+      // then the same release + counter adds as the R roles' hh hand-off
+      epi_sync();
+      const int Kp = P.act_kc[buf] * 64;
+      unsigned char* gbase = P.act[buf] + ((size_t)(2 * g + par) * 64 * Kp + 64 * kc0) * 2;
+      for (int i = et; i < n * 512; i += NEPI) {
+        const int c = i >> 9, r = (i >> 3) & 63, sg = i & 7;
+        const uint4 v = *reinterpret_cast<const uint4*>(stage + (size_t)c * CHUNK + r * 128 + ((sg ^ (r & 7)) << 4));
+        *reinterpret_cast<uint4*>(gbase + ((size_t)r * Kp + 64 * c + 8 * sg) * 2) = v;
+      }
+      epi_sync();
+      if (et == 0) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("fence.release.gpu;" ::: "memory");
+        for (int c = 0; c < n; ++c) red_relaxed_add(cnt + (size_t)(ci + c) * CSTRIDE, 1);
+      }
+      return;
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     epi_sync();
     if (et == PUB_ET) {
@@ -1342,7 +1365,12 @@ struct Epi : CfgFlags<SPEC> {
     // and R_0's weight-free layer-0 cell go first, before the weight traffic),
     // except I_1, the first MMA after the decision, which loads before it
     const bool has_w = role != ROLE_E && !(role == ROLE_I && layer == 0);
-    if (has_w && (WEAGER || (role == ROLE_I && layer == 1) || (role == ROLE_R && layer == 0 && !r0m))) load_weights();
+    if (has_w && (WEAGER || P.pdl || (role == ROLE_I && layer == 1) || (role == ROLE_R && layer == 0 && !r0m)))
+      load_weights();
+    // a programmatic-dependent step launch started while the previous one was
+    // finishing: everything above only touched the weights; the decode state
+    // (control blocks, counters, words, activations) after the primary grid
+    if (P.pdl) pdl_wait();
     if (mode != STEP_ONE) {  // (shared memory is not zeroed at launch: no stale running flags)
       for (int i = et; i < GS_N * MAXG; i += NEPI) sm.grp[i] = 0;
       epi_sync();
@@ -1538,6 +1566,22 @@ struct Epi : CfgFlags<SPEC> {
     }
     __syncwarp();
     if (c0) mark(21);
+    if (PUB_DIRECT) {  // see publish_chunks: 256 x 16-byte plain stores, release, counter
+      epi_sync();
+      const int Kp = P.act_kc[l] * 64;
+      if (et < 256) {
+        const int r = et >> 2, sg = et & 3;
+        const uint4 v = reinterpret_cast<const uint4*>(st16)[et];
+        *reinterpret_cast<uint4*>(P.act[l] + (((size_t)(2 * g + (pe & 1)) * 64 + r) * Kp + 32 * tile + 8 * sg) * 2) = v;
+      }
+      epi_sync();
+      if (et == 0) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("fence.release.gpu;" ::: "memory");
+        red_relaxed_add(cnt + (size_t)cidx_act(l, (32 * tile) >> 6) * CSTRIDE, 1);
+      }
+      return;
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     epi_sync();
     if (et == PUB_ET) {
@@ -1889,6 +1933,7 @@ __device__ __forceinline__ void mma_round(const TParams& P, const Smem& sm, uint
 template <bool TR, int SPEC>
 __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constant__ TParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
+  if (P.pdl) pdl_trigger();  // the next step launch may start its prologue on the free SMs
   unsigned long long t_entry = 0;
   if (STAMPS && threadIdx.x == 64) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
   const int4 rl = P.roles[blockIdx.x];
@@ -1931,13 +1976,19 @@ __global__ void __launch_bounds__(LB_THREADS, 1) ptc_kernel(const __grid_constan
 #ifndef XP_NOWLO
 #define XP_NOWLO 0  // timing experiments only (wrong results): skip the smem weight copy
 #endif
+#ifndef WCOPY_ALL
+#define WCOPY_ALL 0  // A/B: copy the TMEM-resident chunks' W_lo into smem too (round-2 layout)
+#endif
 #ifndef XP_NOWHI
 #define XP_NOWHI 0  // timing experiments only: skip the TMEM weight load
 #endif
   if (tid == 0) {
-    const uint32_t bytes = XP_NOWLO ? 0u : (uint32_t)KC * 16384;
-    mbar_arrive_expect_tx(sm.wbar, bytes);
-    for (uint32_t o = 0; o < bytes; o += 32768)
+    // the first nlo_chunks(KC) chunks' W_lo is TMEM-resident (loaded by the
+    // epilogue): only the rest of the image goes to smem
+    const uint32_t o0 = KC && !WCOPY_ALL ? (uint32_t)nlo_chunks(KC) * 16384 : 0u;
+    const uint32_t bytes = XP_NOWLO ? o0 : (uint32_t)KC * 16384;
+    mbar_arrive_expect_tx(sm.wbar, bytes - o0);
+    for (uint32_t o = o0; o < bytes; o += 32768)
       bulk_g2s(sm.whi + o, wimg + o, bytes - o < 32768 ? bytes - o : 32768, sm.wbar);
   }
 

@@ -758,6 +758,8 @@ rnntg_status setup_tc(rnntg_decoder* d, bool allow_inst = true) {
   tp.ctrl = d->st.ctrl;
   for (int r = 0; r < ptc::NROLES; ++r) tp.prof_first[r] = -1;
   for (int c = G - 1; c >= 0; --c) tp.prof_first[roles[c].x] = c;
+  for (int c = 0; c < G; ++c)  // the traced I CTA: the first one with an MMA (layer 1)
+    if (roles[c].x == ptc::ROLE_I && (roles[c].y & 0xff) == 1) { tp.prof_first[ptc::ROLE_I] = c; break; }
   if (env_flag("RNNTG_STAMPS", false)) CK(d->mem.alloc(&tp.stamps, (size_t)64 * G * 16));
   if (env_flag("RNNTG_PROF", false)) {
     CK(d->mem.alloc(&tp.prof, (size_t)(2 * ptc::NEV + G) * ptc::PROF_WIN));
@@ -776,8 +778,7 @@ cudaError_t launch_tc(rnntg_decoder* d, cudaStream_t st) {
   void* args[1] = {&d->tp};
   // the traced instantiation only when the event trace is on (RNNTG_PROF)
   const void* k = tc_kernel_for(d->tp.algo, d->tp.cell, d->tp.prof != nullptr);
-  return cudaLaunchCooperativeKernel(k, dim3(d->tp.G), dim3(ptc::NTH), args,
-                                     d->tsmem, st);
+  return cudaLaunchCooperativeKernel(k, dim3(d->tp.G), dim3(ptc::NTH), args, d->tsmem, st);
 }
 
 // ---------------------------------------------------------------- K6 step launches
@@ -797,13 +798,14 @@ rnntg_status setup_tc_steps(rnntg_decoder* d, bool use_cond) {
     d->tp_step[i] = tp;
     d->tp_step[i].step_mode = i == 0 ? ptc::STEP_INIT : ptc::STEP_ONE;
     d->tp_step[i].use_cond = use_cond ? 1 : 0;
-    // graph bodies run up to RNNTG_GRAPH_STEPS (default 3) decisions per
+    // graph bodies run up to RNNTG_GRAPH_STEPS (default 8) decisions per
     // launch -- the WHILE body unrolled, amortising the per-launch weight
     // reload and the conditional-node relaunch (~5 us) over the decisions;
     // the sync-requiring host loop stays at one decision (and one flag
     // read-back) per launch
     const char* gs = getenv("RNNTG_GRAPH_STEPS");
-    d->tp_step[i].steps_per_launch = use_cond ? std::max(1, gs ? atoi(gs) : 3) : 1;
+    d->tp_step[i].steps_per_launch = use_cond ? std::max(1, gs ? atoi(gs) : 8) : 1;
+    d->tp_step[i].pdl = use_cond && env_flag("RNNTG_GRAPH_PDL", false) ? 1 : 0;
   }
   d->tc_steps = true;
   return RNNTG_OK;
@@ -866,9 +868,18 @@ cudaError_t build_graph_tc(rnntg_decoder* d) {
   if ((e = coop_node(ob.last)) != cudaSuccess) return e;
   if ((e = ob.while_node(hi, &inner_body)) != cudaSuccess) return e;
   Builder ib{inner_body};
-  ib.pdl = false;
-  if ((e = ib.kernel(k, grid, block, d->tsmem, a_step)) != cudaSuccess) return e;
-  if ((e = coop_node(ib.last)) != cudaSuccess) return e;
+  if (d->tp_step[1].pdl) {
+    // two step launches per inner iteration, the second a programmatic
+    // dependent of the first (its CTAs load their weights while the first
+    // finishes); plain kernel nodes (PDL + cooperative do not mix)
+    ib.pdl = true;
+    if ((e = ib.kernel(k, grid, block, d->tsmem, a_step)) != cudaSuccess) return e;
+    if ((e = ib.kernel(k, grid, block, d->tsmem, a_step)) != cudaSuccess) return e;
+  } else {
+    ib.pdl = false;
+    if ((e = ib.kernel(k, grid, block, d->tsmem, a_step)) != cudaSuccess) return e;
+    if ((e = coop_node(ib.last)) != cudaSuccess) return e;
+  }
   return cudaGraphInstantiate(&d->gexec, d->graph, 0);
 }
 

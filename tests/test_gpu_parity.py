@@ -403,12 +403,12 @@ def test_bind_device_lengths_checked_on_device():
     m.close()
 
 
-@pytest.mark.parametrize("steps", [1, 2])
+@pytest.mark.parametrize("steps", [1, 3])
 @pytest.mark.parametrize("algo", [DecodeAlgo.FrameSync, DecodeAlgo.LabelLoop, DecodeAlgo.TdtLabelLoop],
                          ids=lambda a: a.name)
 def test_graph_decisions_per_launch(steps, algo):
-    """The graph executor's WHILE body with 1 and 2 decisions per kernel-node
-    launch (RNNTG_GRAPH_STEPS; the default 3 is covered by the other suites),
+    """The graph executor's WHILE body with 1 and 3 decisions per kernel-node
+    launch (RNNTG_GRAPH_STEPS; the default 8 is covered by the other suites),
     one and two row groups, against the oracle."""
     _need_gpu()
     tdt = algo == DecodeAlgo.TdtLabelLoop
