@@ -950,6 +950,14 @@ struct Epi : CfgFlags<SPEC> {
   __device__ void joint_round() {
     mark(0);
     post((int)s);
+    // the slot-reuse check's ack loads go out before the accumulator wait
+    // (their L2 round trip overlaps the MMA; evaluated below)
+    const bool ack_due = s >= NSLOT / 2 && s % (NSLOT / 2) == 0;
+    unsigned ack_mn = 0xffffffffu;
+    if (ack_due && et < 32) {
+      const unsigned* ack = P.ack + (size_t)g * P.G;
+      for (int c = P.ic0[inst] + et; c < P.ic0[inst + 1]; c += 32) ack_mn = min(ack_mn, ld_relaxed(ack + c));
+    }
     float v[NR];
     read_acc(round - 1, v);
     mark(1);
@@ -965,14 +973,13 @@ struct Epi : CfgFlags<SPEC> {
     // s - NSLOT .. s - NSLOT/2 - 1, so EVERY CTA (not their sum: an off-path
     // role such as the emitter may lag) must have acked step s - NSLOT/2.
     // Checked once per half window on the per-CTA ack words (min over CTAs).
-    if (s >= NSLOT / 2 && s % (NSLOT / 2) == 0) {
+    if (ack_due) {
       if (et < 32) {
         const unsigned target = (unsigned)(s - NSLOT / 2 + 1);
         const unsigned* ack = P.ack + (size_t)g * P.G;
-        for (;;) {
-          unsigned mn = 0xffffffffu;
-          for (int c = P.ic0[inst] + et; c < P.ic0[inst + 1]; c += 32) mn = min(mn, ld_relaxed(ack + c));
-          if (__reduce_min_sync(0xffffffffu, mn) >= target) break;
+        while (__reduce_min_sync(0xffffffffu, ack_mn) < target) {
+          ack_mn = 0xffffffffu;
+          for (int c = P.ic0[inst] + et; c < P.ic0[inst + 1]; c += 32) ack_mn = min(ack_mn, ld_relaxed(ack + c));
         }
       }
       epi_sync();
