@@ -120,8 +120,14 @@ class ClockSampler:
                  "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
+            # the first sample arrives ~0.1-0.5 s after the query starts: wait for
+            # it so a short timed region is still covered by the 100 ms stream
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < 5.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+        self.n_pre = len(self.samples)
         return self
 
     def _read(self):
@@ -143,6 +149,12 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        note = None
+        if len(self.samples) > self.n_pre:
+            self.samples = self.samples[self.n_pre:]  # the samples taken inside the timed region
+        else:  # region shorter than the sampling period: the sample at its start
+            self.samples = self.samples[-1:]
+            note = "timed region shorter than the 100 ms sampling period: the sample taken as it started"
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -153,7 +165,7 @@ class ClockSampler:
                     reasons.add(n)
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.samples)}
+                "samples": len(self.samples), **({"note": note} if note else {})}
 
 
 def cpu_reference_sample(cfg, seconds_target, threads=None, blank_bias=0.0):
