@@ -430,3 +430,35 @@ def test_graph_decisions_per_launch(steps, algo):
             m.close()
     finally:
         os.environ.pop("RNNTG_GRAPH_STEPS", None)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo", [DecodeAlgo.FrameSync, DecodeAlgo.LabelLoop, DecodeAlgo.TdtLabelLoop],
+                         ids=lambda a: a.name)
+def test_graph_programmatic_dependent_body(algo):
+    """RNNTG_GRAPH_PDL=1: the inner WHILE body as two step launches, the
+    second a programmatic dependent of the first (prologue before
+    griddepcontrol.wait), one and two row groups, against the oracle."""
+    _need_gpu()
+    tdt = algo == DecodeAlgo.TdtLabelLoop
+    d = O.Dims(150, 64, 64, 96, 24, (0, 1, 2, 3, 4) if tdt else (), O.CELL_LSTM, 2)
+    p = O.init_params(53, d)
+    T, ms = 12, 3
+    os.environ["RNNTG_GRAPH_PDL"] = "1"
+    os.environ["RNNTG_GRAPH_STEPS"] = "2"
+    try:
+        for B in (7, 45):
+            x = O.fill_uniform(54, -1.0, 1.0, (B, T, d.feature))
+            lens = np.array([T - (3 * i) % 7 for i in range(B)], np.int32)
+            m = Model(to_model_dims(d), p)
+            cap = D.build_decode_graph(m, algo, B, T, ms, D.Exec.Graph)
+            got = D.replay_decode(cap, x, lens)
+            got2 = D.replay_decode(cap, x, lens)
+            rep = compare_batch(got, O.decode_batch(d, p, x, lens, ms, tdt, record=True), d.vocab, tdt, f"PDL/B{B}")
+            assert rep.ok, rep.failures[:5]
+            assert [h.tokens for h in got2] == [h.tokens for h in got]
+            cap.close()
+            m.close()
+    finally:
+        os.environ.pop("RNNTG_GRAPH_PDL", None)
+        os.environ.pop("RNNTG_GRAPH_STEPS", None)
