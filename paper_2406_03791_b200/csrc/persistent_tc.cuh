@@ -488,6 +488,9 @@ __device__ __forceinline__ void release_after_bulk() {
   if (MM_PROD == 1 || MM_PROD == 3) asm volatile("fence.acq_rel.gpu;" ::: "memory");
   if (MM_PROD == 4) asm volatile("fence.release.gpu;" ::: "memory");
 }
+#ifndef XP_NOREL
+#define XP_NOREL 0  // timing experiments only (unsound; with -DMM_CONS=0): no release fence on the activation publishes
+#endif
 #ifndef PUB_DIRECT
 #define PUB_DIRECT 1  // activation hand-offs: plain stores + release (0: TMA store + wait_group + release)
 #endif
@@ -907,7 +910,7 @@ struct Epi : CfgFlags<SPEC> {
       epi_sync();
       if (et == 0) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        asm volatile("fence.release.gpu;" ::: "memory");
+        if (!XP_NOREL) asm volatile("fence.release.gpu;" ::: "memory");
         for (int c = 0; c < n; ++c) red_relaxed_add(cnt + (size_t)(ci + c) * CSTRIDE, 1);
       }
       return;
@@ -1584,7 +1587,7 @@ struct Epi : CfgFlags<SPEC> {
       epi_sync();
       if (et == 0) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        asm volatile("fence.release.gpu;" ::: "memory");
+        if (!XP_NOREL) asm volatile("fence.release.gpu;" ::: "memory");
         red_relaxed_add(cnt + (size_t)cidx_act(l, (32 * tile) >> 6) * CSTRIDE, 1);
       }
       return;
