@@ -272,7 +272,7 @@ def run_reference_arm(args, cfg, rank, world):
     print(json.dumps(out), flush=True)
 
 
-def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent, step_ms=None):
+def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent, step_ms=None, step_launches=None):
     """Dominant kernel's achieved bandwidth / FLOP rate, measured with CUDA
     events on standalone launches of the decoder's own kernels (step_ms: the
     tcgen05 step kernel's mean launch time from the CUPTI trace, for the graph
@@ -307,8 +307,12 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent, step
     V1 = V + 1
     V1p = (V1 + 15) // 16 * 16
     Dn = len(durs)
-    # algorithmic weight bytes of one prediction step / one joint step (fp32)
-    pred_w = 4 * (H * 4 * H * (2 * L - 1) + 4 * H * L + H * J)
+    # algorithmic weight bytes of one prediction step / one joint step (fp32),
+    # every LSTM layer's W_ih and W_hh (layer 0's input is the
+    # embedding, E = H in every BASELINE config), biases, pred_proj; the joint's
+    # out_proj (+ dur_proj). (K6 reads a table0 row per label instead of
+    # multiplying emb @ W_ih0 -- the figure follows the reference's algorithm.)
+    pred_w = 4 * (H * 4 * H * 2 * L + 4 * H * L + H * J)
     joint_w = 4 * J * (V1 + Dn)
     bytes_per = {  # algorithmic bytes per launch (weights + activations read + outputs written)
         "pred_layer1": 4 * (2 * Hp * 4 * Hp + Bp * 2 * Hp + 2 * Bp * Hp * 2),
@@ -317,20 +321,22 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent, step
         "joint": 4 * (Jp * V1p + 2 * Bp * Jp),
         "enc_proj": 4 * (Bl * T * F + F * Jp + Bl * T * Jp),
         "persistent": (st.pred_steps * pred_w + st.joint_evals * joint_w) / n_sub / ngrp,
-        "ptc_step": (st.pred_steps * pred_w + st.joint_evals * joint_w) / max(st.joint_evals, 1),
+        # (a step launch runs up to RNNTG_GRAPH_STEPS decisions: the decode's
+        # bytes over its step launches)
+        "ptc_step": (st.pred_steps * pred_w + st.joint_evals * joint_w) / max(step_launches or st.joint_evals, 1),
     }
-    pred_f = 2 * Brow * (4 * H * H * (2 * L - 1) + H * J)
+    pred_f = 2 * Brow * (4 * H * H * 2 * L + H * J)
     joint_f = 2 * Brow * J * (V1 + Dn)
     flops_per = {
         "pred_layer1": 2 * Bl * 2 * H * 4 * H, "pred_layer0": 2 * Bl * H * 4 * H,
         "pred_proj": 2 * Bl * H * J, "joint": 2 * Bl * J * V1, "enc_proj": 2 * Bl * T * F * J,
         "persistent": (st.pred_steps * pred_f + st.joint_evals * joint_f) / n_sub,
-        "ptc_step": (st.pred_steps * pred_f + st.joint_evals * joint_f) / max(st.joint_evals, 1),
+        "ptc_step": (st.pred_steps * pred_f + st.joint_evals * joint_f) / max(step_launches or st.joint_evals, 1),
     }
     per_step_counts = {"enc_proj": 1, "pred_layer0": st.pred_steps,
                        "pred_layer1": st.pred_steps if L > 1 else 0,
                        "pred_proj": st.pred_steps, "joint": st.joint_evals, "persistent": n_sub,
-                       "ptc_step": st.joint_evals}
+                       "ptc_step": step_launches or st.joint_evals}
     share = {n: kern[n] * per_step_counts[n] / ms_per_step for n in kern}
     dom = max(share, key=share.get)
     peaks = {}
@@ -380,6 +386,8 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent, step
             "traffic_source": f"profiles/{tsrc} (ncu --set full, C2)" if traffic else None,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)",
             "algorithmic_bytes_per_launch": bytes_per[dom],
+            "algorithmic_bytes_source": "SURVEY.md 8(d) weight bytes per prediction / joint step "
+                                        "(C2: 30.497 MB per inner step) x the launch's steps",
             "avg_launch_us": kern[dom] * 1000.0,
             "launches_per_step": per_step_counts[dom],
             "fp32": {"achieved_tflops": fp32_ach, "peak_tflops": fp32_peak,
@@ -651,10 +659,11 @@ def main():
         launches_per_step = 2 + st.pred_steps * (L + 1) + st.joint_evals + (st.outer_iters if fs else 0)
     hyps_dev = read_hyps(L_, dh, Bl)  # the timed decodes' hypotheses (device-resident inputs)
     idle = measure_idle(L_, dh, ms_per_step)
-    step_ms = None
+    step_ms = step_launches = None
     if tc_steps and idle and idle.get("kernels", 0) > 2:
         step_ms = (idle["busy_ms"] - 0.0) / idle["kernels"]
-    roofline, clk = roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent, step_ms)
+        step_launches = idle["kernels"] - 2  # (K1 and the P0 launch are the other two)
+    roofline, clk = roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent, step_ms, step_launches)
 
     # ---- e2e through the C ABI with host buffers ----
     e2e = None
