@@ -653,7 +653,7 @@ def main():
     if persistent:
         launches_per_step = 2
     elif tc_steps:  # K1 + P0 + one launch per (up to RNNTG_GRAPH_STEPS) decisions
-        k = int(os.environ.get("RNNTG_GRAPH_STEPS", "8")) if args.exec == "graph" else 1
+        k = int(os.environ.get("RNNTG_GRAPH_STEPS", "16")) if args.exec == "graph" else 1
         launches_per_step = 2 + -(-st.joint_evals // max(k, 1))
     else:
         launches_per_step = 2 + st.pred_steps * (L + 1) + st.joint_evals + (st.outer_iters if fs else 0)

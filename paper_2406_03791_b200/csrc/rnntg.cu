@@ -798,13 +798,13 @@ rnntg_status setup_tc_steps(rnntg_decoder* d, bool use_cond) {
     d->tp_step[i] = tp;
     d->tp_step[i].step_mode = i == 0 ? ptc::STEP_INIT : ptc::STEP_ONE;
     d->tp_step[i].use_cond = use_cond ? 1 : 0;
-    // graph bodies run up to RNNTG_GRAPH_STEPS (default 8) decisions per
+    // graph bodies run up to RNNTG_GRAPH_STEPS (default 16) decisions per
     // launch -- the WHILE body unrolled, amortising the per-launch weight
     // reload and the conditional-node relaunch (~5 us) over the decisions;
     // the sync-requiring host loop stays at one decision (and one flag
     // read-back) per launch
     const char* gs = getenv("RNNTG_GRAPH_STEPS");
-    d->tp_step[i].steps_per_launch = use_cond ? std::max(1, gs ? atoi(gs) : 8) : 1;
+    d->tp_step[i].steps_per_launch = use_cond ? std::max(1, gs ? atoi(gs) : 16) : 1;
     d->tp_step[i].pdl = use_cond && env_flag("RNNTG_GRAPH_PDL", false) ? 1 : 0;
   }
   d->tc_steps = true;

@@ -408,7 +408,7 @@ def test_bind_device_lengths_checked_on_device():
                          ids=lambda a: a.name)
 def test_graph_decisions_per_launch(steps, algo):
     """The graph executor's WHILE body with 1 and 3 decisions per kernel-node
-    launch (RNNTG_GRAPH_STEPS; the default 8 is covered by the other suites),
+    launch (RNNTG_GRAPH_STEPS; the default 16 is covered by the other suites),
     one and two row groups, against the oracle."""
     _need_gpu()
     tdt = algo == DecodeAlgo.TdtLabelLoop
