@@ -272,6 +272,17 @@ def run_reference_arm(args, cfg, rank, world):
     print(json.dumps(out), flush=True)
 
 
+def step_weight_bytes(cfg):
+    """Algorithmic fp32 weight bytes of one prediction step and of one joint
+    step: every LSTM layer's W_ih and W_hh (layer 0's input
+    is the embedding, E = H in every BASELINE config), the biases, pred_proj;
+    the joint's out_proj (+ dur_proj).  K6 reads a table0 row per label
+    instead of multiplying emb @ W_ih0; the figure follows the reference's
+    algorithm.  C2: 27.87 + 2.62 = 30.497 MB per inner step."""
+    algo, B, T, ms, durs, L, H, J, V, F, scaling = cfg
+    return 4 * (H * 4 * H * 2 * L + 4 * H * L + H * J), 4 * J * (V + 1 + len(durs))
+
+
 def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent, step_ms=None, step_launches=None):
     """Dominant kernel's achieved bandwidth / FLOP rate, measured with CUDA
     events on standalone launches of the decoder's own kernels (step_ms: the
@@ -307,13 +318,7 @@ def roofline_block(args, L_, dh, st, cfg, Bl, ms_per_step, clk, persistent, step
     V1 = V + 1
     V1p = (V1 + 15) // 16 * 16
     Dn = len(durs)
-    # algorithmic weight bytes of one prediction step / one joint step (fp32),
-    # every LSTM layer's W_ih and W_hh (layer 0's input is the
-    # embedding, E = H in every BASELINE config), biases, pred_proj; the joint's
-    # out_proj (+ dur_proj). (K6 reads a table0 row per label instead of
-    # multiplying emb @ W_ih0 -- the figure follows the reference's algorithm.)
-    pred_w = 4 * (H * 4 * H * 2 * L + 4 * H * L + H * J)
-    joint_w = 4 * J * (V1 + Dn)
+    pred_w, joint_w = step_weight_bytes(cfg)
     bytes_per = {  # algorithmic bytes per launch (weights + activations read + outputs written)
         "pred_layer1": 4 * (2 * Hp * 4 * Hp + Bp * 2 * Hp + 2 * Bp * Hp * 2),
         "pred_layer0": 4 * (Hp * 4 * Hp + Bp * Hp + 2 * Bp * Hp * 2 + Bp * 4 * Hp),

@@ -27,3 +27,13 @@ def test_reference_arm_line():
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert line["parity"]["checked"] and not line["parity"]["mismatched"]
+
+
+@pytest.mark.parametrize("name,mb", [("c1", 3.857), ("c2", 30.497), ("c3", 30.497), ("c4", 30.510)])
+def test_roofline_bytes_follow_survey(name, mb):
+    """The roofline's algorithmic bytes per inner step (one prediction step +
+    one joint step) are SURVEY.md 8(d)'s figures."""
+    sys.path.insert(0, ROOT)
+    import bench
+    pred_w, joint_w = bench.step_weight_bytes(bench.CONFIGS[name])
+    assert abs((pred_w + joint_w) / 1e6 - mb) < 0.0006, (name, pred_w + joint_w)
